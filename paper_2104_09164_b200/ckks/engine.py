@@ -1,0 +1,572 @@
+"""Leveled RNS-CKKS engine on the B200 -- drop-in for hear/ckks/engine.py.
+
+Same parameter objects, same keygen / enc / evaluate / dec contract, same
+randomness: every random polynomial is drawn from the host numpy generator in
+exactly the reference's call order (engine.py:77-147, 194-211), so with equal
+seeds the secret, public, relinearisation and rotation keys and every fresh
+ciphertext are bit-identical to the reference's.  All arithmetic after the
+draw runs in the CUDA kernels of csrc/ (NTT, ModUp/ModDown base conversion,
+key-switch inner product with the Galois gather, rescale, codec).
+
+Ciphertext payloads are `CtData`: one int64 tensor [B, 2, level+1, N] holding
+B independent clips (rows ascending from q0, NTT form).  B = 1 reproduces the
+reference exactly; B > 1 evaluates B clips with the same schedule and the
+same key material in one set of kernel launches.
+
+Key switching follows the reference design (engine.py:288-326): one special
+prime P, per-prime digits (dnum = level+1); ModUp of a digit is the centred
+lift of its residue re-reduced under every target prime, ModDown divides P
+out with the centred special residue.  These are exact integer maps, so the
+GPU results are the same residues the (fixed) reference computes.
+"""
+
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from .. import _native as nat
+from ..backend import BackendBase, Ct, LevelScaleError, Pt
+from .encoder import Embedding
+from .params import ParameterSet
+from .ring import RingContext, shoup_np
+
+
+class MissingRotationKey(RuntimeError):
+    pass
+
+
+class CtData:
+    """Device payload of a (batched) ciphertext: [B, 2, rows, N] int64."""
+
+    __slots__ = ("data",)
+
+    def __init__(self, data: torch.Tensor):
+        self.data = data
+
+    @property
+    def batch(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def rows(self) -> int:
+        return self.data.shape[2]
+
+    def __getitem__(self, i):
+        """payload[0] / payload[1]: c0 / c1 rows (reference tuple access)."""
+        t = self.data[:, i]
+        return t[0] if self.batch == 1 else t
+
+    def to_host(self):
+        """(c0, c1) uint64 numpy arrays shaped like the reference payload."""
+        h = self.data.cpu().numpy().view(np.uint64)
+        if self.batch == 1:
+            return h[0, 0].copy(), h[0, 1].copy()
+        return h[:, 0].copy(), h[:, 1].copy()
+
+
+class _Ksk:
+    __slots__ = ("b", "a", "lmax")
+
+    def __init__(self, b, a, lmax):
+        self.b = b          # [ndig, lmax+2, N] device
+        self.a = a
+        self.lmax = lmax
+
+
+class KeyMaterial:
+    def __init__(self):
+        self.s_coeffs = None
+        self.s_ntt = None   # [L+2, N] device, special row last
+        self.pk_b = None
+        self.pk_a = None
+        self.relin = None
+        self.rot: dict = {}
+
+
+def _tasks(dtype, n, **fields) -> np.ndarray:
+    t = np.zeros(n, dtype=dtype)
+    for k, v in fields.items():
+        t[k] = v
+    return t
+
+
+class CkksBackend(BackendBase):
+    """GPU realisation of the backend contract (hear/ckks/engine.py:48)."""
+
+    exact = False
+
+    def __init__(self, params: ParameterSet, seed: int = 0, device=None):
+        super().__init__(params)
+        self.ring = RingContext(params, device)
+        self.dev = self.ring.device
+        self.emb = Embedding(params.n, self.dev)
+        self.rng = np.random.default_rng(seed)
+        self.n = params.n
+        self.L = params.max_level
+        self.S = self.ring.special_idx
+        self.P = params.special_prime
+        chain = params.chain_primes
+        self._pmod = np.array([self.P % q for q in chain], dtype=np.uint64)
+        self._pinv = np.array([pow(self.P, -1, q) for q in chain], dtype=np.uint64)
+        self._pmod_sh = shoup_np(self._pmod, np.array(chain, dtype=np.uint64))
+        self._pinv_sh = shoup_np(self._pinv, np.array(chain, dtype=np.uint64))
+        # rescale constants: inv[l][j] = q_l^-1 mod q_j (engine.py:67-71)
+        self._resc = []
+        for lvl in range(self.L + 1):
+            inv = np.array([pow(chain[lvl], -1, chain[j]) for j in range(lvl)], dtype=np.uint64)
+            ps = np.array(chain[:lvl], dtype=np.uint64)
+            self._resc.append((inv, shoup_np(inv, ps) if lvl else inv))
+        self._crt_cache: dict = {}
+        self.keys = KeyMaterial()
+        self._keygen()
+
+    # ------------------------------------------------------------------ sampling
+
+    def _ternary(self) -> np.ndarray:
+        return self.rng.integers(-1, 2, self.n).astype(np.int64)
+
+    def _gauss(self) -> np.ndarray:
+        return np.rint(self.rng.normal(0.0, self.params.error_std, self.n)).astype(np.int64)
+
+    def _uniform_rows(self, gidx) -> np.ndarray:
+        out = np.empty((len(gidx), self.n), dtype=np.uint64)
+        for r, g in enumerate(gidx):
+            out[r] = self.rng.integers(0, self.ring.primes[g], self.n, dtype=np.uint64)
+        return out
+
+    def _full_gidx(self, lmax=None) -> list:
+        lmax = self.L if lmax is None else lmax
+        return list(range(lmax + 1)) + [self.S]
+
+    def _dev(self, arr: np.ndarray) -> torch.Tensor:
+        a = np.ascontiguousarray(arr)
+        if a.dtype == np.uint64:
+            a = a.view(np.int64)
+        return torch.from_numpy(a).to(self.dev)
+
+    # ------------------------------------------------------------------ kernels
+
+    def _coeffs_to_ntt(self, coeffs: torch.Tensor, gidx) -> torch.Tensor:
+        """Signed int64 coefficients [M, N] -> NTT rows [M, len(gidx), N]."""
+        coeffs = coeffs.contiguous()
+        m, r = coeffs.shape[0], len(gidx)
+        out = self.ring.empty(m, r)
+        src = np.repeat(self.ring.row_ptrs(coeffs), r)
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * r, src=src, dst=self.ring.row_ptrs(out),
+                                 dst_prime=np.tile(np.asarray(gidx), m),
+                                 src_prime=np.tile(np.asarray(gidx), m)), nat.FWD_I64)
+        return out
+
+    def _ew(self, op, dst, a, b=None, c=None, primes=None, scal=None, scal_sh=None):
+        """Element-wise op over matching row lists (pointer arrays)."""
+        n = len(dst)
+        f = dict(dst=dst, a=a, prime=primes)
+        if b is not None:
+            f["b"] = b
+        if c is not None:
+            f["c"] = c
+        if scal is not None:
+            f["scal"], f["scal_sh"] = scal, scal_sh
+        self.ring.ew(op, _tasks(nat.EW_TASK, n, **f))
+
+    def _row_primes(self, batch_shape: int, rows: int, gidx=None) -> np.ndarray:
+        g = np.arange(rows) if gidx is None else np.asarray(gidx)
+        return np.tile(g, batch_shape)
+
+    def _intt_rows(self, src: torch.Tensor, primes: np.ndarray) -> torch.Tensor:
+        out = torch.empty_like(src)
+        n = src.numel() // self.n
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, n, src=self.ring.row_ptrs(src),
+                                 dst=self.ring.row_ptrs(out), dst_prime=primes, src_prime=primes))
+        return out
+
+    def _moddown_into(self, out: torch.Tensor, src_coef_ptrs, src_prime, aux: torch.Tensor,
+                      scal, scal_sh, add_ptrs=None, perm_ptr=0):
+        """out[..., r, :] = (aux[..., r, :] - lift(src) mod p_r) * scal_r (+ add).
+
+        out/aux: [M, R, N]; src_coef_ptrs: [M] coefficient rows mod src_prime."""
+        m, r = out.shape[0], out.shape[1]
+        f = dict(src=np.repeat(src_coef_ptrs, r), dst=self.ring.row_ptrs(out),
+                 aux=self.ring.row_ptrs(aux), src_prime=np.repeat(np.asarray(src_prime), r)
+                 if np.ndim(src_prime) else src_prime,
+                 dst_prime=np.tile(np.arange(r), m), scal=np.tile(scal, m),
+                 scal_sh=np.tile(scal_sh, m))
+        if add_ptrs is not None:
+            f["add"] = add_ptrs
+            f["perm"] = perm_ptr
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * r, **f), nat.FWD_MODDOWN)
+
+    # ------------------------------------------------------------------ keygen
+
+    def _keygen(self):
+        k = self.keys
+        gidx = self._full_gidx()
+        k.s_coeffs = self._ternary()
+        k.s_ntt = self._coeffs_to_ntt(self._dev(k.s_coeffs)[None], gidx)[0]
+        k.pk_a = self._dev(self._uniform_rows(gidx))
+        e = self._coeffs_to_ntt(self._dev(self._gauss())[None], gidx)[0]
+        k.pk_b = self._sub_prod(e, k.pk_a, k.s_ntt, gidx)
+        s2 = self.ring.empty(len(gidx))
+        rp = self.ring.row_ptrs
+        self._ew(nat.EW_MUL, rp(s2), rp(k.s_ntt), rp(k.s_ntt), primes=np.array(gidx))
+        k.relin = self._make_ksk(s2, self.L)
+
+    def _sub_prod(self, e, a, s, gidx):
+        """e - a*s over rows (keygen b-component)."""
+        rp = self.ring.row_ptrs
+        t = torch.empty_like(a)
+        self._ew(nat.EW_MUL, rp(t), rp(a), rp(s), primes=np.array(gidx))
+        out = torch.empty_like(a)
+        self._ew(nat.EW_SUB, rp(out), rp(e), rp(t), primes=np.array(gidx))
+        return out
+
+    def _make_ksk(self, target_ntt: torch.Tensor, lmax: int) -> _Ksk:
+        """Key encrypting P*target under s, one component per digit prime
+        (engine.py:112-132)."""
+        gidx = self._full_gidx(lmax)
+        rows, ndig = len(gidx), lmax + 1
+        s = self.keys.s_ntt[list(range(lmax + 1)) + [self.L + 1]].contiguous()
+        kb = self.ring.empty(ndig, rows)
+        ka = self.ring.empty(ndig, rows)
+        rp = self.ring.row_ptrs
+        for i in range(ndig):
+            a = self._dev(self._uniform_rows(gidx))
+            e = self._coeffs_to_ntt(self._dev(self._gauss())[None], gidx)[0]
+            ka[i].copy_(a)
+            kb[i].copy_(self._sub_prod(e, a, s, gidx))
+            # digit i's component carries P*target on its own prime row only
+            self._ew(nat.EW_ADD_SCALED, rp(kb[i, i:i + 1]), rp(kb[i, i:i + 1]),
+                     rp(target_ntt[i:i + 1]), primes=np.array([i]),
+                     scal=self._pmod[i:i + 1], scal_sh=self._pmod_sh[i:i + 1])
+        return _Ksk(kb, ka, lmax)
+
+    def ensure_rotation_keys(self, rot_levels: dict):
+        """Keys for {amount: max evaluation level} (engine.py:134-147)."""
+        for amount, lmax in sorted(rot_levels.items()):
+            amount %= self.n2
+            if amount == 0:
+                continue
+            have = self.keys.rot.get(amount)
+            if have is not None and have.lmax >= lmax:
+                continue
+            g = self.ring.galois_element(amount)
+            sg = self.ring.coeff_automorphism(self.keys.s_coeffs, g)
+            target = self._coeffs_to_ntt(self._dev(sg)[None], self._full_gidx(lmax))[0]
+            self.keys.rot[amount] = self._make_ksk(target, lmax)
+
+    # ------------------------------------------------------------------ codec
+
+    def _encode_rows(self, values: torch.Tensor, level: int, scale) -> torch.Tensor:
+        coeffs = self.emb.encode_coeffs(values, float(scale))
+        return self._coeffs_to_ntt(coeffs, list(range(level + 1)))
+
+    def _raw_encode(self, values, level, scale) -> Pt:
+        rows = self._encode_rows(torch.as_tensor(values, dtype=torch.float64)[None], level, scale)
+        return Pt(rows[0], level, scale, self.n2)
+
+    def encode_many(self, values: np.ndarray, level: int, scale) -> list:
+        """Encode M plaintext vectors (M, N/2) at one (level, scale) in one
+        launch sequence.  Same values as M encode() calls."""
+        values = np.asarray(values, dtype=np.float64)
+        if values.ndim != 2 or values.shape[1] != self.n2:
+            raise ValueError(f"plaintexts must have {self.n2} slots")
+        scale = Fraction(scale)
+        rows = self._encode_rows(torch.from_numpy(values), level, scale)
+        return [Pt(rows[i], level, scale, self.n2) for i in range(rows.shape[0])]
+
+    def _rows_needed(self, scale) -> int:
+        """Chain prefix that holds value*scale + noise (engine.py:177-185)."""
+        need = max(np.log2(float(scale)), 0.0) + 40
+        bits = 0.0
+        for k, p in enumerate(self.params.chain_primes):
+            bits += np.log2(p)
+            if bits >= need:
+                return k + 1
+        return self.L + 1
+
+    def _crt_consts(self, keep: int):
+        if keep not in self._crt_cache:
+            primes = list(self.params.chain_primes[:keep])
+            Q = 1
+            for p in primes:
+                Q *= p
+            nl = (Q.bit_length() + 63) // 64
+
+            def limbs(x):
+                return [(x >> (64 * i)) & ((1 << 64) - 1) for i in range(nl)]
+
+            qhat = [Q // p for p in primes]
+            words = limbs(Q) + limbs(Q // 2) + [pow(h, -1, p) for h, p in zip(qhat, primes)]
+            for h in qhat:
+                words += limbs(h)
+            c = torch.from_numpy(np.array(words, dtype=np.uint64).view(np.int64)).to(self.dev)
+            idx = torch.arange(keep, dtype=torch.int32, device=self.dev)
+            self._crt_cache[keep] = (c, idx, nl)
+        return self._crt_cache[keep]
+
+    def _decrypt_coeffs(self, ct: Ct, keep: int) -> torch.Tensor:
+        """Centred coefficients of <ct, s> as float64 [B, N] (engine.py:156-175)."""
+        d = ct.payload.data
+        b = d.shape[0]
+        rp = self.ring.row_ptrs
+        m = self.ring.empty(b, keep)
+        c0 = d[:, 0, :keep].contiguous()
+        c1 = d[:, 1, :keep].contiguous()
+        s = self.keys.s_ntt[:keep].contiguous()
+        self._ew(nat.EW_MULADD, rp(m), rp(c1), np.tile(rp(s), b), rp(c0),
+                 primes=self._row_primes(b, keep))
+        coef = self._intt_rows(m, self._row_primes(b, keep))
+        consts, idx, nl = self._crt_consts(keep)
+        out = torch.empty(b, self.n, dtype=torch.float64, device=self.dev)
+        tasks = _tasks(nat.CRT_TASK, b, rows=rp(coef)[::keep],
+                       out=np.uint64(out.data_ptr()) + np.arange(b, dtype=np.uint64)
+                       * np.uint64(8 * self.n))
+        from .ring import _upload
+        td = _upload(tasks, self.dev)
+        nat.check(nat.lib().hb_crt_double(self.ring.handle, td.data_ptr(), b, consts.data_ptr(),
+                                          idx.data_ptr(), keep, nl, self.ring.stream), "crt")
+        return out
+
+    def _raw_dec(self, ct: Ct) -> np.ndarray:
+        keep = min(ct.level + 1, self._rows_needed(ct.scale))
+        coeffs = self._decrypt_coeffs(ct, keep)
+        vals = self.emb.decode_coeffs(coeffs, float(ct.scale)).cpu().numpy()
+        return vals[0] if ct.payload.batch == 1 else vals
+
+    # ------------------------------------------------------------------ encryption
+
+    def _raw_enc(self, values, level, scale) -> Ct:
+        """Raised-modulus public-key encryption (engine.py:194-211), batched
+        over the leading axis of `values`; randomness drawn per clip in the
+        reference order (u, e0, e1)."""
+        vals = np.ascontiguousarray(np.atleast_2d(values))
+        coeffs = self.emb.encode_coeffs(torch.from_numpy(vals), float(scale))
+        return self._enc_from_coeffs(coeffs, level, scale)
+
+    def _enc_from_coeffs(self, coeffs: torch.Tensor, level: int, scale) -> Ct:
+        """Encrypt B plaintexts given as signed int64 coefficients [B, N]."""
+        b = coeffs.shape[0]
+        rows = list(range(level + 1))
+        gidx = rows + [self.S]
+        r = len(gidx)
+        m = self._coeffs_to_ntt(coeffs, rows)
+        noise = np.empty((b, 3, self.n), dtype=np.int64)
+        for i in range(b):
+            noise[i, 0] = self._ternary()
+            noise[i, 1] = self._gauss()
+            noise[i, 2] = self._gauss()
+        uee = self._coeffs_to_ntt(self._dev(noise).reshape(3 * b, self.n), gidx).reshape(b, 3, r, self.n)
+        sel = rows + [self.L + 1]
+        pkb = self.keys.pk_b[sel].contiguous()
+        pka = self.keys.pk_a[sel].contiguous()
+        rp = self.ring.row_ptrs
+        ext = self.ring.empty(b, 2, r)
+        er = rp(ext).reshape(b, 2, r)
+        ur = rp(uee).reshape(b, 3, r)
+        prim = self._row_primes(b, r, gidx)
+        # c0 = u*pk_b + e0, c1 = u*pk_a + e1
+        self._ew(nat.EW_MULADD, er[:, 0].ravel(), ur[:, 0].ravel(), np.tile(rp(pkb), b),
+                 ur[:, 1].ravel(), primes=prim)
+        self._ew(nat.EW_MULADD, er[:, 1].ravel(), ur[:, 0].ravel(), np.tile(rp(pka), b),
+                 ur[:, 2].ravel(), primes=prim)
+        # c0[:level+1] += P * m
+        c0rows = er[:, 0, :level + 1].ravel()
+        self._ew(nat.EW_ADD_SCALED, c0rows, c0rows, rp(m), primes=self._row_primes(b, level + 1),
+                 scal=np.tile(self._pmod[:level + 1], b),
+                 scal_sh=np.tile(self._pmod_sh[:level + 1], b))
+        out = self._drop_special(ext, level)
+        return Ct(CtData(out), level, scale, self.n2)
+
+    def _drop_special(self, ext: torch.Tensor, level: int) -> torch.Tensor:
+        """ext [M, 2, level+2, N] (special row last) -> (x - [x]_P)/P on the
+        chain rows, [M, 2, level+1, N] (engine.py:213-227)."""
+        m = ext.shape[0]
+        flat = ext.reshape(m * 2, level + 2, self.n)
+        spc = self._intt_rows(flat[:, level + 1].contiguous(), np.full(m * 2, self.S))
+        out = self.ring.empty(m * 2, level + 1)
+        self._moddown_into(out, self.ring.row_ptrs(spc), self.S, flat[:, :level + 1].contiguous(),
+                           self._pinv[:level + 1], self._pinv_sh[:level + 1])
+        return out.reshape(m, 2, level + 1, self.n)
+
+    # ------------------------------------------------------------------ arithmetic
+
+    def _new(self, b, rows) -> torch.Tensor:
+        return self.ring.empty(b, 2, rows)
+
+    def _raw_add(self, a: Ct, b: Ct) -> Ct:
+        self._check_batch(a, b)
+        x, y = a.payload.data, b.payload.data
+        out = torch.empty_like(x)
+        rp = self.ring.row_ptrs
+        self._ew(nat.EW_ADD, rp(out), rp(x), rp(y),
+                 primes=self._row_primes(x.shape[0] * 2, a.level + 1))
+        return Ct(CtData(out), a.level, a.scale, self.n2)
+
+    def _check_batch(self, a: Ct, b: Ct):
+        if a.payload.batch != b.payload.batch:
+            raise ValueError(f"batch mismatch: {a.payload.batch} vs {b.payload.batch}")
+
+    def _pt_rows(self, p: Pt, level: int) -> torch.Tensor:
+        return p.payload[:level + 1]
+
+    def _raw_add_plain(self, a: Ct, p: Pt) -> Ct:
+        x = a.payload.data
+        bsz, lvl = x.shape[0], a.level
+        out = x.clone()
+        rp = self.ring.row_ptrs
+        prow = rp(p.payload)[:lvl + 1]
+        c0 = rp(out).reshape(bsz, 2, lvl + 1)[:, 0].ravel()
+        self._ew(nat.EW_ADD, c0, c0, np.tile(prow, bsz), primes=self._row_primes(bsz, lvl + 1))
+        return Ct(CtData(out), a.level, a.scale, self.n2)
+
+    def _raw_mult_plain(self, a: Ct, p: Pt) -> Ct:
+        x = a.payload.data
+        bsz, lvl = x.shape[0], a.level
+        out = torch.empty_like(x)
+        rp = self.ring.row_ptrs
+        prow = rp(p.payload)[:lvl + 1]
+        self._ew(nat.EW_MUL, rp(out), rp(x), np.tile(prow, 2 * bsz),
+                 primes=self._row_primes(2 * bsz, lvl + 1))
+        return Ct(CtData(out), a.level, a.scale * p.scale, self.n2)
+
+    def _raw_mult(self, a: Ct, b: Ct) -> Ct:
+        self._check_batch(a, b)
+        lvl = a.level
+        x, y = a.payload.data, b.payload.data
+        bsz = x.shape[0]
+        r = lvl + 1
+        d = self.ring.empty(bsz, 3, r)
+        rp = self.ring.row_ptrs
+        xr, yr, dr = rp(x).reshape(bsz, 2, r), rp(y).reshape(bsz, 2, r), rp(d).reshape(bsz, 3, r)
+        t = _tasks(nat.TENSOR_TASK, bsz * r, a0=xr[:, 0].ravel(), a1=xr[:, 1].ravel(),
+                   b0=yr[:, 0].ravel(), b1=yr[:, 1].ravel(), d0=dr[:, 0].ravel(),
+                   d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
+                   prime=self._row_primes(bsz, r))
+        self.ring.tensor(t)
+        de = self._decompose(d[:, 2].contiguous(), lvl)
+        out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
+        return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
+
+    def _raw_rescale(self, a: Ct) -> Ct:
+        """Exact RNS division by the top prime (engine.py:263-281)."""
+        lvl = a.level
+        x = a.payload.data
+        bsz = x.shape[0]
+        top = x[:, :, lvl].contiguous().reshape(bsz * 2, self.n)
+        topc = self._intt_rows(top, np.full(bsz * 2, lvl))
+        out = self.ring.empty(bsz * 2, lvl)
+        aux = x[:, :, :lvl].contiguous().reshape(bsz * 2, lvl, self.n)
+        inv, inv_sh = self._resc[lvl]
+        self._moddown_into(out, self.ring.row_ptrs(topc), lvl, aux, inv, inv_sh)
+        scale = a.scale / self.params.chain_primes[lvl]
+        return Ct(CtData(out.reshape(bsz, 2, lvl, self.n)), lvl - 1, scale, self.n2)
+
+    def _raw_mod_down(self, a: Ct, to_level: int) -> Ct:
+        out = a.payload.data[:, :, :to_level + 1].contiguous()
+        return Ct(CtData(out), to_level, a.scale, self.n2)
+
+    # ------------------------------------------------------------------ key switching
+
+    def _decompose(self, d: torch.Tensor, lvl: int) -> torch.Tensor:
+        """Digits of d [B, lvl+1, N] extended to chain rows 0..lvl plus the
+        special prime: de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303)."""
+        bsz = d.shape[0]
+        ndig, rows = lvl + 1, lvl + 2
+        coef = self._intt_rows(d.contiguous(), self._row_primes(bsz, ndig))
+        de = self.ring.empty(bsz, ndig, rows)
+        gidx = np.array(list(range(lvl + 1)) + [self.S])
+        src = np.repeat(self.ring.row_ptrs(coef), rows)
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, bsz * ndig * rows, src=src,
+                                 dst=self.ring.row_ptrs(de),
+                                 src_prime=np.tile(np.repeat(np.arange(ndig), rows), bsz),
+                                 dst_prime=np.tile(gidx, bsz * ndig)), nat.FWD_LIFT)
+        return de
+
+    def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs) -> list:
+        """Key-switch the decomposed digits once per job and ModDown.
+
+        job = (key, perm_dev | None, addend_ptrs [B, 2, lvl+1] uint64 (0 = none),
+        gather_c0): out = ModDown(<perm(de), key>) + addend, component 0 of the
+        addend read through perm when gather_c0 (the rotation's perm(c0)).
+        Returns [B, 2, lvl+1, N] per job (engine.py:305-351)."""
+        bsz = de.shape[0]
+        ndig, rows = lvl + 1, lvl + 2
+        nj = len(jobs)
+        rp = self.ring.row_ptrs
+        ip = self.ring.empty(nj * bsz * 2, rows)
+        ipr = rp(ip).reshape(nj, bsz, 2, rows)
+        der = rp(de).reshape(bsz, ndig, rows)
+        gidx = np.array(list(range(lvl + 1)) + [self.S])
+        parts = []
+        add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
+        perms = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
+        for j, (key, perm, addend, gather_c0) in enumerate(jobs):
+            if key.lmax < lvl:
+                raise LevelScaleError(f"key switching key trimmed to level {key.lmax}, need {lvl}")
+            krow = np.array(list(range(lvl + 1)) + [key.lmax + 1])
+            kbr = rp(key.b).reshape(key.b.shape[0], key.lmax + 2)[0, krow]
+            kar = rp(key.a).reshape(key.a.shape[0], key.lmax + 2)[0, krow]
+            parts.append(_tasks(
+                nat.KS_TASK, bsz * rows, de=der[:, 0, :].ravel(), kb=np.tile(kbr, bsz),
+                ka=np.tile(kar, bsz), out_b=ipr[j, :, 0].ravel(), out_a=ipr[j, :, 1].ravel(),
+                perm=perm.data_ptr() if perm is not None else 0,
+                de_stride=rows * self.n, key_stride=(key.lmax + 2) * self.n, ndig=ndig,
+                prime=np.tile(gidx, bsz)))
+            if addend is not None:
+                add[j] = addend
+                if gather_c0 and perm is not None:
+                    perms[j, :, 0] = perm.data_ptr()
+        self.ring.ks_inner(np.concatenate(parts))
+        m, r = nj * bsz * 2, lvl + 1
+        spc = self._intt_rows(ip[:, lvl + 1].contiguous(), np.full(m, self.S))
+        out = self.ring.empty(m, r)
+        aux = ip[:, :r].contiguous()
+        t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out), aux=rp(aux),
+                   src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
+                   scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
+                   add=add.ravel(), perm=perms.ravel())
+        self.ring.ntt_fwd(t, nat.FWD_MODDOWN)
+        out = out.reshape(nj, bsz, 2, r, self.n)
+        return [out[j] for j in range(nj)]
+
+    def _rot_key(self, amount: int) -> _Ksk:
+        key = self.keys.rot.get(amount % self.n2)
+        if key is None:
+            raise MissingRotationKey(f"no rotation key for amount {amount % self.n2}")
+        return key
+
+    def _rot_job(self, a: Ct, k: int):
+        g = self.ring.galois_element(k)
+        bsz, r = a.payload.batch, a.level + 1
+        add = np.zeros((bsz, 2, r), dtype=np.uint64)
+        add[:, 0] = self.ring.row_ptrs(a.payload.data).reshape(bsz, 2, r)[:, 0]
+        return (self._rot_key(k), self.ring.perm_dev(g), add, True)
+
+    def _raw_rot(self, a: Ct, k: int) -> Ct:
+        return self._raw_rot_many(a, [k])[k]
+
+    def _raw_rot_many(self, a: Ct, ks) -> dict:
+        if not ks:
+            return {}
+        lvl = a.level
+        jobs = [self._rot_job(a, k) for k in ks]
+        de = self._decompose(a.payload.data[:, 1], lvl)
+        outs = self._ks_apply_many(de, lvl, jobs)
+        return {k: Ct(CtData(o), lvl, a.scale, self.n2) for k, o in zip(ks, outs)}
+
+    # ------------------------------------------------------------------ host interop
+
+    def export(self, ct: Ct):
+        """Reference-format payload (c0, c1) uint64 numpy arrays."""
+        return ct.payload.to_host()
+
+    def import_ct(self, c0: np.ndarray, c1: np.ndarray, level: int, scale) -> Ct:
+        """Wrap reference-format host payloads ((rows, N) or (B, rows, N))."""
+        c0, c1 = np.asarray(c0, dtype=np.uint64), np.asarray(c1, dtype=np.uint64)
+        if c0.ndim == 2:
+            c0, c1 = c0[None], c1[None]
+        data = self._dev(np.stack([c0, c1], axis=1))
+        return Ct(CtData(data), level, Fraction(scale), self.n2)

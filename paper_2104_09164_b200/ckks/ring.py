@@ -1,0 +1,183 @@
+"""Ring context: NTT twiddle tables, Galois permutations and the device-side
+launch helpers over RNS row polynomials.
+
+Host-side tables are exact Python-integer computations of the same values
+hear/ckks/ring.py:253-364 builds (bit-reversed psi powers per prime, the NTT
+evaluation-exponent map, NTT-domain Galois permutations).  One deliberate
+difference: the inverse table holds psi^-brv(j), the true inverse of the
+forward transform; the reference's table (ring.py:282, exponent brv(j)+1)
+makes intt(ntt(a)) != a, so its decryptions are garbage.
+
+All polynomial data lives on the GPU as int64 torch tensors reinterpreted as
+uint64 by the kernels; a "row" is N contiguous residues under one prime.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from .. import _native as nat
+from .ntheory import bit_reverse_table, root_2n
+
+
+def _upload(arr: np.ndarray, device) -> torch.Tensor:
+    """Host task table -> device bytes (async on the current stream)."""
+    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8))
+    if t.numel() == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class RingContext:
+    """Per-parameter-set tables (host) and the kernel library handle (device).
+
+    Global prime index: chain primes 0..L, then the special prime (L+1)."""
+
+    def __init__(self, params, device=None):
+        self.params = params
+        self.n = params.n
+        self.logn = self.n.bit_length() - 1
+        self.primes = list(params.chain_primes) + [params.special_prime]
+        self.special_idx = len(self.primes) - 1
+        self.device = torch.device(device or "cuda")
+        if self.device.type != "cuda" or not torch.cuda.is_available():
+            raise nat.NativeError("the B200 engine needs a CUDA device (no CPU fallback)")
+        self.p = np.array(self.primes, dtype=np.uint64)
+        n, logn = self.n, self.logn
+        brv = bit_reverse_table(logn)
+        self.psi = np.zeros((len(self.primes), n), dtype=np.uint64)
+        self.ipsi = np.zeros((len(self.primes), n), dtype=np.uint64)
+        for i, q in enumerate(self.primes):
+            root = root_2n(q, 2 * n)
+            self.psi[i] = _powers(root, brv, q)
+            self.ipsi[i] = _powers(pow(root, -1, q), brv, q)
+        # NTT output j evaluates at psi^(2 brv(j) + 1) (probed in ring.py:320-334)
+        self.exp_map = 2 * brv + 1
+        self._perm_host: dict = {}
+        self._perm_dev: dict = {}
+        L = nat.lib()
+        h = L.hb_ring_create(logn, len(self.primes), self.p.ctypes.data,
+                             self.psi.ctypes.data, self.ipsi.ctypes.data)
+        if not h:
+            raise nat.NativeError(L.hb_last_error().decode())
+        self.handle = ctypes.c_void_p(h)
+        self._lib = L
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self._lib.hb_ring_destroy(self.handle)
+        except Exception:
+            pass
+
+    # ---- Galois machinery (ring.py:336-364) --------------------------------
+
+    def galois_element(self, r: int) -> int:
+        """X -> X^g realising a left slot rotation by r."""
+        return pow(5, r % (self.n // 2), 2 * self.n)
+
+    def ntt_perm(self, g: int) -> np.ndarray:
+        """out[j] = in[perm[j]] applies X -> X^g to NTT-domain rows."""
+        if g not in self._perm_host:
+            two_n = 2 * self.n
+            pos = np.full(two_n, -1, dtype=np.int64)
+            pos[self.exp_map] = np.arange(self.n)
+            perm = pos[(self.exp_map * g) % two_n]
+            if perm.min() < 0:
+                raise RuntimeError("automorphism leaves the evaluation set")
+            self._perm_host[g] = perm.astype(np.int32)
+        return self._perm_host[g]
+
+    def perm_dev(self, g: int) -> torch.Tensor:
+        if g not in self._perm_dev:
+            self._perm_dev[g] = torch.from_numpy(self.ntt_perm(g)).to(self.device)
+        return self._perm_dev[g]
+
+    def coeff_automorphism(self, coeffs: np.ndarray, g: int) -> np.ndarray:
+        """X -> X^g on signed integer coefficients."""
+        k = np.arange(self.n, dtype=np.int64)
+        e = (k * g) % (2 * self.n)
+        out = np.zeros_like(coeffs)
+        out[e % self.n] = np.where(e >= self.n, -coeffs, coeffs)
+        return out
+
+    # ---- launch helpers ------------------------------------------------------
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def ntt_fwd(self, tasks: np.ndarray, mode: int = nat.FWD_PLAIN):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_ntt_fwd(self.handle, _ptr(d), len(tasks), mode, self.stream),
+                      "ntt_fwd")
+
+    def ntt_inv(self, tasks: np.ndarray):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_ntt_inv(self.handle, _ptr(d), len(tasks), self.stream),
+                      "ntt_inv")
+
+    def ew(self, op: int, tasks: np.ndarray):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_ew(self.handle, op, _ptr(d), len(tasks), self.stream), "ew")
+
+    def mac(self, tasks: np.ndarray, terms: np.ndarray):
+        if len(tasks):
+            d, t = _upload(tasks, self.device), _upload(terms, self.device)
+            nat.check(self._lib.hb_mac(self.handle, _ptr(d), len(tasks), _ptr(t), self.stream),
+                      "mac")
+
+    def tensor(self, tasks: np.ndarray):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_tensor(self.handle, _ptr(d), len(tasks), self.stream),
+                      "tensor")
+
+    def ks_inner(self, tasks: np.ndarray):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_ks_inner(self.handle, _ptr(d), len(tasks), self.stream),
+                      "ks_inner")
+
+    # ---- row-pointer helpers ---------------------------------------------------
+
+    def row_ptrs(self, t: torch.Tensor) -> np.ndarray:
+        """Base addresses of every row of a contiguous (..., R, N) tensor, in
+        row-major order (flattened leading dims)."""
+        assert t.is_contiguous() and t.shape[-1] == self.n
+        rows = t.numel() // self.n
+        return np.uint64(t.data_ptr()) + np.arange(rows, dtype=np.uint64) * np.uint64(8 * self.n)
+
+    def zeros(self, *shape) -> torch.Tensor:
+        return torch.zeros(*shape, self.n, dtype=torch.int64, device=self.device)
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, self.n, dtype=torch.int64, device=self.device)
+
+
+def _powers(base: int, exps: np.ndarray, q: int) -> np.ndarray:
+    """base^e mod q for every e in exps (exact, via a power table)."""
+    n = len(exps)
+    pw = np.empty(2 * n, dtype=object)
+    acc = 1
+    for e in range(2 * n):
+        pw[e] = acc
+        acc = acc * base % q
+    return np.array([pw[int(e)] for e in exps], dtype=np.uint64)
+
+
+def shoup_np(w: np.ndarray, p: np.ndarray) -> np.ndarray:
+    w = np.broadcast_to(np.asarray(w, dtype=object), np.broadcast(w, p).shape)
+    p = np.broadcast_to(np.asarray(p, dtype=object), w.shape)
+    return np.array([(int(a) << 64) // int(b) for a, b in zip(w.ravel(), p.ravel())],
+                    dtype=np.uint64).reshape(w.shape)

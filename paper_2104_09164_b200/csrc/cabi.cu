@@ -1,0 +1,316 @@
+// C-ABI of the B200 HEAR kernels (declared in include/hear_b200.h).
+//
+// Two families of entry points:
+//   hb_*     device-pointer, task-table launches used by the Python engine
+//            (paper_2104_09164_b200/ckks/engine.py); every call is
+//            asynchronous on the given stream.
+//   hear_*   reference-shaped, host-buffer entry points with the argument
+//            meaning of hear/ckks/ring.py's numba kernels (rows x N uint64
+//            arrays + per-row prime index), for a maintainer who binds them
+//            from the reference via ctypes.  They copy in,
+//            launch, copy out and synchronise.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ring.cuh"
+
+namespace hb {
+cudaError_t launch_ntt_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
+cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
+cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
+struct HbCrtTask;
+cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
+                              int, int, cudaStream_t);
+cudaError_t launch_encode(const double*, long long*, int, double, const HbFftTables&, int*,
+                          cudaStream_t);
+cudaError_t launch_decode(const double*, double*, int, double, const HbFftTables&, cudaStream_t);
+}  // namespace hb
+
+using namespace hb;
+
+struct hb_ring {
+  HbRing dev;            // pointers into device memory
+  HbPrime* primes_dev;
+  HbTw* tw_fwd_dev;
+  HbTw* tw_inv_dev;
+  std::vector<HbPrime> primes_host;
+  int last_err;
+};
+
+struct hb_fft {
+  HbFftTables t;
+  double2* root_dev;
+  double2* twist_dev;
+  int* pos_dev;
+};
+
+static thread_local char g_err[512];
+
+static int fail(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return (int)e;
+}
+
+static unsigned long long shoup(unsigned long long w, unsigned long long p) {
+  return (unsigned long long)(((unsigned __int128)w << 64) / p);
+}
+
+extern "C" {
+
+const char* hb_last_error(void) { return g_err; }
+
+int hb_version(void) { return 1; }
+
+hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
+                        const unsigned long long* psi, const unsigned long long* ipsi) {
+  const int n = 1 << logn;
+  hb_ring* r = new hb_ring();
+  memset(&r->dev, 0, sizeof(r->dev));
+  r->dev.logn = logn;
+  r->dev.n = n;
+  r->dev.nprimes = nprimes;
+  r->primes_host.resize(nprimes);
+  for (int i = 0; i < nprimes; ++i) {
+    const unsigned long long p = primes[i];
+    if (p >> 62) {
+      snprintf(g_err, sizeof(g_err), "prime %llu exceeds 62 bits", p);
+      delete r;
+      return nullptr;
+    }
+    HbPrime& P = r->primes_host[i];
+    P.p = p;
+    P.two_p = 2 * p;
+    P.one_sh = (unsigned long long)(((unsigned __int128)1 << 64) / p);
+    P.r64 = (unsigned long long)(((unsigned __int128)1 << 64) % p);
+    P.r64_sh = shoup(P.r64, p);
+    // N^-1 mod p by Fermat
+    unsigned __int128 acc = 1, base = (unsigned long long)n % p;
+    unsigned long long e = p - 2;
+    while (e) {
+      if (e & 1) acc = acc * base % p;
+      base = base * base % p;
+      e >>= 1;
+    }
+    P.ninv = (unsigned long long)acc;
+    P.ninv_sh = shoup(P.ninv, p);
+    P.half = p >> 1;
+  }
+  std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
+  for (int i = 0; i < nprimes; ++i) {
+    for (int j = 0; j < n; ++j) {
+      const size_t k = (size_t)i * n + j;
+      tf[k].w = psi[k];
+      tf[k].wsh = shoup(psi[k], primes[i]);
+      ti[k].w = ipsi[k];
+      ti[k].wsh = shoup(ipsi[k], primes[i]);
+    }
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc(&r->primes_dev, sizeof(HbPrime) * nprimes)) ||
+      (e = cudaMalloc(&r->tw_fwd_dev, sizeof(HbTw) * tf.size())) ||
+      (e = cudaMalloc(&r->tw_inv_dev, sizeof(HbTw) * ti.size())) ||
+      (e = cudaMemcpy(r->primes_dev, r->primes_host.data(), sizeof(HbPrime) * nprimes,
+                      cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(r->tw_fwd_dev, tf.data(), sizeof(HbTw) * tf.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(r->tw_inv_dev, ti.data(), sizeof(HbTw) * ti.size(), cudaMemcpyHostToDevice))) {
+    fail(e, "hb_ring_create");
+    delete r;
+    return nullptr;
+  }
+  r->dev.primes = r->primes_dev;
+  r->dev.tw_fwd = r->tw_fwd_dev;
+  r->dev.tw_inv = r->tw_inv_dev;
+  return r;
+}
+
+void hb_ring_destroy(hb_ring* r) {
+  if (!r) return;
+  cudaFree(r->primes_dev);
+  cudaFree(r->tw_fwd_dev);
+  cudaFree(r->tw_inv_dev);
+  delete r;
+}
+
+// Per-prime constants as the kernels see them (host copy, for tests).
+int hb_ring_prime_consts(const hb_ring* r, int i, unsigned long long* out8) {
+  if (!r || i < 0 || i >= r->dev.nprimes) return -1;
+  memcpy(out8, &r->primes_host[i], sizeof(HbPrime));
+  return 0;
+}
+
+int hb_sizeof_task(int kind) {
+  switch (kind) {
+    case 0: return (int)sizeof(HbNttTask);
+    case 1: return (int)sizeof(HbEwTask);
+    case 2: return (int)sizeof(HbMacTask);
+    case 3: return (int)sizeof(HbMacTerm);
+    case 4: return (int)sizeof(HbKsTask);
+    default: return -1;
+  }
+}
+
+int hb_ntt_fwd(hb_ring* r, const void* tasks, int count, int mode, void* stream) {
+  cudaError_t e = launch_ntt_fwd((const HbNttTask*)tasks, count, r->dev, mode, (cudaStream_t)stream);
+  return e ? fail(e, "hb_ntt_fwd") : 0;
+}
+
+int hb_ntt_inv(hb_ring* r, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_ntt_inv((const HbNttTask*)tasks, count, r->dev, (cudaStream_t)stream);
+  return e ? fail(e, "hb_ntt_inv") : 0;
+}
+
+int hb_ew(hb_ring* r, int op, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_ew(op, (const HbEwTask*)tasks, count, r->dev.primes, r->dev.n,
+                            (cudaStream_t)stream);
+  return e ? fail(e, "hb_ew") : 0;
+}
+
+int hb_mac(hb_ring* r, const void* tasks, int count, const void* terms, void* stream) {
+  cudaError_t e = launch_mac((const HbMacTask*)tasks, count, (const HbMacTerm*)terms,
+                             r->dev.primes, r->dev.n, (cudaStream_t)stream);
+  return e ? fail(e, "hb_mac") : 0;
+}
+
+int hb_tensor(hb_ring* r, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_tensor(tasks, count, r->dev.primes, r->dev.n, (cudaStream_t)stream);
+  return e ? fail(e, "hb_tensor") : 0;
+}
+
+int hb_ks_inner(hb_ring* r, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_ks_inner((const HbKsTask*)tasks, count, r->dev.primes, r->dev.n,
+                                  (cudaStream_t)stream);
+  return e ? fail(e, "hb_ks_inner") : 0;
+}
+
+int hb_crt_double(hb_ring* r, const void* tasks, int count, const unsigned long long* consts,
+                  const int* prime_idx, int keep, int nl, void* stream) {
+  cudaError_t e = launch_crt_double((const HbCrtTask*)tasks, count, consts, r->dev.primes, prime_idx,
+                                    keep, nl, r->dev.n, (cudaStream_t)stream);
+  return e ? fail(e, "hb_crt_double") : 0;
+}
+
+hb_fft* hb_fft_create(int logn2, const double* root_re_im, const double* twist_re_im,
+                      const int* slot_pos) {
+  const int n2 = 1 << logn2;
+  hb_fft* f = new hb_fft();
+  f->t.logn2 = logn2;
+  f->t.n2 = n2;
+  cudaError_t e;
+  if ((e = cudaMalloc(&f->root_dev, sizeof(double2) * (n2 / 2))) ||
+      (e = cudaMalloc(&f->twist_dev, sizeof(double2) * n2)) ||
+      (e = cudaMalloc(&f->pos_dev, sizeof(int) * n2)) ||
+      (e = cudaMemcpy(f->root_dev, root_re_im, sizeof(double2) * (n2 / 2), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(f->twist_dev, twist_re_im, sizeof(double2) * n2, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(f->pos_dev, slot_pos, sizeof(int) * n2, cudaMemcpyHostToDevice))) {
+    fail(e, "hb_fft_create");
+    delete f;
+    return nullptr;
+  }
+  f->t.root = f->root_dev;
+  f->t.twist = f->twist_dev;
+  f->t.slot_pos = f->pos_dev;
+  return f;
+}
+
+void hb_fft_destroy(hb_fft* f) {
+  if (!f) return;
+  cudaFree(f->root_dev);
+  cudaFree(f->twist_dev);
+  cudaFree(f->pos_dev);
+  delete f;
+}
+
+int hb_encode(hb_fft* f, const double* slots, long long* coeffs, int npoly, double scale,
+              int* overflow, void* stream) {
+  cudaError_t e = launch_encode(slots, coeffs, npoly, scale, f->t, overflow, (cudaStream_t)stream);
+  return e ? fail(e, "hb_encode") : 0;
+}
+
+int hb_decode(hb_fft* f, const double* coeffs, double* slots, int npoly, double scale,
+              void* stream) {
+  cudaError_t e = launch_decode(coeffs, slots, npoly, scale, f->t, (cudaStream_t)stream);
+  return e ? fail(e, "hb_decode") : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Reference-shaped host-buffer entry points (ring.py signatures).
+
+static int host_rows_op(hb_ring* r, int nrows, const long long* gidx, int kind,
+                        unsigned long long* inout, const unsigned long long* b,
+                        unsigned long long* out) {
+  const int n = r->dev.n;
+  const size_t bytes = (size_t)nrows * n * sizeof(u64);
+  u64 *d_a = nullptr, *d_b = nullptr, *d_o = nullptr;
+  void* d_t = nullptr;
+  cudaError_t e = cudaSuccess;
+  if ((e = cudaMalloc(&d_a, bytes))) return fail(e, "hear host op");
+  if (b && (e = cudaMalloc(&d_b, bytes))) goto done;
+  if ((e = cudaMalloc(&d_o, bytes))) goto done;
+  if ((e = cudaMemcpy(d_a, inout, bytes, cudaMemcpyHostToDevice))) goto done;
+  if (b && (e = cudaMemcpy(d_b, b, bytes, cudaMemcpyHostToDevice))) goto done;
+  if (kind <= 1) {
+    std::vector<HbNttTask> t(nrows);
+    for (int i = 0; i < nrows; ++i) {
+      memset(&t[i], 0, sizeof(HbNttTask));
+      t[i].src = d_a + (size_t)i * n;
+      t[i].dst = d_o + (size_t)i * n;
+      t[i].dst_prime = t[i].src_prime = (int)gidx[i];
+    }
+    if ((e = cudaMalloc(&d_t, sizeof(HbNttTask) * nrows))) goto done;
+    if ((e = cudaMemcpy(d_t, t.data(), sizeof(HbNttTask) * nrows, cudaMemcpyHostToDevice))) goto done;
+    e = kind == 0 ? launch_ntt_fwd((HbNttTask*)d_t, nrows, r->dev, 0, 0)
+                  : launch_ntt_inv((HbNttTask*)d_t, nrows, r->dev, 0);
+  } else {
+    std::vector<HbEwTask> t(nrows);
+    for (int i = 0; i < nrows; ++i) {
+      memset(&t[i], 0, sizeof(HbEwTask));
+      t[i].dst = d_o + (size_t)i * n;
+      t[i].a = d_a + (size_t)i * n;
+      t[i].b = d_b ? d_b + (size_t)i * n : nullptr;
+      t[i].prime = (int)gidx[i];
+    }
+    if ((e = cudaMalloc(&d_t, sizeof(HbEwTask) * nrows))) goto done;
+    if ((e = cudaMemcpy(d_t, t.data(), sizeof(HbEwTask) * nrows, cudaMemcpyHostToDevice))) goto done;
+    e = launch_ew(kind - 2, (HbEwTask*)d_t, nrows, r->dev.primes, n, 0);
+  }
+  if (e) goto done;
+  if ((e = cudaDeviceSynchronize())) goto done;
+  e = cudaMemcpy(out ? out : inout, d_o, bytes, cudaMemcpyDeviceToHost);
+done:
+  cudaFree(d_a);
+  cudaFree(d_b);
+  cudaFree(d_o);
+  cudaFree(d_t);
+  return e ? fail(e, "hear host op") : 0;
+}
+
+// ring.py:113 ntt_fwd(a, gidx, ...) -- in place on a host (rows, N) array.
+int hear_ntt_fwd(hb_ring* r, unsigned long long* a, int nrows, const long long* gidx) {
+  return host_rows_op(r, nrows, gidx, 0, a, nullptr, nullptr);
+}
+// ring.py:120 ntt_inv(a, gidx, ...) -- in place.
+int hear_ntt_inv(hb_ring* r, unsigned long long* a, int nrows, const long long* gidx) {
+  return host_rows_op(r, nrows, gidx, 1, a, nullptr, nullptr);
+}
+// ring.py:127 pw_mul(out, a, b, gidx, ...)
+int hear_pw_mul(hb_ring* r, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx) {
+  return host_rows_op(r, nrows, gidx, 2 + 2, const_cast<unsigned long long*>(a), b, out);
+}
+// ring.py:159 pw_add(out, a, b, gidx, p)
+int hear_pw_add(hb_ring* r, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx) {
+  return host_rows_op(r, nrows, gidx, 2 + 0, const_cast<unsigned long long*>(a), b, out);
+}
+// ring.py:167 pw_sub(out, a, b, gidx, p)
+int hear_pw_sub(hb_ring* r, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx) {
+  return host_rows_op(r, nrows, gidx, 2 + 1, const_cast<unsigned long long*>(a), b, out);
+}
+
+}  // extern "C"

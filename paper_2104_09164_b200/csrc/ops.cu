@@ -1,0 +1,350 @@
+// Element-wise RNS kernels: modular add/sub/mul, plaintext multiply-
+// accumulate, the ciphertext tensor product, the key-switch inner product
+// with the fused Galois gather, and the CRT reconstruction for decryption.
+//
+// All rows are N contiguous u64 residues; every task names its prime.  Each
+// thread handles two adjacent coefficients (one 16-byte load per operand),
+// grid.y walks the task list, grid.x the row.
+#include "ring.cuh"
+
+namespace hb {
+
+enum EwOp : int {
+  EW_ADD = 0,       // dst = a + b                       (ring.py:159 pw_add)
+  EW_SUB = 1,       // dst = a - b                       (ring.py:167 pw_sub)
+  EW_MUL = 2,       // dst = a * b                       (ring.py:127 pw_mul)
+  EW_MUL_SCALAR = 3,// dst = a * scal                    (ring.py:175 scalar_mul)
+  EW_MULADD = 4,    // dst = a * b + c                   (engine.py:202-203)
+  EW_ADD_SCALED = 5,// dst = a + b * scal                (engine.py:204-208)
+  EW_COPY = 6,      // dst = a
+  EW_PERM = 7,      // dst = a[perm]  (b reinterpreted as int32 perm)
+  EW_SUB_SCALED = 8,// dst = (a - b) * scal              (ring.py:210 sub_scaled_inv)
+};
+
+constexpr int EW_THREADS = 256;
+
+template <int OP>
+__global__ void __launch_bounds__(EW_THREADS)
+k_ew(const HbEwTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes, int n) {
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbEwTask tk = tasks[t];
+    const HbPrime P = primes[tk.prime];
+    const u64 p = P.p;
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tk.a + j);
+    ulonglong2 r;
+    if (OP == EW_ADD || OP == EW_SUB || OP == EW_MUL || OP == EW_MULADD ||
+        OP == EW_ADD_SCALED || OP == EW_SUB_SCALED) {
+      ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tk.b + j);
+      if (OP == EW_ADD) { r.x = add_mod(a.x, b.x, p); r.y = add_mod(a.y, b.y, p); }
+      if (OP == EW_SUB) { r.x = sub_mod(a.x, b.x, p); r.y = sub_mod(a.y, b.y, p); }
+      if (OP == EW_MUL) { r.x = mul_mod(a.x, b.x, P); r.y = mul_mod(a.y, b.y, P); }
+      if (OP == EW_MULADD) {
+        ulonglong2 c = *reinterpret_cast<const ulonglong2*>(tk.c + j);
+        r.x = add_mod(mul_mod(a.x, b.x, P), c.x, p);
+        r.y = add_mod(mul_mod(a.y, b.y, P), c.y, p);
+      }
+      if (OP == EW_ADD_SCALED) {
+        r.x = add_mod(a.x, mul_shoup(b.x, tk.scal, tk.scal_sh, p), p);
+        r.y = add_mod(a.y, mul_shoup(b.y, tk.scal, tk.scal_sh, p), p);
+      }
+      if (OP == EW_SUB_SCALED) {
+        r.x = mul_shoup(sub_mod(a.x, b.x, p), tk.scal, tk.scal_sh, p);
+        r.y = mul_shoup(sub_mod(a.y, b.y, p), tk.scal, tk.scal_sh, p);
+      }
+    } else if (OP == EW_MUL_SCALAR) {
+      r.x = mul_shoup(a.x, tk.scal, tk.scal_sh, p);
+      r.y = mul_shoup(a.y, tk.scal, tk.scal_sh, p);
+    } else if (OP == EW_COPY) {
+      r = a;
+    } else if (OP == EW_PERM) {
+      const int* perm = reinterpret_cast<const int*>(tk.b);
+      r.x = __ldg(tk.a + __ldg(perm + j));
+      r.y = __ldg(tk.a + __ldg(perm + j + 1));
+    }
+    *reinterpret_cast<ulonglong2*>(tk.dst + j) = r;
+  }
+}
+
+static dim3 ew_grid(int ntasks, int n) {
+  const int bx = (n / 2 + EW_THREADS - 1) / EW_THREADS;
+  return dim3(bx, ntasks < 65535 ? ntasks : 65535);
+}
+
+cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* primes, int n,
+                      cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  dim3 grid = ew_grid(ntasks, n);
+  switch (op) {
+#define HB_EW_CASE(OPC) \
+  case OPC: k_ew<OPC><<<grid, EW_THREADS, 0, st>>>(tasks, ntasks, primes, n); break;
+    HB_EW_CASE(EW_ADD)
+    HB_EW_CASE(EW_SUB)
+    HB_EW_CASE(EW_MUL)
+    HB_EW_CASE(EW_MUL_SCALAR)
+    HB_EW_CASE(EW_MULADD)
+    HB_EW_CASE(EW_ADD_SCALED)
+    HB_EW_CASE(EW_COPY)
+    HB_EW_CASE(EW_PERM)
+    HB_EW_CASE(EW_SUB_SCALED)
+#undef HB_EW_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Plaintext multiply-accumulate: one output row = sum over its terms of
+// pt * ct (mod p).  Replaces chains of ring.py:127 pw_mul + ring.py:159
+// pw_add issued by the convolution / FC schedules; modular sums are exact,
+// so the result equals the chained ops bit for bit.  Products accumulate in
+// 128 bits and fold to a residue every 8 terms (p < 2^62 => no overflow).
+__global__ void __launch_bounds__(EW_THREADS)
+k_mac(const HbMacTask* __restrict__ tasks, int ntasks, const HbMacTerm* __restrict__ terms,
+      const HbPrime* __restrict__ primes, int n) {
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbMacTask tk = tasks[t];
+    const HbPrime P = primes[tk.prime];
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    Acc128 s0, s1;
+    for (int k = 0; k < tk.nterms; ++k) {
+      const HbMacTerm tm = terms[tk.term_off + k];
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(tm.pt + j));
+      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(tm.ct + j));
+      s0.mac(a.x, b.x);
+      s1.mac(a.y, b.y);
+      if ((k & 7) == 7) { s0.fold(P); s1.fold(P); }
+    }
+    ulonglong2 r;
+    r.x = s0.fold(P);
+    r.y = s1.fold(P);
+    *reinterpret_cast<ulonglong2*>(tk.dst + j) = r;
+  }
+}
+
+cudaError_t launch_mac(const HbMacTask* tasks, int ntasks, const HbMacTerm* terms,
+                       const HbPrime* primes, int n, cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  k_mac<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(tasks, ntasks, terms, primes, n);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Tensor product of two ciphertexts row by row (engine.py:249-257):
+//   d0 = a0*b0, d1 = a0*b1 + a1*b0, d2 = a1*b1.
+struct HbTensorTask {
+  const u64 *a0, *a1, *b0, *b1;
+  u64 *d0, *d1, *d2;
+  int prime;
+  int _pad;
+};
+
+__global__ void __launch_bounds__(EW_THREADS)
+k_tensor(const HbTensorTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes,
+         int n) {
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbTensorTask tk = tasks[t];
+    const HbPrime P = primes[tk.prime];
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(tk.a0 + j);
+    const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(tk.a1 + j);
+    const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(tk.b0 + j);
+    const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(tk.b1 + j);
+    ulonglong2 r0, r1, r2;
+    r0.x = mul_mod(a0.x, b0.x, P);
+    r0.y = mul_mod(a0.y, b0.y, P);
+    {
+      Acc128 s;
+      s.mac(a0.x, b1.x);
+      s.mac(a1.x, b0.x);
+      r1.x = s.fold(P);
+      Acc128 u;
+      u.mac(a0.y, b1.y);
+      u.mac(a1.y, b0.y);
+      r1.y = u.fold(P);
+    }
+    r2.x = mul_mod(a1.x, b1.x, P);
+    r2.y = mul_mod(a1.y, b1.y, P);
+    *reinterpret_cast<ulonglong2*>(tk.d0 + j) = r0;
+    *reinterpret_cast<ulonglong2*>(tk.d1 + j) = r1;
+    *reinterpret_cast<ulonglong2*>(tk.d2 + j) = r2;
+  }
+}
+
+cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, int n,
+                          cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  k_tensor<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(
+      reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Key-switch inner product with the Galois gather fused in
+// (ring.py:136-156 pw_mul_accum_perm): for every output row r,
+//   out_b[n] = sum_i de_i[perm[n]] * kb_i[n],   out_a[n] = sum_i de_i[perm[n]] * ka_i[n].
+__global__ void __launch_bounds__(EW_THREADS)
+k_ks_inner(const HbKsTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes,
+           int n) {
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbKsTask tk = tasks[t];
+    const HbPrime P = primes[tk.prime];
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    int s0 = j, s1 = j + 1;
+    if (tk.perm) {
+      const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+      s0 = pp.x;
+      s1 = pp.y;
+    }
+    Acc128 b0, b1, a0, a1;
+    for (int i = 0; i < tk.ndig; ++i) {
+      const u64* de = tk.de + i * tk.de_stride;
+      const u64 x0 = __ldg(de + s0), x1 = __ldg(de + s1);
+      const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
+      const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
+      b0.mac(x0, kb.x);
+      b1.mac(x1, kb.y);
+      a0.mac(x0, ka.x);
+      a1.mac(x1, ka.y);
+      if ((i & 7) == 7) { b0.fold(P); b1.fold(P); a0.fold(P); a1.fold(P); }
+    }
+    ulonglong2 rb, ra;
+    rb.x = b0.fold(P);
+    rb.y = b1.fold(P);
+    ra.x = a0.fold(P);
+    ra.y = a1.fold(P);
+    *reinterpret_cast<ulonglong2*>(tk.out_b + j) = rb;
+    *reinterpret_cast<ulonglong2*>(tk.out_a + j) = ra;
+  }
+}
+
+cudaError_t launch_ks_inner(const HbKsTask* tasks, int ntasks, const HbPrime* primes, int n,
+                            cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  k_ks_inner<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(tasks, ntasks, primes, n);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Exact CRT reconstruction of `keep` coefficient rows into a centred integer,
+// correctly rounded to double (engine.py:156-175).  Constants (little-endian
+// 64-bit limbs, NL limbs each): Q, floor(Q/2), and per prime the residue
+// coefficient qhat_inv_i and the multiword qhat_i = Q/q_i.
+//   v = sum_i [x_i * qhat_inv_i]_{q_i} * qhat_i  mod Q;  v > Q/2 => v - Q.
+constexpr int CRT_MAXL = 8;
+
+struct HbCrtTask {
+  const u64* rows;   // keep rows of n coefficients (row stride n)
+  double* out;       // n doubles
+};
+
+HB_DEV double mw_to_double(const u64* m, int nl, bool neg) {
+  int top = nl - 1;
+  while (top > 0 && m[top] == 0) --top;
+  if (top == 0 && m[0] == 0) return 0.0;
+  const int lz = __clzll(m[top]);
+  const int msb = top * 64 + (63 - lz);  // bit index of the leading 1
+  // Extract 64 bits [msb-63, msb], OR-ing everything below into a sticky bit.
+  const int lo_bit = msb - 63;
+  if (lo_bit <= 0) {  // value < 2^64: one correctly rounded conversion
+    const double d = __ull2double_rn(m[0]);
+    return neg ? -d : d;
+  }
+  bool sticky = false;
+  const int wi = lo_bit >> 6, bi = lo_bit & 63;
+  u64 w = m[wi] >> bi;
+  if (bi) w |= m[wi + 1] << (64 - bi);
+  if (bi && (m[wi] & ((1ull << bi) - 1))) sticky = true;
+  for (int k = 0; k < wi && !sticky; ++k)
+    if (m[k]) sticky = true;
+  if (sticky) w |= 1ull;  // bit 0 is below the 53-bit mantissa: acts as sticky
+  double d = ldexp(__ull2double_rn(w), lo_bit);
+  return neg ? -d : d;
+}
+
+__global__ void k_crt_double(const HbCrtTask* __restrict__ tasks, int ntasks, const u64* __restrict__ consts,
+                             const HbPrime* __restrict__ primes, const int* __restrict__ prime_idx,
+                             int keep, int nl, int n) {
+  // consts layout: Q[nl], Qhalf[nl], qhat_inv[keep], qhat[keep][nl]
+  const u64* Q = consts;
+  const u64* Qh = consts + nl;
+  const u64* qinv = consts + 2 * nl;
+  const u64* qhat = consts + 2 * nl + keep;
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbCrtTask tk = tasks[t];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) continue;
+    u64 acc[CRT_MAXL + 1];
+    for (int l = 0; l <= nl; ++l) acc[l] = 0;
+    for (int i = 0; i < keep; ++i) {
+      const HbPrime P = primes[prime_idx[i]];
+      const u64 y = mul_mod(tk.rows[(size_t)i * n + j], qinv[i], P);
+      // acc += y * qhat_i (multiword)
+      u64 carry = 0;
+      for (int l = 0; l < nl; ++l) {
+        const u64 m = qhat[i * nl + l];
+        u64 lo = y * m, hi = __umul64hi(y, m);
+        lo += carry;
+        hi += (lo < carry);
+        const u64 s = acc[l] + lo;
+        hi += (s < lo);
+        acc[l] = s;
+        carry = hi;
+      }
+      acc[nl] += carry;
+    }
+    // reduce mod Q: acc < keep * Q, subtract Q while acc >= Q
+    for (int rep = 0; rep < keep; ++rep) {
+      bool ge = acc[nl] != 0;
+      if (!ge) {
+        ge = true;
+        for (int l = nl - 1; l >= 0; --l) {
+          if (acc[l] != Q[l]) { ge = acc[l] > Q[l]; break; }
+        }
+      }
+      if (!ge) break;
+      u64 borrow = 0;
+      for (int l = 0; l < nl; ++l) {
+        const u64 q = Q[l] + borrow;
+        const u64 nb = (q < borrow) || (acc[l] < q);
+        acc[l] -= q;
+        borrow = nb;
+      }
+      acc[nl] -= borrow;
+    }
+    // centre: v > Q/2 -> v - Q (negative, magnitude Q - v)
+    bool gt = false;
+    for (int l = nl - 1; l >= 0; --l) {
+      if (acc[l] != Qh[l]) { gt = acc[l] > Qh[l]; break; }
+    }
+    u64 mag[CRT_MAXL];
+    if (gt) {
+      u64 borrow = 0;
+      for (int l = 0; l < nl; ++l) {
+        const u64 a = acc[l] + borrow;
+        const u64 nb = (a < borrow) || (Q[l] < a);
+        mag[l] = Q[l] - a;
+        borrow = nb;
+      }
+    } else {
+      for (int l = 0; l < nl; ++l) mag[l] = acc[l];
+    }
+    tk.out[j] = mw_to_double(mag, nl, gt);
+  }
+}
+
+cudaError_t launch_crt_double(const HbCrtTask* tasks, int ntasks, const u64* consts,
+                              const HbPrime* primes, const int* prime_idx, int keep, int nl, int n,
+                              cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  if (nl > CRT_MAXL) return cudaErrorInvalidValue;
+  dim3 grid((n + 255) / 256, ntasks < 65535 ? ntasks : 65535);
+  k_crt_double<<<grid, 256, 0, st>>>(tasks, ntasks, consts, primes, prime_idx, keep, nl, n);
+  return cudaGetLastError();
+}
+
+}  // namespace hb

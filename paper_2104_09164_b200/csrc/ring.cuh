@@ -1,0 +1,86 @@
+// Device-side ring context and task descriptors shared by all kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include "modarith.cuh"
+
+// Twiddle entry: power of the 2N-th root plus its Shoup companion, stored
+// together so one 16-byte load fetches both.
+struct __align__(16) HbTw {
+  u64 w, wsh;
+};
+
+struct HbRing {
+  int logn;
+  int n;
+  int nprimes;
+  int _pad;
+  const HbPrime* primes;  // [nprimes]
+  const HbTw* tw_fwd;     // [nprimes][n]  psi^brv(j)            (ring.py:281)
+  const HbTw* tw_inv;     // [nprimes][n]  psi^-brv(j)  (true inverse)
+};
+
+// One row-polynomial transform.  Field meaning depends on the kernel mode;
+// see ntt.cu.
+struct HbNttTask {
+  const u64* src;
+  u64* dst;
+  const u64* aux;   // ModDown/rescale: extended-basis row x_r
+  const u64* add;   // optional addend row (gathered through perm if set)
+  const int* perm;  // optional automorphism gather for `add`
+  u64 scal;         // epilogue constant (P^-1 / q_l^-1 mod p_dst)
+  u64 scal_sh;
+  int src_prime;    // prime of src when it differs from dst_prime (lift)
+  int dst_prime;    // prime the transform runs in
+};
+
+// One output row of a plaintext multiply-accumulate:
+//   dst = sum_t pt_t * ct_t  (mod p)   over terms [term_off, term_off + nterms)
+struct HbMacTask {
+  u64* dst;
+  int prime;
+  int nterms;
+  int term_off;
+  int _pad;
+};
+
+struct HbMacTerm {
+  const u64* pt;
+  const u64* ct;
+};
+
+// One output row pair of the key-switch inner product:
+//   out_b[n] = sum_i de_i[perm[n]] * kb_i[n],  out_a likewise with ka.
+// de_i = de + i * de_stride, kb_i = kb + i * key_stride.
+struct HbKsTask {
+  const u64* de;
+  const u64* kb;
+  const u64* ka;
+  u64* out_b;
+  u64* out_a;
+  const int* perm;
+  long long de_stride;
+  long long key_stride;
+  int ndig;
+  int prime;
+};
+
+// Generic element-wise row op.
+struct HbEwTask {
+  u64* dst;
+  const u64* a;
+  const u64* b;
+  const u64* c;
+  u64 scal;
+  u64 scal_sh;
+  int prime;
+  int _pad;
+};
+
+// Special-FFT tables of the canonical embedding (fft.cu).
+struct HbFftTables {
+  int logn2;            // log2(N/2)
+  int n2;
+  const double2* root;  // [n2/2]: e^{+2 pi i k / n2}
+  const double2* twist; // [n2]:   zeta^k = e^{i pi k / N}
+  const int* slot_pos;  // [n2]:   m_j, slot j -> DFT bin
+};
