@@ -45,6 +45,7 @@ def lib():
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_mac.argtypes = [vp, vp, i32, vp, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
+        L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
         L.hb_ks_inner.argtypes = [vp, vp, i32, vp]
         L.hb_crt_double.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
         L.hb_fft_create.restype = vp
@@ -77,6 +78,7 @@ EW_TASK = np.dtype([("dst", "<u8"), ("a", "<u8"), ("b", "<u8"), ("c", "<u8"),
 MAC_TASK = np.dtype([("dst", "<u8"), ("prime", "<i4"), ("nterms", "<i4"),
                      ("term_off", "<i4"), ("_pad", "<i4")])
 MAC_TERM = np.dtype([("pt", "<u8"), ("ct", "<u8")])
+MAC_OUT = np.dtype([("dst", "<u8"), ("nterms", "<i4"), ("term_off", "<i4")])
 KS_TASK = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
                     ("out_a", "<u8"), ("perm", "<u8"), ("de_stride", "<i8"),
                     ("key_stride", "<i8"), ("ndig", "<i4"), ("prime", "<i4")])

@@ -485,34 +485,37 @@ class CkksBackend(BackendBase):
                                  dst_prime=np.tile(gidx, bsz * ndig)), nat.FWD_LIFT)
         return de
 
-    def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs) -> list:
-        """Key-switch the decomposed digits once per job and ModDown.
+    def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None) -> list:
+        """Key-switch decomposed digits once per job and ModDown.
 
-        job = (key, perm_dev | None, addend_ptrs [B, 2, lvl+1] uint64 (0 = none),
-        gather_c0): out = ModDown(<perm(de), key>) + addend, component 0 of the
-        addend read through perm when gather_c0 (the rotation's perm(c0)).
-        Returns [B, 2, lvl+1, N] per job (engine.py:305-351)."""
-        bsz = de.shape[0]
+        job = (key, perm_dev | None, addend_ptrs [bsz, 2, lvl+1] uint64 (0 = none),
+        gather_c0[, de_off]): out = ModDown(<perm(de[de_off:de_off+bsz]), key>)
+        + addend, component 0 of the addend read through perm when gather_c0
+        (the rotation's perm(c0)).  Returns [bsz, 2, lvl+1, N] per job
+        (engine.py:305-351)."""
+        bsz = de.shape[0] if bsz is None else bsz
         ndig, rows = lvl + 1, lvl + 2
         nj = len(jobs)
         rp = self.ring.row_ptrs
         ip = self.ring.empty(nj * bsz * 2, rows)
         ipr = rp(ip).reshape(nj, bsz, 2, rows)
-        der = rp(de).reshape(bsz, ndig, rows)
+        der = rp(de).reshape(de.shape[0], ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         parts = []
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
         perms = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
-        for j, (key, perm, addend, gather_c0) in enumerate(jobs):
+        for j, job in enumerate(jobs):
+            key, perm, addend, gather_c0 = job[:4]
+            off = job[4] if len(job) > 4 else 0
             if key.lmax < lvl:
                 raise LevelScaleError(f"key switching key trimmed to level {key.lmax}, need {lvl}")
             krow = np.array(list(range(lvl + 1)) + [key.lmax + 1])
             kbr = rp(key.b).reshape(key.b.shape[0], key.lmax + 2)[0, krow]
             kar = rp(key.a).reshape(key.a.shape[0], key.lmax + 2)[0, krow]
             parts.append(_tasks(
-                nat.KS_TASK, bsz * rows, de=der[:, 0, :].ravel(), kb=np.tile(kbr, bsz),
-                ka=np.tile(kar, bsz), out_b=ipr[j, :, 0].ravel(), out_a=ipr[j, :, 1].ravel(),
-                perm=perm.data_ptr() if perm is not None else 0,
+                nat.KS_TASK, bsz * rows, de=der[off:off + bsz, 0, :].ravel(),
+                kb=np.tile(kbr, bsz), ka=np.tile(kar, bsz), out_b=ipr[j, :, 0].ravel(),
+                out_a=ipr[j, :, 1].ravel(), perm=perm.data_ptr() if perm is not None else 0,
                 de_stride=rows * self.n, key_stride=(key.lmax + 2) * self.n, ndig=ndig,
                 prime=np.tile(gidx, bsz)))
             if addend is not None:
@@ -548,14 +551,147 @@ class CkksBackend(BackendBase):
     def _raw_rot(self, a: Ct, k: int) -> Ct:
         return self._raw_rot_many(a, [k])[k]
 
+    # ------------------------------------------------------------------ layer-wide batches
+
+    # HBM budget for one batched launch group's temporaries (decomposed
+    # digits of many ciphertexts); larger groups are split into chunks.
+    ks_budget_bytes = 6 << 30
+
+    @staticmethod
+    def _by_level(items, level_of):
+        groups: dict = {}
+        for i, it in enumerate(items):
+            groups.setdefault(level_of(it), []).append(i)
+        return groups
+
+    def _raw_mac_many(self, jobs) -> list:
+        out = [None] * len(jobs)
+        for lvl, idx in self._by_level(jobs, lambda t: t[0][0].level).items():
+            bsz = jobs[idx[0]][0][0].payload.batch
+            r = lvl + 1
+            res = self.ring.empty(len(idx), bsz, 2, r)
+            rp = self.ring.row_ptrs
+            dst = rp(res).reshape(len(idx), -1)[:, 0]
+            counts = np.array([len(jobs[i]) for i in idx], dtype=np.int64)
+            offs = np.concatenate([[0], np.cumsum(counts)[:-1]])
+            terms = np.zeros(int(counts.sum()), dtype=nat.MAC_TERM)
+            k = 0
+            for i in idx:
+                for ct, pt in jobs[i]:
+                    if ct.payload.batch != bsz:
+                        raise ValueError("batch mismatch inside accumulation")
+                    terms[k] = (pt.payload.data_ptr(), ct.payload.data.data_ptr())
+                    k += 1
+            outs = _tasks(nat.MAC_OUT, len(idx), dst=dst, nterms=counts, term_off=offs)
+            self.ring.mac_strided(outs, terms, r, 2 * bsz)
+            for q, i in enumerate(idx):
+                t0 = jobs[i][0]
+                out[i] = Ct(CtData(res[q]), lvl, t0[0].scale * t0[1].scale, self.n2)
+        return out
+
+    def _raw_add_each(self, pairs) -> list:
+        out = [None] * len(pairs)
+        for lvl, idx in self._by_level(pairs, lambda p: p[0].level).items():
+            bsz = pairs[idx[0]][0].payload.batch
+            r = lvl + 1
+            res = self.ring.empty(len(idx), bsz, 2, r)
+            rp = self.ring.row_ptrs
+            a = np.concatenate([rp(pairs[i][0].payload.data) for i in idx])
+            b = np.concatenate([rp(pairs[i][1].payload.data) for i in idx])
+            self._ew(nat.EW_ADD, rp(res), a, b, primes=self._row_primes(len(idx) * bsz * 2, r))
+            for q, i in enumerate(idx):
+                out[i] = Ct(CtData(res[q]), lvl, pairs[i][0].scale, self.n2)
+        return out
+
+    def _raw_rescale_each(self, cts) -> list:
+        out = [None] * len(cts)
+        for lvl, idx in self._by_level(cts, lambda c: c.level).items():
+            bsz = cts[idx[0]].payload.batch
+            k = len(idx)
+            rp = self.ring.row_ptrs
+            rows = np.stack([rp(cts[i].payload.data).reshape(bsz * 2, lvl + 1) for i in idx])
+            rows = rows.reshape(k * bsz * 2, lvl + 1)
+            topc = self.ring.empty(k * bsz * 2)
+            self.ring.ntt_inv(_tasks(nat.NTT_TASK, k * bsz * 2, src=rows[:, lvl],
+                                     dst=rp(topc), dst_prime=lvl, src_prime=lvl))
+            res = self.ring.empty(k, bsz, 2, lvl)
+            inv, inv_sh = self._resc[lvl]
+            m = k * bsz * 2
+            t = _tasks(nat.NTT_TASK, m * lvl, src=np.repeat(rp(topc), lvl), dst=rp(res),
+                       aux=rows[:, :lvl].ravel(), src_prime=lvl,
+                       dst_prime=np.tile(np.arange(lvl), m), scal=np.tile(inv, m),
+                       scal_sh=np.tile(inv_sh, m))
+            self.ring.ntt_fwd(t, nat.FWD_MODDOWN)
+            for q, i in enumerate(idx):
+                c = cts[i]
+                out[i] = Ct(CtData(res[q]), lvl - 1, c.scale / self.params.chain_primes[lvl],
+                            self.n2)
+        return out
+
+    def _ks_chunk(self, bsz: int, lvl: int) -> int:
+        per = bsz * (lvl + 1) * (lvl + 2) * self.n * 8
+        return max(1, int(self.ks_budget_bytes // max(per, 1)))
+
+    def _raw_rot_each(self, items) -> list:
+        out = [None] * len(items)
+        for lvl, idx in self._by_level(items, lambda it: it[0].level).items():
+            bsz = items[idx[0]][0].payload.batch
+            step = self._ks_chunk(bsz, lvl)
+            for c0 in range(0, len(idx), step):
+                chunk = idx[c0:c0 + step]
+                c1 = torch.cat([items[i][0].payload.data[:, 1] for i in chunk])
+                de = self._decompose(c1, lvl)
+                jobs = []
+                for q, i in enumerate(chunk):
+                    key, perm, add, g = self._rot_job(*items[i])
+                    jobs.append((key, perm, add, g, q * bsz))
+                res = self._ks_apply_many(de, lvl, jobs, bsz)
+                del de
+                for q, i in enumerate(chunk):
+                    ct = items[i][0]
+                    out[i] = Ct(CtData(res[q]), lvl, ct.scale, self.n2)
+        return out
+
+    def _raw_square_each(self, cts) -> list:
+        out = [None] * len(cts)
+        for lvl, idx in self._by_level(cts, lambda c: c.level).items():
+            bsz = cts[idx[0]].payload.batch
+            r = lvl + 1
+            step = self._ks_chunk(bsz, lvl)
+            rp = self.ring.row_ptrs
+            for c0 in range(0, len(idx), step):
+                chunk = idx[c0:c0 + step]
+                k = len(chunk)
+                d = self.ring.empty(k, bsz, 3, r)
+                xr = np.stack([rp(cts[i].payload.data).reshape(bsz, 2, r) for i in chunk])
+                dr = rp(d).reshape(k, bsz, 3, r)
+                self.ring.tensor(_tasks(
+                    nat.TENSOR_TASK, k * bsz * r, a0=xr[:, :, 0].ravel(), a1=xr[:, :, 1].ravel(),
+                    b0=xr[:, :, 0].ravel(), b1=xr[:, :, 1].ravel(), d0=dr[:, :, 0].ravel(),
+                    d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
+                    prime=self._row_primes(k * bsz, r)))
+                de = self._decompose(d[:, :, 2].reshape(k * bsz, r, self.n), lvl)
+                jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
+                res = self._ks_apply_many(de, lvl, jobs, bsz)
+                del de
+                for q, i in enumerate(chunk):
+                    c = cts[i]
+                    out[i] = Ct(CtData(res[q]), lvl, c.scale * c.scale, self.n2)
+        return out
+
     def _raw_rot_many(self, a: Ct, ks) -> dict:
         if not ks:
             return {}
         lvl = a.level
-        jobs = [self._rot_job(a, k) for k in ks]
         de = self._decompose(a.payload.data[:, 1], lvl)
-        outs = self._ks_apply_many(de, lvl, jobs)
-        return {k: Ct(CtData(o), lvl, a.scale, self.n2) for k, o in zip(ks, outs)}
+        outs = {}
+        step = max(1, self._ks_chunk(a.payload.batch, lvl) * 4)
+        for c0 in range(0, len(ks), step):
+            sub = ks[c0:c0 + step]
+            res = self._ks_apply_many(de, lvl, [self._rot_job(a, k) for k in sub])
+            for k, o in zip(sub, res):
+                outs[k] = Ct(CtData(o), lvl, a.scale, self.n2)
+        return outs
 
     # ------------------------------------------------------------------ host interop
 

@@ -137,6 +137,12 @@ class RingContext:
             nat.check(self._lib.hb_mac(self.handle, _ptr(d), len(tasks), _ptr(t), self.stream),
                       "mac")
 
+    def mac_strided(self, outs: np.ndarray, terms: np.ndarray, rows: int, bc: int):
+        if len(outs):
+            d, t = _upload(outs, self.device), _upload(terms, self.device)
+            nat.check(self._lib.hb_mac_strided(self.handle, _ptr(d), len(outs), _ptr(t), rows, bc,
+                                               self.stream), "mac_strided")
+
     def tensor(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)

@@ -22,6 +22,8 @@ cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
+                               cudaStream_t);
 cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
 struct HbCrtTask;
 cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
@@ -174,6 +176,13 @@ int hb_mac(hb_ring* r, const void* tasks, int count, const void* terms, void* st
   cudaError_t e = launch_mac((const HbMacTask*)tasks, count, (const HbMacTerm*)terms,
                              r->dev.primes, r->dev.n, (cudaStream_t)stream);
   return e ? fail(e, "hb_mac") : 0;
+}
+
+int hb_mac_strided(hb_ring* r, const void* outs, int nout, const void* terms, int rows, int bc,
+                   void* stream) {
+  cudaError_t e = launch_mac_strided(outs, nout, (const HbMacTerm*)terms, r->dev.primes, r->dev.n,
+                                     rows, bc, (cudaStream_t)stream);
+  return e ? fail(e, "hb_mac_strided") : 0;
 }
 
 int hb_tensor(hb_ring* r, const void* tasks, int count, void* stream) {

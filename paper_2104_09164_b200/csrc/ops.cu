@@ -348,3 +348,59 @@ cudaError_t launch_crt_double(const HbCrtTask* tasks, int ntasks, const u64* con
 }
 
 }  // namespace hb
+
+namespace hb {
+
+// ---------------------------------------------------------------------------
+// Strided plaintext multiply-accumulate for a whole layer in one launch.
+// Every output o is a [BC, R, N] block (BC = batch x 2 components) at
+// outs[o].dst; its terms reference plaintext bases (rows r at +r*N) and
+// ciphertext bases with the same [BC, R, N] geometry.  grid.y walks
+// (o, bc, r); the row index is the chain-prime index.
+struct HbMacOut {
+  u64* dst;
+  int nterms;
+  int term_off;
+};
+
+__global__ void __launch_bounds__(EW_THREADS)
+k_mac_strided(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __restrict__ terms,
+              const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  const long long total = (long long)nout * BC * R;
+  for (long long y = blockIdx.y; y < total; y += gridDim.y) {
+    const int o = (int)(y / ((long long)BC * R));
+    const int rem = (int)(y % ((long long)BC * R));
+    const int bc = rem / R, r = rem % R;
+    const HbMacOut ou = outs[o];
+    const HbPrime P = primes[r];
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    const size_t ct_off = ((size_t)bc * R + r) * n + j;
+    const size_t pt_off = (size_t)r * n + j;
+    Acc128 s0, s1;
+    for (int k = 0; k < ou.nterms; ++k) {
+      const HbMacTerm tm = terms[ou.term_off + k];
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(tm.pt + pt_off));
+      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(tm.ct + ct_off));
+      s0.mac(a.x, b.x);
+      s1.mac(a.y, b.y);
+      if ((k & 7) == 7) { s0.fold(P); s1.fold(P); }
+    }
+    ulonglong2 v;
+    v.x = s0.fold(P);
+    v.y = s1.fold(P);
+    *reinterpret_cast<ulonglong2*>(ou.dst + ct_off) = v;
+  }
+}
+
+cudaError_t launch_mac_strided(const void* outs, int nout, const HbMacTerm* terms,
+                               const HbPrime* primes, int n, int R, int BC, cudaStream_t st) {
+  if (nout <= 0) return cudaSuccess;
+  const long long total = (long long)nout * BC * R;
+  dim3 grid((n / 2 + EW_THREADS - 1) / EW_THREADS, total < 65535 ? (int)total : 65535);
+  k_mac_strided<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout, terms,
+                                             primes, n, R, BC);
+  return cudaGetLastError();
+}
+
+}  // namespace hb

@@ -1,0 +1,90 @@
+"""Encrypted HEAR-CNN inference on the GPU engine vs the reference.
+
+Decrypted logits must match the reference CKKS engine's decrypted logits
+(same model/input/key seeds; tests/golden/pipeline_golden.json) within
+1e-3 x logit scale with the same argmax, per-layer operation counters must
+equal the reference's exactly, and batched evaluation must be bit-identical
+to clip-by-clip evaluation.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def pgold():
+    with open(os.path.join(HERE, "golden", "pipeline_golden.json")) as f:
+        return json.load(f)
+
+
+def _run(shape, model_seed, input_seed, prof, mode, strat, backend_seed, batch=None):
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline, infer
+    from paper_2104_09164_b200.model import collapse_layers, make_random_input, make_random_model
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    cpar = collapse_layers(make_random_model(shape, model_seed), shape)
+    be = CkksBackend(gen_params(prof), seed=backend_seed)
+    cp = compile_pipeline(shape, mode, strat, be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    x = make_random_input(shape, input_seed)
+    if batch:
+        x = np.stack([make_random_input(shape, input_seed + i) for i in range(batch)])
+    lg, cnt, enc = infer(cpar, x, mode, strat, be, encoder=ModelEncoder(cp, cpar, be))
+    return lg, cnt, cpar, x, be
+
+
+def _check(lg, gold):
+    ref = np.array(gold["logits"])
+    scale = max(np.abs(ref).max(), 1e-12)
+    assert np.abs(lg - ref).max() <= 1e-3 * scale, (lg, ref)
+    assert int(np.argmax(lg)) == int(np.argmax(ref))
+
+
+def test_toy_network_matches_reference(pgold):
+    from paper_2104_09164_b200.model import NetworkShape
+    g = pgold["ckks"]["toy/fast/giant/toy-fast"]
+    shape = NetworkShape(1, 32, 15, (4, 8, 16), 4)
+    lg, cnt, *_ = _run(shape, 3, 4, "toy-fast", "fast", "giant", 5)
+    _check(lg, g)
+    assert cnt.as_dict() == g["counters"]
+
+
+@pytest.mark.parametrize("key", ["1d-w64/fast/giant/fast-hear", "1d-w64/hear/full/hear"])
+def test_real_params_match_reference(pgold, key):
+    from paper_2104_09164_b200.model import net_by_name
+    net, mode, strat, prof = key.split("/")
+    g = pgold["ckks"][key]
+    lg, cnt, *_ = _run(net_by_name(net), 1, 2, prof, mode, strat, 0)
+    _check(lg, g)
+    assert cnt.as_dict() == g["counters"]
+    clear = np.array(g["clear"])
+    tol = 2.0 ** -9 if mode == "hear" else 2.0 ** -5
+    assert np.abs(lg - clear).max() <= tol
+
+
+def test_batched_equals_clipwise():
+    """B clips in one handle == the same clips one by one (same RNG order)."""
+    from paper_2104_09164_b200.model import NetworkShape
+    shape = NetworkShape(1, 32, 15, (4, 8, 16), 4)
+    lg_b, *_ = _run(shape, 3, 10, "toy-fast", "fast", "baby", 9, batch=3)
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline, encrypt_input, run_pipeline, dec_logits
+    from paper_2104_09164_b200.model import collapse_layers, make_random_input, make_random_model
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    cpar = collapse_layers(make_random_model(shape, 3), shape)
+    be = CkksBackend(gen_params("toy-fast"), seed=9)
+    cp = compile_pipeline(shape, "fast", "baby", be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    enc = ModelEncoder(cp, cpar, be)
+    cts = [encrypt_input(make_random_input(shape, 10 + i), cp, be) for i in range(3)]
+    outs = [dec_logits(run_pipeline(enc, c, be), cp, be) for c in cts]
+    assert np.array_equal(np.stack(outs), lg_b)
