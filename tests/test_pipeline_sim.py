@@ -1,0 +1,88 @@
+"""Network schedule on the exact slot simulator (CPU): equivalence with the
+cleartext network and with the reference's simulator logits, and exact
+per-layer operation counters against the reference (pipeline_golden.json)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.slotsim import SimBackend
+from paper_2104_09164_b200.ckks.params import gen_params
+from paper_2104_09164_b200.fastpath import compile_pipeline, infer
+from paper_2104_09164_b200.model import (collapse_layers, infer_clear, make_random_input,
+                                         make_random_model, net_by_name)
+from paper_2104_09164_b200.modelenc import ModelEncoder
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+with open(os.path.join(HERE, "golden", "pipeline_golden.json")) as _f:
+    GOLD = json.load(_f)
+
+CASES = [(net, mode, strat) for net in ("1d-w64", "1d-w128", "2d-w64")
+         for mode in ("hear", "fast") for strat in ("full", "giant", "baby")]
+
+
+@pytest.mark.parametrize("net,mode,strat", CASES)
+def test_sim_matches_reference(net, mode, strat):
+    g = GOLD["sim"][f"{net}/{mode}/{strat}"]
+    shape = net_by_name(net)
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    x = make_random_input(shape, 2)
+    be = SimBackend(gen_params("hear" if mode == "hear" else "fast-hear"))
+    lg, cnt, _ = infer(cpar, x, mode, strat, be)
+    assert np.abs(lg - infer_clear(cpar, x)).max() <= 1e-9
+    assert np.abs(lg - np.array(g["logits"])).max() <= 1e-9
+    assert np.allclose(infer_clear(cpar, x), g["clear"], atol=1e-12)
+    assert cnt.as_dict() == g["counters"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", ["hear", "fast"])
+def test_sim_2d_w128(mode):
+    g = GOLD["sim"][f"2d-w128/{mode}/giant"]
+    shape = net_by_name("2d-w128")
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    x = make_random_input(shape, 2)
+    be = SimBackend(gen_params("hear" if mode == "hear" else "fast-hear"))
+    lg, cnt, _ = infer(cpar, x, mode, "giant", be)
+    assert cnt.as_dict() == g["counters"]
+    assert np.abs(lg - infer_clear(cpar, x)).max() <= 1e-9
+
+
+def test_table_viii_totals():
+    """2D-CNN-W128 Fast-HEAR: Mult = 56, Rescale = 172 (paper Table VIII)."""
+    c = GOLD["sim"]["2d-w128/fast/giant"]["counters"]
+    tot = {k: sum(row[k] for row in c.values()) for k in next(iter(c.values()))}
+    assert tot["mult"] == 56 and tot["rescale"] == 172
+
+
+def test_batched_sim_equals_clipwise():
+    shape = net_by_name("1d-w64")
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    xs = np.stack([make_random_input(shape, 5 + i) for i in range(3)])
+    be = SimBackend(gen_params("fast-hear"))
+    lg, *_ = infer(cpar, xs, "fast", "giant", be)
+    for i in range(3):
+        one, *_ = infer(cpar, xs[i], "fast", "giant", SimBackend(gen_params("fast-hear")))
+        assert np.abs(lg[i] - one).max() <= 1e-12
+
+
+@pytest.mark.parametrize("key", sorted(GOLD["storage"]))
+def test_level_aware_storage(key):
+    net, mode = key.split("/")
+    prof = "hear" if mode == "hear" else "fast-hear"
+    shape = net_by_name(net)
+    cp = compile_pipeline(shape, mode, "giant", gen_params(prof))
+    rep = ModelEncoder(cp, collapse_layers(make_random_model(shape, 1), shape),
+                       SimBackend(gen_params(prof))).storage_report()
+    assert rep == GOLD["storage"][key]
+    assert rep["ratio"] < 0.6
+
+
+def test_ladders():
+    cp = compile_pipeline(net_by_name("2d-w128"), "hear", "giant", gen_params("hear"))
+    assert cp.ladder_levels() == [10, 9, 8, 7, 7, 6, 5, 4, 4, 3, 2, 1, 0]
+    cp = compile_pipeline(net_by_name("2d-w128"), "fast", "giant", gen_params("fast-hear"))
+    assert cp.ladder_levels()[0] == 12 and cp.ladder_levels()[-1] == 0
+    assert cp.expected("merge2").level == 8 and cp.expected("merge3").level == 4
