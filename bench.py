@@ -1,0 +1,339 @@
+"""Encrypted HEAR-CNN inference benchmark (B200 engine vs the CPU reference arm).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--net 1d-w64] [--mode fast] [--strategy giant] [--batch B]
+
+One step = one pass of the encrypted network over a batch of B synthetic
+clips per GPU (weak scaling: clips are partitioned across ranks, evaluation
+keys are generated on rank 0 and broadcast once at setup, no collectives in
+the per-clip loop).  Rank 0 prints one JSON line.
+
+  value  encrypted inferences/s over all ranks, inputs already resident in HBM
+  e2e    same metric through the public API with host buffers: every step copies
+         the encrypted clips host->device (pinned) and the encrypted logits
+         device->host
+Synthetic data: inputs uniform[0,1) 32x15x2 from seeds, random-init weights of
+the named reference network (no datasets or checkpoints on the box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--net", default="1d-w64")
+    ap.add_argument("--mode", default="fast", choices=["fast", "hear"])
+    ap.add_argument("--strategy", default="giant", choices=["full", "giant", "baby"])
+    ap.add_argument("--batch", type=int, default=64, help="clips per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--roofline-only", action="store_true")
+    return ap.parse_args()
+
+
+def profile_of(mode: str) -> str:
+    return "fast-hear" if mode == "fast" else "hear"
+
+
+def metric_name() -> str:
+    return "encrypted HEAR-CNN inferences/sec"
+
+
+# ---------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- CPU arm
+
+def cpu_oracle_run(args, n_clips: int, warm: int = 0):
+    """Time the CPU oracle (oracle/, C + OpenMP port of the reference engine)
+    on `n_clips` single-clip inferences.  Returns (clips/s, threads, per-clip s)."""
+    from oracle.cpu_engine import OracleCkks, lib
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline, encrypt_input, run_pipeline
+    from paper_2104_09164_b200.model import collapse_layers, make_random_input, make_random_model
+    from paper_2104_09164_b200.model import net_by_name
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    shape = net_by_name(args.net)
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    be = OracleCkks(gen_params(profile_of(args.mode)), seed=0)
+    cp = compile_pipeline(shape, args.mode, args.strategy, be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    enc = ModelEncoder(cp, cpar, be)
+    cts = [encrypt_input(make_random_input(shape, 1000 + i), cp, be) for i in range(warm + n_clips)]
+    for i in range(warm):
+        run_pipeline(enc, cts[i], be)
+    t0 = time.perf_counter()
+    for i in range(warm, warm + n_clips):
+        run_pipeline(enc, cts[i], be)
+    dt = time.perf_counter() - t0
+    return n_clips / dt, int(lib().or_num_threads()), dt / max(n_clips, 1)
+
+
+def reference_arm(args):
+    from paper_2104_09164_b200.parallel import world
+    rank, ws, _ = world()
+    if rank != 0:
+        return
+    value, cores, per_clip = cpu_oracle_run(args, args.steps, warm=args.warmup)
+    sample = (f"{args.steps} timed single-clip encrypted inferences ({args.warmup} warm-up) of "
+              f"{args.net}/{args.mode}/{args.strategy} at {profile_of(args.mode)} parameters")
+    line = {
+        "metric": metric_name(), "value": value, "unit": "inferences/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_clip * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"HEAR CNN {args.net} {args.mode}/{args.strategy}, "
+                   f"{profile_of(args.mode)} params, 1 clip per step on the host CPU",
+                   "net": args.net, "mode": args.mode, "strategy": args.strategy,
+                   "params": profile_of(args.mode), "clips_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
+    """Time the key-switch ModUp NTT launch (FWD_LIFT over B*(l+1)*(l+2) rows,
+    the most-launched-work kernel of the evaluation) with CUDA events on its
+    own stream and report it against the measured HBM peak."""
+    import torch
+    from paper_2104_09164_b200 import _native as nat
+    from paper_2104_09164_b200.ckks.engine import _tasks
+    from paper_2104_09164_b200.ckks.ring import _upload
+    n = be.n
+    ndig, rows = lvl + 1, lvl + 2
+    coef = be.ring.empty(bsz, ndig)
+    coef.random_(0, 1 << 30)
+    de = be.ring.empty(bsz, ndig, rows)
+    gidx = np.array(list(range(lvl + 1)) + [be.S])
+    t = _tasks(nat.NTT_TASK, bsz * ndig * rows, src=np.repeat(be.ring.row_ptrs(coef), rows),
+               dst=be.ring.row_ptrs(de), src_prime=np.tile(np.repeat(np.arange(ndig), rows), bsz),
+               dst_prime=np.tile(gidx, bsz * ndig))
+    d = _upload(t, be.dev)
+    L = nat.lib()
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_LIFT, st.cuda_stream), "ntt")
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_LIFT, st.cuda_stream), "ntt")
+    e1.record(st)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / reps
+    out_rows = len(t)
+    # algorithmic bytes: each output row written once, each digit row read once
+    algo = (out_rows + bsz * ndig) * n * 8
+    gbs = algo / sec / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    butterflies = out_rows * (n // 2) * (n.bit_length() - 1)
+    return {"kernel": "k_ntt_fwd<FWD_LIFT> (key-switch ModUp)", "bound": "hbm",
+            "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "traffic": None, "launch_us": round(sec * 1e6, 2), "rows_per_launch": out_rows,
+            "algorithmic_bytes_per_launch": algo,
+            "butterflies_per_s": round(butterflies / sec / 1e12, 3),
+            "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
+
+
+def gpu_arm(args):
+    import torch
+    from paper_2104_09164_b200 import _native as nat
+    from paper_2104_09164_b200 import parallel as par
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import (compile_pipeline, dec_logits, encrypt_input,
+                                                run_pipeline)
+    from paper_2104_09164_b200.model import (collapse_layers, infer_clear, make_random_input,
+                                             make_random_model, net_by_name)
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    from paper_2104_09164_b200.backend import Ct
+    from paper_2104_09164_b200.ckks.engine import CtData
+
+    rank, ws, local = par.world()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    par.init("nccl")
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+
+    params = gen_params(profile_of(args.mode))
+    shape = net_by_name(args.net)
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    cp = compile_pipeline(shape, args.mode, args.strategy, params)
+    be = CkksBackend(params, seed=0, device=dev, keygen=(rank == 0))
+    if rank == 0:
+        be.ensure_rotation_keys(cp.rotations)
+    par.replicate_keys(be, src=0)
+    enc = ModelEncoder(cp, cpar, be).prepare()
+    bsz = args.batch
+    seeds = [10_000 * (rank + 1) + i for i in range(bsz)]
+    x = np.stack([make_random_input(shape, s) for s in seeds])
+    ct = encrypt_input(x, cp, be)
+    host_in = ct.payload.data.cpu().pin_memory()
+    out0 = run_pipeline(enc, ct, be)
+    host_out = torch.empty(out0.payload.data.shape, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    maxerr = None
+    if rank == 0:
+        lg = dec_logits(out0, cp, be)
+        ref = np.stack([infer_clear(cpar, xi) for xi in x])
+        maxerr = float(np.abs(lg - ref).max())
+
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        run_pipeline(enc, ct, be)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    par.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = nat.launch_count
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            run_pipeline(enc, ct, be)
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = nat.launch_count - l0
+    par.barrier()
+    ms = par.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+
+    # ---- end-to-end timed region (host buffers, copies inside)
+    par.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(st)
+    for _ in range(args.steps):
+        d_in = host_in.to(dev, non_blocking=True)
+        out = run_pipeline(enc, Ct(CtData(d_in), ct.level, ct.scale, ct.slots), be)
+        host_out.copy_(out.payload.data, non_blocking=True)
+    f1.record(st)
+    torch.cuda.synchronize()
+    par.barrier()
+    ms_e2e = par.max_over_ranks(f0.elapsed_time(f1) / args.steps, dev)
+
+    roof = dominant_kernel_roofline(be, lvl=6, bsz=min(bsz, 16), peaks=peaks)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, per_clip = cpu_oracle_run(args, 1)
+            cpu = {"value": v, "unit": "inferences/s", "cores": cores, "kind": "port",
+                   "sample": f"1 single-clip encrypted inference of {args.net}/{args.mode}/"
+                             f"{args.strategy} ({per_clip:.1f} s) on the oracle C/OpenMP port"}
+        except Exception as exc:  # the oracle must not break the GPU number
+            cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(),
+                   "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        total = bsz * ws
+        line = {
+            "metric": metric_name(), "value": total / (ms / 1e3), "unit": "inferences/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": f"HEAR CNN {args.net} {args.mode}/{args.strategy}, "
+                       f"{params.name} params (N=2^{params.n.bit_length() - 1}, L={params.max_level}),"
+                       f" {bsz} clips per GPU per step", "net": args.net, "mode": args.mode,
+                       "strategy": args.strategy, "params": params.name, "clips_per_gpu": bsz,
+                       "global_clips_per_step": total, "parallelism": f"clip-sharded dp{ws}",
+                       "l2": "working set (keys + plaintexts + ciphertexts) >> 126 MB L2",
+                       "latency_ms_per_batch": ms, "decrypt_max_abs_err_vs_clear": maxerr},
+            "e2e": {"value": total / (ms_e2e / 1e3), "unit": "inferences/s",
+                    "h2d_bytes_per_step": int(host_in.numel() * 8),
+                    "d2h_bytes_per_step": int(host_out.numel() * 8)},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    par.barrier()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

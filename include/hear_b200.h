@@ -1,0 +1,107 @@
+/*
+ * hear_b200.h -- C ABI of the B200 kernels behind HEAR's RNS-CKKS hot path.
+ *
+ * Library: paper_2104_09164_b200/lib/libhear_b200.so (sm_100a).  Plain
+ * pointers and sizes only.  Two families:
+ *
+ *  hear_*  reference-shaped, HOST-buffer entry points.  Same argument meaning
+ *          as the numba kernels of hear/ckks/ring.py that they replace: an
+ *          (nrows, N) uint64 row-major array plus a per-row global prime index
+ *          (chain primes 0..L, then the special prime).  Each call copies in,
+ *          runs on the GPU, copies out, synchronises; returns 0 on success.
+ *          Binding recipe for the reference: INTEGRATION.md.
+ *
+ *  hb_*    device-pointer entry points used by the Python engine
+ *          (paper_2104_09164_b200/ckks/engine.py).  Work is described by task
+ *          tables resident in device memory (layouts: csrc/ring.cuh) and is
+ *          enqueued asynchronously on `stream` (a cudaStream_t, may be 0).
+ *          Return 0 or a cudaError_t code; hb_last_error() has the text.
+ *
+ * Residues are canonical (in [0, p)), so every kernel's output is
+ * bit-identical to the reference's integer arithmetic on the same inputs
+ * (after the two ring-table corrections documented in DESIGN.md §2).
+ */
+#ifndef HEAR_B200_H
+#define HEAR_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hb_ring hb_ring; /* per-parameter-set tables on the GPU   */
+typedef struct hb_fft hb_fft;   /* canonical-embedding FFT tables        */
+
+/* ---- library / context -------------------------------------------------- */
+const char* hb_last_error(void);
+int hb_version(void);
+
+/* Replaces hear/ckks/ring.py:253-292 RingContext table construction.
+ * primes[nprimes] (< 2^62, = 1 mod 2N); psi/ipsi: [nprimes][N] bit-reversed
+ * powers of the primitive 2N-th root and of its inverse. NULL on failure. */
+hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
+                        const unsigned long long* psi, const unsigned long long* ipsi);
+void hb_ring_destroy(hb_ring* ring);
+int hb_ring_prime_consts(const hb_ring* ring, int prime_index, unsigned long long* out8);
+int hb_sizeof_task(int kind); /* 0 ntt, 1 ew, 2 mac, 3 mac-term, 4 ks */
+
+/* ---- reference-shaped host-buffer kernels (hear/ckks/ring.py) ------------ */
+/* ring.py:113 ntt_fwd(a, gidx, psi, psish, p) -- in place                     */
+int hear_ntt_fwd(hb_ring* ring, unsigned long long* a, int nrows, const long long* gidx);
+/* ring.py:120 ntt_inv(a, gidx, ipsi, ipsish, p, ninv, ninvsh) -- in place     */
+int hear_ntt_inv(hb_ring* ring, unsigned long long* a, int nrows, const long long* gidx);
+/* ring.py:127 pw_mul(out, a, b, gidx, p, mu, sh)                              */
+int hear_pw_mul(hb_ring* ring, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx);
+/* ring.py:159 pw_add(out, a, b, gidx, p)                                      */
+int hear_pw_add(hb_ring* ring, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx);
+/* ring.py:167 pw_sub(out, a, b, gidx, p)                                      */
+int hear_pw_sub(hb_ring* ring, unsigned long long* out, const unsigned long long* a,
+                const unsigned long long* b, int nrows, const long long* gidx);
+
+/* ---- device task-table kernels --------------------------------------------- */
+/* Forward NTT over `count` row tasks (HbNttTask).  mode 0: plain
+ * (ring.py:113); 1: fused centred lift + reduce of a digit row, the ModUp of
+ * engine.py:290-303 (ring.py:186-207 + 113); 2: ModUp + sub_scaled_inv +
+ * optional Galois-gathered addend, the ModDown / rescale of
+ * engine.py:213-227, 263-281, 350; 3: signed int64 coefficients
+ * (engine.py:84-88 _coeffs_to_ntt). */
+int hb_ntt_fwd(hb_ring* ring, const void* tasks, int count, int mode, void* stream);
+/* Inverse NTT over row tasks (ring.py:120, true inverse twiddles).            */
+int hb_ntt_inv(hb_ring* ring, const void* tasks, int count, void* stream);
+/* Element-wise op `op` over HbEwTask rows: 0 add (ring.py:159), 1 sub
+ * (ring.py:167), 2 mul (ring.py:127), 3 scalar mul (ring.py:175), 4 a*b+c
+ * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,
+ * 8 (a-b)*c (ring.py:210).                                                   */
+int hb_ew(hb_ring* ring, int op, const void* tasks, int count, void* stream);
+/* Plaintext multiply-accumulate rows: sum_t pt_t * ct_t (the mult_plain/add
+ * chains of hear/convolution.py:276-312, fastpath.py:168-180).               */
+int hb_mac(hb_ring* ring, const void* tasks, int count, const void* terms, void* stream);
+/* Same, one launch per layer over [B*2, rows, N] ciphertext blocks.          */
+int hb_mac_strided(hb_ring* ring, const void* outs, int nout, const void* terms, int rows,
+                   int bc, void* stream);
+/* Ciphertext tensor product d0, d1, d2 (engine.py:249-257).                  */
+int hb_tensor(hb_ring* ring, const void* tasks, int count, void* stream);
+/* Key-switch inner product with the fused Galois gather
+ * (ring.py:136-156 pw_mul_accum_perm).                                       */
+int hb_ks_inner(hb_ring* ring, const void* tasks, int count, void* stream);
+/* Exact CRT of `keep` coefficient rows to centred doubles (engine.py:156-175). */
+int hb_crt_double(hb_ring* ring, const void* tasks, int count, const unsigned long long* consts,
+                  const int* prime_idx, int keep, int nl, void* stream);
+
+/* ---- canonical-embedding codec (hear/ckks/encoder.py) ------------------------ */
+hb_fft* hb_fft_create(int logn2, const double* root_re_im, const double* twist_re_im,
+                      const int* slot_pos);
+void hb_fft_destroy(hb_fft* fft);
+/* encoder.py:48-56 encode_coeffs: slots [npoly][N/2] -> rint(coeffs*scale)
+ * [npoly][N] int64; *overflow set when |coeff| >= 2^52.                      */
+int hb_encode(hb_fft* fft, const double* slots, long long* coeffs, int npoly, double scale,
+              int* overflow, void* stream);
+/* encoder.py:59-60 decode_coeffs: coeffs [npoly][N] -> real slots / scale.    */
+int hb_decode(hb_fft* fft, const double* coeffs, double* slots, int npoly, double scale,
+              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEAR_B200_H */

@@ -62,7 +62,13 @@ def lib():
     return _lib
 
 
+launch_count = 0   # kernel launches issued through this binding (one per hb_* call)
+
+
 def check(rc: int, what: str):
+    """Verify one hb_* launch call and count it."""
+    global launch_count
+    launch_count += 1
     if rc != 0:
         msg = _lib.hb_last_error().decode() if _lib is not None else "?"
         raise NativeError(f"{what} failed ({rc}): {msg}")

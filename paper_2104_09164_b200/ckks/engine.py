@@ -98,7 +98,7 @@ class CkksBackend(BackendBase):
 
     exact = False
 
-    def __init__(self, params: ParameterSet, seed: int = 0, device=None):
+    def __init__(self, params: ParameterSet, seed: int = 0, device=None, keygen: bool = True):
         super().__init__(params)
         self.ring = RingContext(params, device)
         self.dev = self.ring.device
@@ -121,7 +121,34 @@ class CkksBackend(BackendBase):
             self._resc.append((inv, shoup_np(inv, ps) if lvl else inv))
         self._crt_cache: dict = {}
         self.keys = KeyMaterial()
-        self._keygen()
+        if keygen:
+            self._keygen()
+
+    # ------------------------------------------------------------------ key transport
+
+    def key_tensors(self) -> list:
+        """Ordered (name, tensor) list of the public evaluation material, for
+        replication to other ranks (bench.py broadcasts it over NCCL)."""
+        k = self.keys
+        out = [("pk_b", k.pk_b), ("pk_a", k.pk_a), ("relin_b", k.relin.b),
+               ("relin_a", k.relin.a)]
+        for amt in sorted(k.rot):
+            out += [(f"rot{amt}_b", k.rot[amt].b), (f"rot{amt}_a", k.rot[amt].a)]
+        return out
+
+    def key_manifest(self) -> list:
+        """[(amount, lmax)] of the rotation keys (shapes follow from it)."""
+        return [(a, self.keys.rot[a].lmax) for a in sorted(self.keys.rot)]
+
+    def alloc_keys(self, manifest):
+        """Allocate empty evaluation keys of the given layout (receiver side)."""
+        k = self.keys
+        full = self.L + 2
+        k.pk_b, k.pk_a = self.ring.empty(full), self.ring.empty(full)
+        k.relin = _Ksk(self.ring.empty(self.L + 1, full), self.ring.empty(self.L + 1, full), self.L)
+        for amt, lmax in manifest:
+            k.rot[amt] = _Ksk(self.ring.empty(lmax + 1, lmax + 2),
+                              self.ring.empty(lmax + 1, lmax + 2), lmax)
 
     # ------------------------------------------------------------------ sampling
 
