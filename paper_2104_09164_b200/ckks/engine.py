@@ -473,7 +473,7 @@ class CkksBackend(BackendBase):
                    d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
                    prime=self._row_primes(bsz, r))
         self.ring.tensor(t)
-        de = self._decompose(d[:, 2].contiguous(), lvl)
+        de = self._decompose(dr[:, 2], lvl)
         out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
@@ -497,19 +497,40 @@ class CkksBackend(BackendBase):
 
     # ------------------------------------------------------------------ key switching
 
-    def _decompose(self, d: torch.Tensor, lvl: int) -> torch.Tensor:
-        """Digits of d [B, lvl+1, N] extended to chain rows 0..lvl plus the
-        special prime: de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303)."""
-        bsz = d.shape[0]
+    def _decompose(self, d, lvl: int) -> torch.Tensor:
+        """Digits of d extended to chain rows 0..lvl plus the special prime:
+        de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303).
+
+        d: tensor [B, lvl+1, N] (any strides between clips) or a uint64
+        pointer array [B, lvl+1] of NTT-form rows.  Row i of digit i is the
+        input row itself (the lift of a residue re-reduced under its own
+        prime is the residue), so it is copied instead of transformed."""
+        if isinstance(d, torch.Tensor):
+            if d.stride(-1) != 1 or d.stride(-2) != self.n:
+                d = d.contiguous()
+            ptrs = (np.uint64(d.data_ptr()) + np.uint64(8) * (
+                np.arange(d.shape[0], dtype=np.uint64)[:, None] * np.uint64(d.stride(0))
+                + np.arange(d.shape[1], dtype=np.uint64)[None, :] * np.uint64(self.n)))
+        else:
+            ptrs = np.asarray(d, dtype=np.uint64)
+        bsz = ptrs.shape[0]
         ndig, rows = lvl + 1, lvl + 2
-        coef = self._intt_rows(d.contiguous(), self._row_primes(bsz, ndig))
+        rp = self.ring.row_ptrs
+        coef = self.ring.empty(bsz, ndig)
+        prim = self._row_primes(bsz, ndig)
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                 dst_prime=prim, src_prime=prim))
         de = self.ring.empty(bsz, ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
-        src = np.repeat(self.ring.row_ptrs(coef), rows)
-        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, bsz * ndig * rows, src=src,
-                                 dst=self.ring.row_ptrs(de),
-                                 src_prime=np.tile(np.repeat(np.arange(ndig), rows), bsz),
-                                 dst_prime=np.tile(gidx, bsz * ndig)), nat.FWD_LIFT)
+        src = np.repeat(rp(coef), rows)
+        dst = rp(de)
+        sp = np.tile(np.repeat(np.arange(ndig), rows), bsz)
+        dp = np.tile(gidx, bsz * ndig)
+        ident = sp == np.tile(np.tile(np.arange(rows), ndig), bsz)
+        lift = ~ident
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, int(lift.sum()), src=src[lift], dst=dst[lift],
+                                 src_prime=sp[lift], dst_prime=dp[lift]), nat.FWD_LIFT)
+        self._ew(nat.EW_COPY, dst[ident], ptrs.ravel(), primes=prim)
         return de
 
     def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None) -> list:
@@ -551,10 +572,14 @@ class CkksBackend(BackendBase):
                     perms[j, :, 0] = perm.data_ptr()
         self.ring.ks_inner(np.concatenate(parts))
         m, r = nj * bsz * 2, lvl + 1
-        spc = self._intt_rows(ip[:, lvl + 1].contiguous(), np.full(m, self.S))
+        iprows = rp(ip).reshape(m, rows)
+        spc = self.ring.empty(m)
+        sprime = np.full(m, self.S)
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=iprows[:, lvl + 1], dst=rp(spc),
+                                 dst_prime=sprime, src_prime=sprime))
         out = self.ring.empty(m, r)
-        aux = ip[:, :r].contiguous()
-        t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out), aux=rp(aux),
+        t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out),
+                   aux=iprows[:, :r].ravel(),
                    src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
                    scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
                    add=add.ravel(), perm=perms.ravel())
@@ -666,7 +691,9 @@ class CkksBackend(BackendBase):
             step = self._ks_chunk(bsz, lvl)
             for c0 in range(0, len(idx), step):
                 chunk = idx[c0:c0 + step]
-                c1 = torch.cat([items[i][0].payload.data[:, 1] for i in chunk])
+                c1 = np.concatenate([
+                    self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
+                    for i in chunk])
                 de = self._decompose(c1, lvl)
                 jobs = []
                 for q, i in enumerate(chunk):
@@ -697,7 +724,7 @@ class CkksBackend(BackendBase):
                     b0=xr[:, :, 0].ravel(), b1=xr[:, :, 1].ravel(), d0=dr[:, :, 0].ravel(),
                     d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
                     prime=self._row_primes(k * bsz, r)))
-                de = self._decompose(d[:, :, 2].reshape(k * bsz, r, self.n), lvl)
+                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de

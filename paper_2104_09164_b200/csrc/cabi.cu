@@ -11,6 +11,7 @@
 //            launch, copy out and synchronise.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,6 +41,8 @@ struct hb_ring {
   HbPrime* primes_dev;
   HbTw* tw_fwd_dev;
   HbTw* tw_inv_dev;
+  HbTwD* twd_fwd_dev;
+  HbTwD* twd_inv_dev;
   std::vector<HbPrime> primes_host;
   int last_err;
 };
@@ -73,6 +76,9 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   const int n = 1 << logn;
   hb_ring* r = new hb_ring();
   memset(&r->dev, 0, sizeof(r->dev));
+  r->primes_dev = nullptr;
+  r->tw_fwd_dev = r->tw_inv_dev = nullptr;
+  r->twd_fwd_dev = r->twd_inv_dev = nullptr;
   r->dev.logn = logn;
   r->dev.n = n;
   r->dev.nprimes = nprimes;
@@ -101,15 +107,29 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
     P.ninv = (unsigned long long)acc;
     P.ninv_sh = shoup(P.ninv, p);
     P.half = p >> 1;
+    P.pd = (double)p;
+    P.pinv = 1.0 / (double)p;
+    P.ninvd = (double)P.ninv;
+    P.ninvq = (double)P.ninv / (double)p;
   }
+  bool f64 = true;
+  for (int i = 0; i < nprimes; ++i) f64 = f64 && primes[i] < (1ull << 42);
+  const char* force = getenv("HEAR_B200_INT_NTT");
+  r->dev.use_f64 = (f64 && !(force && force[0] == '1')) ? 1 : 0;
   std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
+  std::vector<HbTwD> tfd((size_t)nprimes * n), tid((size_t)nprimes * n);
   for (int i = 0; i < nprimes; ++i) {
+    const double pd = (double)primes[i];
     for (int j = 0; j < n; ++j) {
       const size_t k = (size_t)i * n + j;
       tf[k].w = psi[k];
       tf[k].wsh = shoup(psi[k], primes[i]);
       ti[k].w = ipsi[k];
       ti[k].wsh = shoup(ipsi[k], primes[i]);
+      tfd[k].w = (double)psi[k];
+      tfd[k].wq = (double)psi[k] / pd;
+      tid[k].w = (double)ipsi[k];
+      tid[k].wq = (double)ipsi[k] / pd;
     }
   }
   cudaError_t e;
@@ -119,7 +139,11 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
       (e = cudaMemcpy(r->primes_dev, r->primes_host.data(), sizeof(HbPrime) * nprimes,
                       cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(r->tw_fwd_dev, tf.data(), sizeof(HbTw) * tf.size(), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(r->tw_inv_dev, ti.data(), sizeof(HbTw) * ti.size(), cudaMemcpyHostToDevice))) {
+      (e = cudaMemcpy(r->tw_inv_dev, ti.data(), sizeof(HbTw) * ti.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMalloc(&r->twd_fwd_dev, sizeof(HbTwD) * tfd.size())) ||
+      (e = cudaMalloc(&r->twd_inv_dev, sizeof(HbTwD) * tid.size())) ||
+      (e = cudaMemcpy(r->twd_fwd_dev, tfd.data(), sizeof(HbTwD) * tfd.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(r->twd_inv_dev, tid.data(), sizeof(HbTwD) * tid.size(), cudaMemcpyHostToDevice))) {
     fail(e, "hb_ring_create");
     delete r;
     return nullptr;
@@ -127,6 +151,8 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.primes = r->primes_dev;
   r->dev.tw_fwd = r->tw_fwd_dev;
   r->dev.tw_inv = r->tw_inv_dev;
+  r->dev.twd_fwd = r->twd_fwd_dev;
+  r->dev.twd_inv = r->twd_inv_dev;
   return r;
 }
 
@@ -135,13 +161,15 @@ void hb_ring_destroy(hb_ring* r) {
   cudaFree(r->primes_dev);
   cudaFree(r->tw_fwd_dev);
   cudaFree(r->tw_inv_dev);
+  cudaFree(r->twd_fwd_dev);
+  cudaFree(r->twd_inv_dev);
   delete r;
 }
 
 // Per-prime constants as the kernels see them (host copy, for tests).
 int hb_ring_prime_consts(const hb_ring* r, int i, unsigned long long* out8) {
   if (!r || i < 0 || i >= r->dev.nprimes) return -1;
-  memcpy(out8, &r->primes_host[i], sizeof(HbPrime));
+  memcpy(out8, &r->primes_host[i], 8 * sizeof(unsigned long long));  // integer constants
   return 0;
 }
 

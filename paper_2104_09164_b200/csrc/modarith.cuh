@@ -25,7 +25,50 @@ struct HbPrime {
   u64 ninv;     // N^-1 mod p
   u64 ninv_sh;  // Shoup companion of ninv
   u64 half;     // p >> 1, threshold of the centred lift
+  // fp64-pipe arithmetic (used when every prime of the ring is < 2^42)
+  double pd;    // p as a double (exact)
+  double pinv;  // fl(1/p)
+  double ninvd; // N^-1 mod p as a double
+  double ninvq; // fl(ninv / p)
 };
+
+// ---------------------------------------------------------------------------
+// fp64-pipe modular arithmetic for p < 2^42.
+//
+// Residues are integer-valued doubles in a balanced range; a product a*w is
+// split error-free into hi + lo (hi = fl(aw), lo = fma(a, w, -hi)), the
+// quotient q = round(a * fl(w/p)) comes from one fma against 1.5*2^52, and
+// r = fma(-q, p, hi) + lo is computed exactly (all intermediate integers are
+// below 2^53), giving r = a*w mod p with |r| <= (1/2 + 2^-7) p for any
+// |a| <= 2^45.  Six fp64 ops, no integer multiplies: the fp64 pipe of B200
+// sustains ~2.6x the 64-bit-Shoup rate of the integer pipe (measured, see
+// DESIGN.md), and it is otherwise idle in this workload.
+#define HB_RND_MAGIC 6755399441055744.0  // 1.5 * 2^52
+
+HB_DEV double fmod_mul(double a, double w, double wq, double p) {
+  const double hi = a * w;
+  const double lo = __fma_rn(a, w, -hi);
+  const double q = __fma_rn(a, wq, HB_RND_MAGIC) - HB_RND_MAGIC;
+  return __fma_rn(-q, p, hi) + lo;
+}
+
+// |x| <= 2^51 -> x mod p in (-(1/2 + eps) p, (1/2 + eps) p)
+HB_DEV double fmod_reduce(double x, double p, double pinv) {
+  const double q = __fma_rn(x, pinv, HB_RND_MAGIC) - HB_RND_MAGIC;
+  return __fma_rn(-q, p, x);
+}
+
+// balanced residue -> canonical u64 in [0, p)
+HB_DEV u64 fmod_canon(double x, double p, double pinv) {
+  double r = fmod_reduce(x, p, pinv);
+  if (r < 0.0) r += p;
+  return (u64)__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull;
+}
+
+// canonical u64 (< 2^52) -> double, exact, without the conversion pipe
+HB_DEV double u64_to_f(u64 x) {
+  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
+}
 
 HB_DEV u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
 

@@ -2,25 +2,29 @@
 //
 // Computes exactly the transform of hear/ckks/ring.py:71-124 (Cooley-Tukey
 // forward with bit-reversed psi powers, Gentleman-Sande inverse), so outputs
-// are bit-identical residues; the inverse uses the true inverse twiddles
-// psi^-brv(j) (ring.py:282 has an off-by-one exponent).
+// are bit-identical canonical residues; the inverse uses the true inverse
+// twiddles psi^-brv(j) (ring.py:282 has an off-by-one exponent).
 //
 // Schedule (B200): the whole row lives in shared memory (<= 128 KB), each of
 // the N/16 threads owns 16 elements and runs 4 butterfly stages per round in
-// registers (Harvey lazy reduction, values in [0,4p)), so a 2^14 transform
-// is 4 register rounds with 3 shared-memory exchanges instead of 14 stage
-// barriers.  The first forward round reads global memory directly
-// (coalesced: lanes own consecutive columns); the last (contiguous) round
-// goes through a swizzled shared-memory stage so the store to HBM is
-// coalesced too.  Swizzle sw(j) = j ^ ((j>>4)&15) makes both the strided
-// (t >= 16) and the contiguous (16 per thread) access patterns conflict-free.
+// registers, so a 2^14 transform is 4 register rounds with 3 shared-memory
+// exchanges instead of 14 stage barriers.  The first forward round reads
+// global memory directly (coalesced: lanes own consecutive columns); the last
+// (contiguous) round goes through a swizzled shared-memory stage so the HBM
+// store is coalesced too.  Swizzle sw(j) = j ^ ((j>>4)&15) makes both the
+// strided (t >= 16) and the contiguous (16 per thread) phases conflict-free.
+//
+// Arithmetic policies (chosen per ring on the host):
+//   F64  all primes < 2^42: butterflies on the fp64 pipe (modarith.cuh
+//        fmod_mul: 6 fp64 ops, balanced residues, no integer multiplies);
+//   U64  otherwise: Harvey lazy butterflies with 64-bit Shoup products.
+// Both produce the same canonical residues.
 #include "ring.cuh"
 
 namespace hb {
 
 HB_DEV int sw(int j) { return j ^ ((j >> 4) & 15); }
 
-// Fused input/epilogue modes of the forward transform.
 enum FwdMode : int {
   FWD_PLAIN = 0,     // src canonical mod dst prime
   FWD_LIFT = 1,      // src mod src_prime: centred lift then reduce (ModUp digit)
@@ -28,25 +32,90 @@ enum FwdMode : int {
   FWD_I64 = 3,       // src holds signed int64 coefficients (encoder output)
 };
 
-template <int MODE>
-HB_DEV u64 fwd_load(const HbNttTask& tk, const HbPrime& P, u64 ps, u64 ps_half, int j) {
-  u64 x = __ldg(tk.src + j);
-  if (MODE == FWD_PLAIN) return x;
-  if (MODE == FWD_I64) {
-    i64 v = (i64)x;
+// ---------------------------------------------------------------------------
+// Arithmetic policies.
+
+struct PolU64 {
+  typedef u64 T;
+  typedef HbTw Tw;
+  u64 p, two_p;
+  HbPrime P;
+  HB_DEV PolU64(const HbPrime& pr) : p(pr.p), two_p(pr.two_p), P(pr) {}
+  static HB_DEV const Tw* fwd_table(const HbRing& R, int prime) {
+    return R.tw_fwd + (size_t)prime * R.n;
+  }
+  static HB_DEV const Tw* inv_table(const HbRing& R, int prime) {
+    return R.tw_inv + (size_t)prime * R.n;
+  }
+  HB_DEV T from_canon(u64 x) const { return x; }
+  HB_DEV T from_signed(i64 v) const {
     if (v < 0) {
       u64 m = reduce64((u64)(-v), P);
-      return m ? P.p - m : 0ull;
+      return m ? p - m : 0ull;
     }
-    return reduce64(x, P);
+    return reduce64((u64)v, P);
   }
-  return lift_reduce(x, ps, ps_half, P);
-}
+  HB_DEV T from_lift(u64 x, u64 ps, u64 ps_half) const { return lift_reduce(x, ps, ps_half, P); }
+  // values in [0, 4p)
+  HB_DEV void fwd(T& x, T& y, const Tw& t) const {
+    u64 X = csub(x, two_p);
+    u64 Tv = mul_shoup_lazy(y, t.w, t.wsh, p);
+    x = X + Tv;
+    y = X - Tv + two_p;
+  }
+  // values in [0, 2p)
+  HB_DEV void inv(T& x, T& y, const Tw& t) const {
+    u64 X = x, Y = y;
+    x = csub(X + Y, two_p);
+    y = mul_shoup_lazy(X - Y + two_p, t.w, t.wsh, p);
+  }
+  HB_DEV T inv_round_end(T x) const { return x; }
+  HB_DEV u64 fwd_final(T x) const { return csub(csub(x, two_p), p); }
+  HB_DEV u64 inv_final(T x) const { return mul_shoup(x, P.ninv, P.ninv_sh, p); }
+};
 
-// Forward CT butterflies for one group of 2^K elements (x[0..2^K)) covering
-// stages s0..s0+K-1; G = group index along the outer axis.
-template <int K>
-HB_DEV void fwd_group(u64* x, int s0, int G, const HbTw* tw, u64 p, u64 two_p) {
+struct PolF64 {
+  typedef double T;
+  typedef HbTwD Tw;
+  double p, pinv, ninv, ninvq;
+  HB_DEV PolF64(const HbPrime& pr) : p(pr.pd), pinv(pr.pinv), ninv(pr.ninvd), ninvq(pr.ninvq) {}
+  static HB_DEV const Tw* fwd_table(const HbRing& R, int prime) {
+    return R.twd_fwd + (size_t)prime * R.n;
+  }
+  static HB_DEV const Tw* inv_table(const HbRing& R, int prime) {
+    return R.twd_inv + (size_t)prime * R.n;
+  }
+  HB_DEV T from_canon(u64 x) const { return u64_to_f(x); }
+  HB_DEV T from_signed(i64 v) const { return fmod_reduce((double)v, p, pinv); }
+  HB_DEV T from_lift(u64 x, u64 ps, u64 ps_half) const {
+    // centred lift of x mod ps (< 2^42): exact as a signed double
+    const double c = x > ps_half ? -u64_to_f(ps - x) : u64_to_f(x);
+    return fmod_reduce(c, p, pinv);
+  }
+  // |x| grows by <= 0.51p per stage, |y| reduced: stays < 9p over 14 stages
+  HB_DEV void fwd(T& x, T& y, const Tw& t) const {
+    const double Tv = fmod_mul(y, t.w, t.wq, p);
+    const double X = x;
+    x = X + Tv;
+    y = X - Tv;
+  }
+  HB_DEV void inv(T& x, T& y, const Tw& t) const {
+    const double X = x, Y = y;
+    x = X + Y;
+    y = fmod_mul(X - Y, t.w, t.wq, p);
+  }
+  // x doubles per GS stage: re-centre every round (4 stages -> |x| < 9p)
+  HB_DEV T inv_round_end(T x) const { return fmod_reduce(x, p, pinv); }
+  HB_DEV u64 fwd_final(T x) const { return fmod_canon(x, p, pinv); }
+  HB_DEV u64 inv_final(T x) const { return fmod_canon(fmod_mul(x, ninv, ninvq, p), p, pinv); }
+};
+
+// ---------------------------------------------------------------------------
+// Butterfly groups.
+
+template <class Pol, int K>
+HB_DEV void fwd_group(typename Pol::T* x, int s0, int G, const typename Pol::Tw* tw,
+                      const Pol& pol) {
 #pragma unroll
   for (int st = 0; st < K; ++st) {
     const int s = s0 + st;
@@ -55,18 +124,14 @@ HB_DEV void fwd_group(u64* x, int s0, int G, const HbTw* tw, u64 p, u64 two_p) {
     for (int u = 0; u < (1 << K); ++u) {
       if (u & h) continue;
       const int i = G * ((1 << K) / (2 * h)) + u / (2 * h);
-      const HbTw t = tw[(1 << s) + i];
-      u64 X = csub(x[u], two_p);
-      u64 T = mul_shoup_lazy(x[u + h], t.w, t.wsh, p);
-      x[u] = X + T;
-      x[u + h] = X - T + two_p;
+      pol.fwd(x[u], x[u + h], tw[(1 << s) + i]);
     }
   }
 }
 
-// Inverse GS butterflies for one group of 2^K elements, stages r0..r0+K-1.
-template <int K>
-HB_DEV void inv_group(u64* x, int r0, int G, int logn, const HbTw* tw, u64 p, u64 two_p) {
+template <class Pol, int K>
+HB_DEV void inv_group(typename Pol::T* x, int r0, int G, int logn, const typename Pol::Tw* tw,
+                      const Pol& pol) {
 #pragma unroll
   for (int st = 0; st < K; ++st) {
     const int r = r0 + st;
@@ -75,97 +140,92 @@ HB_DEV void inv_group(u64* x, int r0, int G, int logn, const HbTw* tw, u64 p, u6
     for (int u = 0; u < (1 << K); ++u) {
       if (u & hh) continue;
       const int i = ((G << (r0 + K)) >> (r + 1)) + u / (2 * hh);
-      const HbTw t = tw[((1 << logn) >> (r + 1)) + i];
-      u64 X = x[u], Y = x[u + hh];
-      x[u] = csub(X + Y, two_p);
-      x[u + hh] = mul_shoup_lazy(X - Y + two_p, t.w, t.wsh, p);
+      pol.inv(x[u], x[u + hh], tw[((1 << logn) >> (r + 1)) + i]);
     }
   }
 }
 
-// One strided forward round (t_last = N >> (s0+K) >= 16) from/to smem.
-template <int LOGN, int K>
-HB_DEV void fwd_round_smem(u64* sm, int s0, const HbTw* tw, u64 p, u64 two_p) {
-  constexpr int N = 1 << LOGN, T = N / 16, GPT = 16 >> K;  // groups per thread
+// One strided forward round (t_last = N >> (s0+K) >= 16) on smem.
+template <class Pol, int LOGN, int K>
+HB_DEV void fwd_round_smem(typename Pol::T* sm, int s0, const typename Pol::Tw* tw,
+                           const Pol& pol) {
+  constexpr int N = 1 << LOGN, T = N / 16, GPT = 16 >> K;
   const int tl = N >> (s0 + K);
-  u64 x[16];
+  typename Pol::T x[16];
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    const int c = gid % tl, G = gid / tl;
-    const int base = G * ((1 << K) * tl) + c;
+    const int base = (gid / tl) * ((1 << K) * tl) + gid % tl;
 #pragma unroll
     for (int u = 0; u < (1 << K); ++u) x[q * (1 << K) + u] = sm[sw(base + u * tl)];
   }
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    fwd_group<K>(x + q * (1 << K), s0, gid / tl, tw, p, two_p);
+    fwd_group<Pol, K>(x + q * (1 << K), s0, gid / tl, tw, pol);
   }
-  __syncthreads();
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    const int c = gid % tl, G = gid / tl;
-    const int base = G * ((1 << K) * tl) + c;
+    const int base = (gid / tl) * ((1 << K) * tl) + gid % tl;
 #pragma unroll
     for (int u = 0; u < (1 << K); ++u) sm[sw(base + u * tl)] = x[q * (1 << K) + u];
   }
   __syncthreads();
 }
 
-template <int LOGN, int MODE>
-__global__ void __launch_bounds__((1 << LOGN) / 16)
-k_ntt_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
+template <class Pol, int MODE>
+HB_DEV typename Pol::T fwd_load(const HbNttTask& tk, const Pol& pol, u64 ps, u64 ps_half, int j) {
+  const u64 x = __ldg(tk.src + j);
+  if (MODE == FWD_PLAIN) return pol.from_canon(x);
+  if (MODE == FWD_I64) return pol.from_signed((i64)x);
+  return pol.from_lift(x, ps, ps_half);
+}
+
+template <class Pol, int LOGN, int MODE>
+HB_DEV void ntt_fwd_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P) {
   constexpr int N = 1 << LOGN, T = N / 16;
-  extern __shared__ u64 sm[];
-  const HbNttTask tk = tasks[blockIdx.x];
-  const HbPrime P = R.primes[tk.dst_prime];
-  const u64 p = P.p, two_p = P.two_p;
+  typedef typename Pol::T V;
+  extern __shared__ u64 smraw[];
+  V* sm = reinterpret_cast<V*>(smraw);
+  const Pol pol(P);
   u64 ps = 0, ps_half = 0;
   if (MODE == FWD_LIFT || MODE == FWD_MODDOWN) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
-  const HbTw* tw = R.tw_fwd + (size_t)tk.dst_prime * N;
+  const typename Pol::Tw* tw = Pol::fwd_table(R, tk.dst_prime);
   const int g = threadIdx.x;
-
-  // Round 0: stages 0..3 straight from global (G = 0, column g).
-  {
-    u64 x[16];
+  {  // round 0: stages 0..3 straight from global (G = 0, column g)
+    V x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = fwd_load<MODE>(tk, P, ps, ps_half, u * T + g);
-    fwd_group<4>(x, 0, 0, tw, p, two_p);
+    for (int u = 0; u < 16; ++u) x[u] = fwd_load<Pol, MODE>(tk, pol, ps, ps_half, u * T + g);
+    fwd_group<Pol, 4>(x, 0, 0, tw, pol);
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[sw(u * T + g)] = x[u];
     __syncthreads();
   }
-  // Middle strided rounds: stages 4 .. LOGN-5.
-  constexpr int MID = LOGN - 8;  // stages left between round 0 and the final round
-  if (MID >= 4) fwd_round_smem<LOGN, 4>(sm, 4, tw, p, two_p);
-  if (MID >= 8) fwd_round_smem<LOGN, 4>(sm, 8, tw, p, two_p);
-  constexpr int REM = MID % 4;
-  constexpr int SREM = 4 + (MID / 4) * 4;
-  if (REM == 1) fwd_round_smem<LOGN, 1>(sm, SREM, tw, p, two_p);
-  if (REM == 2) fwd_round_smem<LOGN, 2>(sm, SREM, tw, p, two_p);
-  if (REM == 3) fwd_round_smem<LOGN, 3>(sm, SREM, tw, p, two_p);
-  // Final contiguous round: stages LOGN-4 .. LOGN-1, thread g owns [16g, 16g+16).
-  {
-    u64 x[16];
+  constexpr int MID = LOGN - 8;
+  if (MID >= 4) fwd_round_smem<Pol, LOGN, 4>(sm, 4, tw, pol);
+  if (MID >= 8) fwd_round_smem<Pol, LOGN, 4>(sm, 8, tw, pol);
+  constexpr int REM = MID % 4, SREM = 4 + (MID / 4) * 4;
+  if (REM == 1) fwd_round_smem<Pol, LOGN, 1>(sm, SREM, tw, pol);
+  if (REM == 2) fwd_round_smem<Pol, LOGN, 2>(sm, SREM, tw, pol);
+  if (REM == 3) fwd_round_smem<Pol, LOGN, 3>(sm, SREM, tw, pol);
+  {  // final contiguous round; results canonical, staged for a coalesced store
+    V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[sw(16 * g + u)];
-    fwd_group<4>(x, LOGN - 4, g, tw, p, two_p);
+    fwd_group<Pol, 4>(x, LOGN - 4, g, tw, pol);
+    u64* smu = smraw;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = csub(csub(x[u], two_p), p);
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 16; ++u) sm[sw(16 * g + u)] = x[u];
+    for (int u = 0; u < 16; ++u) smu[sw(16 * g + u)] = pol.fwd_final(x[u]);
     __syncthreads();
   }
-  // Coalesced copy-out with the fused epilogue.
+  const u64 p = P.p;
 #pragma unroll 4
   for (int j = g; j < N; j += T) {
-    u64 v = sm[sw(j)];
+    u64 v = smraw[sw(j)];
     if (MODE == FWD_MODDOWN) {
       v = mul_shoup(sub_mod(__ldg(tk.aux + j), v, p), tk.scal, tk.scal_sh, p);
       if (tk.add) {
@@ -177,140 +237,155 @@ k_ntt_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   }
 }
 
-// Inverse: contiguous round first (via a coalesced global->smem stage), then
-// strided rounds; the last round writes global directly (lanes = columns)
+template <int LOGN, int MODE, bool F64>
+__global__ void __launch_bounds__((1 << LOGN) / 16)
+k_ntt_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
+  const HbNttTask tk = tasks[blockIdx.x];
+  const HbPrime P = R.primes[tk.dst_prime];
+  if (F64)
+    ntt_fwd_body<PolF64, LOGN, MODE>(tk, R, P);
+  else
+    ntt_fwd_body<PolU64, LOGN, MODE>(tk, R, P);
+}
+
+// Inverse: contiguous round first (after a coalesced global->smem stage),
+// then strided rounds; the last round writes global directly (lanes = columns)
 // with the N^-1 scaling fused.
-template <int LOGN, int K>
-HB_DEV void inv_round_strided(u64* sm, int r0, const HbTw* tw, u64 p, u64 two_p,
-                              bool last, const HbNttTask& tk, const HbPrime& P) {
+template <class Pol, int LOGN, int K>
+HB_DEV void inv_round_strided(typename Pol::T* sm, int r0, const typename Pol::Tw* tw,
+                              const Pol& pol, bool last, u64* dst) {
   constexpr int N = 1 << LOGN, T = N / 16, GPT = 16 >> K;
   const int tl = 1 << r0;
-  u64 x[16];
+  typename Pol::T x[16];
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    const int c = gid % tl, G = gid / tl;
-    const int base = G * ((1 << K) * tl) + c;
+    const int base = (gid / tl) * ((1 << K) * tl) + gid % tl;
 #pragma unroll
     for (int u = 0; u < (1 << K); ++u) x[q * (1 << K) + u] = sm[sw(base + u * tl)];
   }
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    inv_group<K>(x + q * (1 << K), r0, gid / tl, LOGN, tw, p, two_p);
+    inv_group<Pol, K>(x + q * (1 << K), r0, gid / tl, LOGN, tw, pol);
   }
   if (last) {
 #pragma unroll
     for (int q = 0; q < GPT; ++q) {
       const int gid = threadIdx.x + q * T;
-      const int c = gid % tl, G = gid / tl;
-      const int base = G * ((1 << K) * tl) + c;
+      const int base = (gid / tl) * ((1 << K) * tl) + gid % tl;
 #pragma unroll
-      for (int u = 0; u < (1 << K); ++u)
-        tk.dst[base + u * tl] = mul_shoup(x[q * (1 << K) + u], P.ninv, P.ninv_sh, p);
+      for (int u = 0; u < (1 << K); ++u) dst[base + u * tl] = pol.inv_final(x[q * (1 << K) + u]);
     }
     return;
   }
-  __syncthreads();
 #pragma unroll
   for (int q = 0; q < GPT; ++q) {
     const int gid = threadIdx.x + q * T;
-    const int c = gid % tl, G = gid / tl;
-    const int base = G * ((1 << K) * tl) + c;
+    const int base = (gid / tl) * ((1 << K) * tl) + gid % tl;
 #pragma unroll
-    for (int u = 0; u < (1 << K); ++u) sm[sw(base + u * tl)] = x[q * (1 << K) + u];
+    for (int u = 0; u < (1 << K); ++u)
+      sm[sw(base + u * tl)] = pol.inv_round_end(x[q * (1 << K) + u]);
   }
   __syncthreads();
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16)
-k_ntt_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
+template <class Pol, int LOGN>
+HB_DEV void ntt_inv_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P) {
   constexpr int N = 1 << LOGN, T = N / 16;
-  extern __shared__ u64 sm[];
-  const HbNttTask tk = tasks[blockIdx.x];
-  const HbPrime P = R.primes[tk.dst_prime];
-  const u64 p = P.p, two_p = P.two_p;
-  const HbTw* tw = R.tw_inv + (size_t)tk.dst_prime * N;
+  typedef typename Pol::T V;
+  extern __shared__ u64 smraw[];
+  V* sm = reinterpret_cast<V*>(smraw);
+  const Pol pol(P);
+  const typename Pol::Tw* tw = Pol::inv_table(R, tk.dst_prime);
   const int g = threadIdx.x;
-  // Coalesced stage-in.
 #pragma unroll 4
-  for (int j = g; j < N; j += T) sm[sw(j)] = __ldg(tk.src + j);
+  for (int j = g; j < N; j += T) sm[sw(j)] = pol.from_canon(__ldg(tk.src + j));
   __syncthreads();
-  // Round 0: stages 0..3 on contiguous 16-element groups.
-  {
-    u64 x[16];
+  {  // round 0: stages 0..3 on contiguous 16-element groups
+    V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[sw(16 * g + u)];
-    inv_group<4>(x, 0, g, LOGN, tw, p, two_p);
-    __syncthreads();
+    inv_group<Pol, 4>(x, 0, g, LOGN, tw, pol);
 #pragma unroll
-    for (int u = 0; u < 16; ++u) sm[sw(16 * g + u)] = x[u];
+    for (int u = 0; u < 16; ++u) sm[sw(16 * g + u)] = pol.inv_round_end(x[u]);
     __syncthreads();
   }
-  // Strided rounds r0 = 4, 8, ...; the last one stores to global.
-  constexpr int REST = LOGN - 4;
-  constexpr int NFULL = REST / 4, REM = REST % 4;
+  constexpr int REST = LOGN - 4, NFULL = REST / 4, REM = REST % 4;
   if (REM == 0) {
-    if (NFULL >= 1) inv_round_strided<LOGN, 4>(sm, 4, tw, p, two_p, NFULL == 1, tk, P);
-    if (NFULL >= 2) inv_round_strided<LOGN, 4>(sm, 8, tw, p, two_p, NFULL == 2, tk, P);
-    if (NFULL >= 3) inv_round_strided<LOGN, 4>(sm, 12, tw, p, two_p, NFULL == 3, tk, P);
+    if (NFULL >= 1) inv_round_strided<Pol, LOGN, 4>(sm, 4, tw, pol, NFULL == 1, tk.dst);
+    if (NFULL >= 2) inv_round_strided<Pol, LOGN, 4>(sm, 8, tw, pol, NFULL == 2, tk.dst);
+    if (NFULL >= 3) inv_round_strided<Pol, LOGN, 4>(sm, 12, tw, pol, NFULL == 3, tk.dst);
   } else {
-    if (NFULL >= 1) inv_round_strided<LOGN, 4>(sm, 4, tw, p, two_p, false, tk, P);
-    if (NFULL >= 2) inv_round_strided<LOGN, 4>(sm, 8, tw, p, two_p, false, tk, P);
+    if (NFULL >= 1) inv_round_strided<Pol, LOGN, 4>(sm, 4, tw, pol, false, tk.dst);
+    if (NFULL >= 2) inv_round_strided<Pol, LOGN, 4>(sm, 8, tw, pol, false, tk.dst);
     constexpr int RR = 4 + NFULL * 4;
-    if (REM == 1) inv_round_strided<LOGN, 1>(sm, RR, tw, p, two_p, true, tk, P);
-    if (REM == 2) inv_round_strided<LOGN, 2>(sm, RR, tw, p, two_p, true, tk, P);
-    if (REM == 3) inv_round_strided<LOGN, 3>(sm, RR, tw, p, two_p, true, tk, P);
+    if (REM == 1) inv_round_strided<Pol, LOGN, 1>(sm, RR, tw, pol, true, tk.dst);
+    if (REM == 2) inv_round_strided<Pol, LOGN, 2>(sm, RR, tw, pol, true, tk.dst);
+    if (REM == 3) inv_round_strided<Pol, LOGN, 3>(sm, RR, tw, pol, true, tk.dst);
   }
+}
+
+template <int LOGN, bool F64>
+__global__ void __launch_bounds__((1 << LOGN) / 16)
+k_ntt_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
+  const HbNttTask tk = tasks[blockIdx.x];
+  const HbPrime P = R.primes[tk.dst_prime];
+  if (F64)
+    ntt_inv_body<PolF64, LOGN>(tk, R, P);
+  else
+    ntt_inv_body<PolU64, LOGN>(tk, R, P);
 }
 
 // ---------------------------------------------------------------------------
 // Host launchers.
 
+template <int LOGN, int MODE, bool F64>
+static cudaError_t fwd_one(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  constexpr int N = 1 << LOGN, T = N / 16;
+  const size_t smem = (size_t)N * sizeof(u64);
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt_fwd<LOGN, MODE, F64>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_ntt_fwd<LOGN, MODE, F64><<<count, T, smem, st>>>(tasks, R);
+  return cudaGetLastError();
+}
+
+template <int LOGN, bool F64>
+static cudaError_t fwd_mode(const HbNttTask* tasks, int count, const HbRing& R, int mode,
+                            cudaStream_t st) {
+  switch (mode) {
+    case FWD_PLAIN: return fwd_one<LOGN, FWD_PLAIN, F64>(tasks, count, R, st);
+    case FWD_LIFT: return fwd_one<LOGN, FWD_LIFT, F64>(tasks, count, R, st);
+    case FWD_MODDOWN: return fwd_one<LOGN, FWD_MODDOWN, F64>(tasks, count, R, st);
+    case FWD_I64: return fwd_one<LOGN, FWD_I64, F64>(tasks, count, R, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int LOGN>
 static cudaError_t launch_fwd_t(const HbNttTask* tasks, int count, const HbRing& R, int mode,
                                 cudaStream_t st) {
+  return R.use_f64 ? fwd_mode<LOGN, true>(tasks, count, R, mode, st)
+                   : fwd_mode<LOGN, false>(tasks, count, R, mode, st);
+}
+
+template <int LOGN, bool F64>
+static cudaError_t inv_one(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int N = 1 << LOGN, T = N / 16;
   const size_t smem = (size_t)N * sizeof(u64);
-  auto set = [&](const void* f) {
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  };
-  cudaError_t e = cudaSuccess;
-  switch (mode) {
-    case FWD_PLAIN:
-      e = set((const void*)k_ntt_fwd<LOGN, FWD_PLAIN>);
-      if (e == cudaSuccess) k_ntt_fwd<LOGN, FWD_PLAIN><<<count, T, smem, st>>>(tasks, R);
-      break;
-    case FWD_LIFT:
-      e = set((const void*)k_ntt_fwd<LOGN, FWD_LIFT>);
-      if (e == cudaSuccess) k_ntt_fwd<LOGN, FWD_LIFT><<<count, T, smem, st>>>(tasks, R);
-      break;
-    case FWD_MODDOWN:
-      e = set((const void*)k_ntt_fwd<LOGN, FWD_MODDOWN>);
-      if (e == cudaSuccess) k_ntt_fwd<LOGN, FWD_MODDOWN><<<count, T, smem, st>>>(tasks, R);
-      break;
-    case FWD_I64:
-      e = set((const void*)k_ntt_fwd<LOGN, FWD_I64>);
-      if (e == cudaSuccess) k_ntt_fwd<LOGN, FWD_I64><<<count, T, smem, st>>>(tasks, R);
-      break;
-    default:
-      return cudaErrorInvalidValue;
-  }
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt_inv<LOGN, F64>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  k_ntt_inv<LOGN, F64><<<count, T, smem, st>>>(tasks, R);
   return cudaGetLastError();
 }
 
 template <int LOGN>
 static cudaError_t launch_inv_t(const HbNttTask* tasks, int count, const HbRing& R,
                                 cudaStream_t st) {
-  constexpr int N = 1 << LOGN, T = N / 16;
-  const size_t smem = (size_t)N * sizeof(u64);
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt_inv<LOGN>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_ntt_inv<LOGN><<<count, T, smem, st>>>(tasks, R);
-  return cudaGetLastError();
+  return R.use_f64 ? inv_one<LOGN, true>(tasks, count, R, st)
+                   : inv_one<LOGN, false>(tasks, count, R, st);
 }
 
 cudaError_t launch_ntt_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,

@@ -9,14 +9,21 @@ struct __align__(16) HbTw {
   u64 w, wsh;
 };
 
+// fp64 twiddle entry: w as an exact double and fl(w / p).
+struct __align__(16) HbTwD {
+  double w, wq;
+};
+
 struct HbRing {
   int logn;
   int n;
   int nprimes;
-  int _pad;
+  int use_f64;            // every prime < 2^42: transforms run on the fp64 pipe
   const HbPrime* primes;  // [nprimes]
   const HbTw* tw_fwd;     // [nprimes][n]  psi^brv(j)            (ring.py:281)
   const HbTw* tw_inv;     // [nprimes][n]  psi^-brv(j)  (true inverse)
+  const HbTwD* twd_fwd;   // fp64 copies of the two tables
+  const HbTwD* twd_inv;
 };
 
 // One row-polynomial transform.  Field meaning depends on the kernel mode;

@@ -129,3 +129,27 @@ def test_encrypt_bit_exact_given_coeffs(prof, golden):
     assert digest(*be.export(ct)) == golden[prof]["enc_L"]
     err = np.abs(be.dec(ct) - vals).max()
     assert err < 2 * golden[prof]["dec_maxerr"] + 1e-9
+
+
+def test_integer_ntt_policy_bit_exact(golden):
+    """The 64-bit-Shoup transform (used for primes >= 2^42) gives the same
+    residues as the fp64-pipe transform the reference profiles run on."""
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    os.environ["HEAR_B200_INT_NTT"] = "1"
+    try:
+        be = CkksBackend(gen_params("toy-fast"), seed=7)
+    finally:
+        del os.environ["HEAR_B200_INT_NTT"]
+    g = golden["toy-fast"]
+    assert digest(host(be.keys.relin.b)) == g["relin_b"]
+    ps = be.params
+    lvl = 6
+    A = be.import_ct(*rand_ct(ps, lvl, 100 + lvl), lvl, ps.msg_scale)
+    B = be.import_ct(*rand_ct(ps, lvl, 200 + lvl), lvl, ps.msg_scale)
+    be.ensure_rotation_keys({int(a): l for a, l in g["rot_levels"].items()})
+    assert digest(*be.export(be._raw_mult(A, B))) == g["ops"]["6"]["mult"]
+    assert digest(*be.export(be._raw_rescale(A))) == g["ops"]["6"]["rescale"]
+    m = be._raw_rot_many(A, [1, 5])
+    assert digest(*be.export(m[5])) == g["ops"]["6"]["rot_many_5"]
