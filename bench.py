@@ -264,12 +264,17 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = nat.launch_count
+    prof_range = os.environ.get("HEAR_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clk:
+        if prof_range:
+            torch.cuda.profiler.start()
         e0.record(st)
         for _ in range(args.steps):
             run_pipeline(enc, ct, be)
         e1.record(st)
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.profiler.stop()
     launches = nat.launch_count - l0
     par.barrier()
     ms = par.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)

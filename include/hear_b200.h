@@ -80,6 +80,14 @@ int hb_mac(hb_ring* ring, const void* tasks, int count, const void* terms, void*
 /* Same, one launch per layer over [B*2, rows, N] ciphertext blocks.          */
 int hb_mac_strided(hb_ring* ring, const void* outs, int nout, const void* terms, int rows,
                    int bc, void* stream);
+/* Shared-term MAC for a group of outputs over one ciphertext term list:
+ * dsts[o] = sum_t pts[o*nterms + t] * cts[t]; device arrays of row-block
+ * base pointers ([bc, rows, N] ciphertext blocks, [rows, N] plaintexts).     */
+int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* dsts, int nterms,
+                  int nout, int rows, int bc, void* stream);
+/* Key-switch inner product, one task per (job, output row), nb clips per task
+ * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
+int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);
 /* Ciphertext tensor product d0, d1, d2 (engine.py:249-257).                  */
 int hb_tensor(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Key-switch inner product with the fused Galois gather

@@ -47,6 +47,8 @@ def lib():
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
         L.hb_ks_inner.argtypes = [vp, vp, i32, vp]
+        L.hb_ks_inner2.argtypes = [vp, vp, i32, i32, vp]
+        L.hb_mac_shared.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
         L.hb_crt_double.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
         L.hb_fft_create.restype = vp
         L.hb_fft_create.argtypes = [i32, vp, vp, vp]
@@ -88,6 +90,10 @@ MAC_OUT = np.dtype([("dst", "<u8"), ("nterms", "<i4"), ("term_off", "<i4")])
 KS_TASK = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
                     ("out_a", "<u8"), ("perm", "<u8"), ("de_stride", "<i8"),
                     ("key_stride", "<i8"), ("ndig", "<i4"), ("prime", "<i4")])
+KS_TASK2 = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
+                     ("out_a", "<u8"), ("perm", "<u8"), ("de_bstride", "<i8"),
+                     ("de_dstride", "<i8"), ("key_stride", "<i8"), ("out_bstride", "<i8"),
+                     ("ndig", "<i4"), ("prime", "<i4")])
 TENSOR_TASK = np.dtype([("a0", "<u8"), ("a1", "<u8"), ("b0", "<u8"), ("b1", "<u8"),
                         ("d0", "<u8"), ("d1", "<u8"), ("d2", "<u8"),
                         ("prime", "<i4"), ("_pad", "<i4")])
@@ -102,7 +108,7 @@ EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PER
 
 def _check_layouts():
     L = _lib
-    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, KS_TASK)):
+    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, KS_TASK, KS_TASK2)):
         if L.hb_sizeof_task(kind) != dt.itemsize:
             raise NativeError(f"task layout {kind} mismatch: C {L.hb_sizeof_task(kind)} "
                               f"vs numpy {dt.itemsize}")

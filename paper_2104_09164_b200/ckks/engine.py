@@ -561,16 +561,16 @@ class CkksBackend(BackendBase):
             kbr = rp(key.b).reshape(key.b.shape[0], key.lmax + 2)[0, krow]
             kar = rp(key.a).reshape(key.a.shape[0], key.lmax + 2)[0, krow]
             parts.append(_tasks(
-                nat.KS_TASK, bsz * rows, de=der[off:off + bsz, 0, :].ravel(),
-                kb=np.tile(kbr, bsz), ka=np.tile(kar, bsz), out_b=ipr[j, :, 0].ravel(),
-                out_a=ipr[j, :, 1].ravel(), perm=perm.data_ptr() if perm is not None else 0,
-                de_stride=rows * self.n, key_stride=(key.lmax + 2) * self.n, ndig=ndig,
-                prime=np.tile(gidx, bsz)))
+                nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
+                out_a=ipr[j, 0, 1], perm=perm.data_ptr() if perm is not None else 0,
+                de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
+                key_stride=(key.lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
+                prime=gidx))
             if addend is not None:
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        self.ring.ks_inner(np.concatenate(parts))
+        self.ring.ks_inner2(np.concatenate(parts), bsz)
         m, r = nj * bsz * 2, lvl + 1
         iprows = rp(ip).reshape(m, rows)
         spc = self.ring.empty(m)
@@ -617,6 +617,36 @@ class CkksBackend(BackendBase):
         return groups
 
     def _raw_mac_many(self, jobs) -> list:
+        """Groups of outputs that share one ciphertext term list (conv partial
+        sums, FC diagonals) go through the shared-term kernel; the rest
+        through the generic strided MAC."""
+        out = [None] * len(jobs)
+        groups: dict = {}
+        for i, terms in enumerate(jobs):
+            key = (terms[0][0].level, tuple(ct.payload.data.data_ptr() for ct, _ in terms))
+            groups.setdefault(key, []).append(i)
+        rest = []
+        for (lvl, ctkey), idx in groups.items():
+            if len(idx) < 2:
+                rest += idx
+                continue
+            bsz = jobs[idx[0]][0][0].payload.batch
+            r = lvl + 1
+            res = self.ring.empty(len(idx), bsz, 2, r)
+            dsts = self.ring.row_ptrs(res).reshape(len(idx), -1)[:, 0]
+            pts = np.array([[pt.payload.data_ptr() for _, pt in jobs[i]] for i in idx],
+                           dtype=np.uint64)
+            self.ring.mac_shared(np.array(ctkey, dtype=np.uint64), pts, dsts, r, 2 * bsz)
+            for q, i in enumerate(idx):
+                t0 = jobs[i][0]
+                out[i] = Ct(CtData(res[q]), lvl, t0[0].scale * t0[1].scale, self.n2)
+        if rest:
+            sub = self._raw_mac_strided([jobs[i] for i in rest])
+            for i, c in zip(rest, sub):
+                out[i] = c
+        return out
+
+    def _raw_mac_strided(self, jobs) -> list:
         out = [None] * len(jobs)
         for lvl, idx in self._by_level(jobs, lambda t: t[0][0].level).items():
             bsz = jobs[idx[0]][0][0].payload.batch

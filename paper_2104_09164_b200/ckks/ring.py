@@ -149,6 +149,23 @@ class RingContext:
             nat.check(self._lib.hb_tensor(self.handle, _ptr(d), len(tasks), self.stream),
                       "tensor")
 
+    def mac_shared(self, cts: np.ndarray, pts: np.ndarray, dsts: np.ndarray, rows: int, bc: int):
+        """Shared-term MAC: dsts[o] = sum_t pts[o, t] * cts[t] over [bc, rows, N] blocks."""
+        nout, nterms = pts.shape
+        if nout:
+            buf = _upload(np.concatenate([cts.ravel(), pts.ravel(), dsts.ravel()])
+                          .astype(np.uint64), self.device)
+            base = _ptr(buf)
+            nat.check(self._lib.hb_mac_shared(self.handle, base, base + 8 * nterms,
+                                              base + 8 * (nterms + nout * nterms), nterms, nout,
+                                              rows, bc, self.stream), "mac_shared")
+
+    def ks_inner2(self, tasks: np.ndarray, nb: int):
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            nat.check(self._lib.hb_ks_inner2(self.handle, _ptr(d), len(tasks), nb, self.stream),
+                      "ks_inner2")
+
     def ks_inner(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)

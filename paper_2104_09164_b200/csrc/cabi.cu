@@ -26,6 +26,14 @@ cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
                                cudaStream_t);
 cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_mac_shared(const void*, const void*, const void*, int, int, const HbPrime*, int,
+                              int, int, cudaStream_t);
+cudaError_t launch_mac_gemm(const void*, const void*, const void*, int, int, const HbPrime*, int,
+                            int, int, cudaStream_t);
+cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int, const HbPrime*,
+                                int, int, int, cudaStream_t);
+cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
 struct HbCrtTask;
 cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
                               int, int, cudaStream_t);
@@ -180,6 +188,7 @@ int hb_sizeof_task(int kind) {
     case 2: return (int)sizeof(HbMacTask);
     case 3: return (int)sizeof(HbMacTerm);
     case 4: return (int)sizeof(HbKsTask);
+    case 5: return (int)sizeof(HbKsTask2);
     default: return -1;
   }
 }
@@ -222,6 +231,27 @@ int hb_ks_inner(hb_ring* r, const void* tasks, int count, void* stream) {
   cudaError_t e = launch_ks_inner((const HbKsTask*)tasks, count, r->dev.primes, r->dev.n,
                                   (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_inner") : 0;
+}
+
+int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts, int nterms,
+                  int nout, int rows, int bc, void* stream) {
+  const char* old = getenv("HEAR_B200_MAC_SHARED");
+  cudaError_t e = (old && old[0] == '1')
+      ? launch_mac_shared(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
+                          (cudaStream_t)stream)
+      : r->dev.use_f64
+      ? launch_mac_gemm_f64(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
+                            (cudaStream_t)stream)
+      : launch_mac_gemm(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
+                        (cudaStream_t)stream);
+  return e ? fail(e, "hb_mac_shared") : 0;
+}
+
+int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {
+  cudaError_t e = r->dev.use_f64
+      ? launch_ks_inner2_f64(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream)
+      : launch_ks_inner2(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream);
+  return e ? fail(e, "hb_ks_inner2") : 0;
 }
 
 int hb_crt_double(hb_ring* r, const void* tasks, int count, const unsigned long long* consts,

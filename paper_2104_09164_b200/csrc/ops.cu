@@ -5,6 +5,7 @@
 // All rows are N contiguous u64 residues; every task names its prime.  Each
 // thread handles two adjacent coefficients (one 16-byte load per operand),
 // grid.y walks the task list, grid.x the row.
+#include <cstdlib>
 #include "ring.cuh"
 
 namespace hb {
@@ -400,6 +401,377 @@ cudaError_t launch_mac_strided(const void* outs, int nout, const HbMacTerm* term
   dim3 grid((n / 2 + EW_THREADS - 1) / EW_THREADS, total < 65535 ? (int)total : 65535);
   k_mac_strided<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout, terms,
                                              primes, n, R, BC);
+  return cudaGetLastError();
+}
+
+}  // namespace hb
+
+namespace hb {
+
+// ---------------------------------------------------------------------------
+// Shared-term multiply-accumulate: a group of outputs that sum products with
+// the SAME ciphertext term list (hconv's giant/baby partial sums, the FC
+// diagonals): out_o = sum_t pt[o][t] * ct[t].  Block = 32 coefficient pairs
+// x up to 8 clip-components (bc); a thread keeps 8 outputs' 128-bit
+// accumulators while streaming the terms, so each ciphertext row is read
+// once per 8 outputs instead of once per output, and the 8 bc-warps of a
+// block read the same plaintext addresses (L1 broadcast).
+struct HbMacGroup {
+  const u64* const* cts;   // [nterms] ciphertext bases ([BC, R, N] blocks)
+  const u64* const* pts;   // [nout][nterms] plaintext bases (rows at +r*N)
+  u64* const* dsts;        // [nout] output bases ([BC, R, N])
+  int nterms;
+  int nout;
+};
+
+constexpr int MAC_OT = 8;
+
+__global__ void __launch_bounds__(256)
+k_mac_shared(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  const int jp = blockIdx.x * 32 + threadIdx.x;       // coefficient pair
+  const int r = blockIdx.y % R;
+  const int bc = (blockIdx.y / R) * blockDim.y + threadIdx.y;
+  const int o0 = blockIdx.z * MAC_OT;
+  const int j = 2 * jp;
+  if (j >= n || bc >= BC) return;
+  const HbPrime P = primes[r];
+  const int no = min(MAC_OT, g.nout - o0);
+  const size_t ct_off = ((size_t)bc * R + r) * n + j;
+  const size_t pt_off = (size_t)r * n + j;
+  Acc128 acc[MAC_OT][2];
+  for (int t = 0; t < g.nterms; ++t) {
+    const ulonglong2 c = __ldg(reinterpret_cast<const ulonglong2*>(g.cts[t] + ct_off));
+#pragma unroll
+    for (int o = 0; o < MAC_OT; ++o) {
+      if (o < no) {
+        const ulonglong2 a =
+            __ldg(reinterpret_cast<const ulonglong2*>(g.pts[(size_t)(o0 + o) * g.nterms + t] + pt_off));
+        acc[o][0].mac(a.x, c.x);
+        acc[o][1].mac(a.y, c.y);
+      }
+    }
+    if ((t & 7) == 7) {
+#pragma unroll
+      for (int o = 0; o < MAC_OT; ++o) { acc[o][0].fold(P); acc[o][1].fold(P); }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < MAC_OT; ++o) {
+    if (o < no) {
+      ulonglong2 v;
+      v.x = acc[o][0].fold(P);
+      v.y = acc[o][1].fold(P);
+      *reinterpret_cast<ulonglong2*>(g.dsts[o0 + o] + ct_off) = v;
+    }
+  }
+}
+
+cudaError_t launch_mac_shared(const void* cts, const void* pts, const void* dsts, int nterms,
+                              int nout, const HbPrime* primes, int n, int R, int BC,
+                              cudaStream_t st) {
+  if (nout <= 0 || nterms <= 0) return cudaSuccess;
+  HbMacGroup g;
+  g.cts = reinterpret_cast<const u64* const*>(cts);
+  g.pts = reinterpret_cast<const u64* const*>(pts);
+  g.dsts = reinterpret_cast<u64* const*>(dsts);
+  g.nterms = nterms;
+  g.nout = nout;
+  const int by = BC < 8 ? BC : 8;
+  dim3 block(32, by);
+  dim3 grid((n / 2 + 31) / 32, R * ((BC + by - 1) / by), (nout + MAC_OT - 1) / MAC_OT);
+  k_mac_shared<<<grid, block, 0, st>>>(g, primes, n, R, BC);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Key-switch inner product, clip-blocked: one task per (job, output row r);
+// block = 32 coefficient pairs x up to 8 clips, so the key rows (shared by
+// every clip) are fetched once per block and broadcast through L1.
+
+
+__global__ void __launch_bounds__(256)
+k_ks_inner2(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
+            int nb) {
+  const HbKsTask2 tk = tasks[blockIdx.y];
+  const int b = blockIdx.z * blockDim.y + threadIdx.y;
+  const int j = 2 * (blockIdx.x * 32 + threadIdx.x);
+  if (j >= n || b >= nb) return;
+  const HbPrime P = primes[tk.prime];
+  int s0 = j, s1 = j + 1;
+  if (tk.perm) {
+    const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+    s0 = pp.x;
+    s1 = pp.y;
+  }
+  const u64* de = tk.de + b * tk.de_bstride;
+  Acc128 b0, b1, a0, a1;
+  for (int i = 0; i < tk.ndig; ++i) {
+    const u64* d = de + i * tk.de_dstride;
+    const u64 x0 = __ldg(d + s0), x1 = __ldg(d + s1);
+    const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
+    const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
+    b0.mac(x0, kb.x);
+    b1.mac(x1, kb.y);
+    a0.mac(x0, ka.x);
+    a1.mac(x1, ka.y);
+    if ((i & 7) == 7) { b0.fold(P); b1.fold(P); a0.fold(P); a1.fold(P); }
+  }
+  ulonglong2 rb, ra;
+  rb.x = b0.fold(P);
+  rb.y = b1.fold(P);
+  ra.x = a0.fold(P);
+  ra.y = a1.fold(P);
+  *reinterpret_cast<ulonglong2*>(tk.out_b + b * tk.out_bstride + j) = rb;
+  *reinterpret_cast<ulonglong2*>(tk.out_a + b * tk.out_bstride + j) = ra;
+}
+
+cudaError_t launch_ks_inner2(const void* tasks, int ntasks, int nb, const HbPrime* primes, int n,
+                             cudaStream_t st) {
+  if (ntasks <= 0 || nb <= 0) return cudaSuccess;
+  const int by = nb < 8 ? nb : 8;
+  dim3 block(32, by);
+  dim3 grid((n / 2 + 31) / 32, ntasks, (nb + by - 1) / by);
+  k_ks_inner2<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
+  return cudaGetLastError();
+}
+
+}  // namespace hb
+
+namespace hb {
+
+// ---------------------------------------------------------------------------
+// Shared-term MAC as a per-coefficient modular GEMM:
+//   out[o][bc][r][j] = sum_t pt[o][t][r][j] * ct[t][bc][r][j]   (mod p_r)
+// for a group of outputs sharing one ciphertext term list (hconv partial
+// sums, FC diagonals).  Lanes own 32 consecutive coefficients (coalesced 8 B
+// loads of both operands); each thread keeps a TO x TB register tile of
+// 128-bit accumulators, so every loaded plaintext value feeds TB products
+// and every ciphertext value TO products.  The 8 warps of a block tile
+// (WO x WB) over outputs x clip-components; pointer tables live in smem.
+template <int TO, int TB, int WO, int WB>
+__global__ void __launch_bounds__(256, (TO * TB > 16 ? 1 : 2))
+k_mac_gemm(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  extern __shared__ const u64* ptrs[];   // cts[T] | pts[O*T] | dsts[O]
+  const int T = g.nterms, O = g.nout;
+  for (int i = threadIdx.x + threadIdx.y * 32; i < T + O * T + O; i += 256) {
+    if (i < T) ptrs[i] = g.cts[i];
+    else if (i < T + O * T) ptrs[i] = g.pts[i - T];
+    else ptrs[i] = g.dsts[i - T - O * T];
+  }
+  __syncthreads();
+  const u64* const* cts = ptrs;
+  const u64* const* pts = ptrs + T;
+  u64* const* dsts = const_cast<u64* const*>(ptrs + T + O * T);
+
+  const int nchunk = n / 32;
+  const int r = blockIdx.x / nchunk;
+  const int j = (blockIdx.x % nchunk) * 32 + threadIdx.x;
+  const int w = threadIdx.y;
+  const int o0 = (blockIdx.y * WO + w / WB) * TO;
+  const int b0 = (blockIdx.z * WB + w % WB) * TB;
+  if (o0 >= O || b0 >= BC) return;
+  const HbPrime P = primes[r];
+  const size_t rj = (size_t)r * n + j;
+  Acc128 acc[TO][TB];
+  for (int t = 0; t < T; ++t) {
+    u64 c[TB];
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+      c[b] = (b0 + b < BC) ? __ldg(cts[t] + (size_t)(b0 + b) * R * n + rj) : 0ull;
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      const u64 a = (o0 + o < O) ? __ldg(pts[(size_t)(o0 + o) * T + t] + rj) : 0ull;
+#pragma unroll
+      for (int b = 0; b < TB; ++b) acc[o][b].mac(a, c[b]);
+    }
+    if ((t & 7) == 7) {
+#pragma unroll
+      for (int o = 0; o < TO; ++o)
+#pragma unroll
+        for (int b = 0; b < TB; ++b) acc[o][b].fold(P);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < TO; ++o) {
+    if (o0 + o >= O) continue;
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+      if (b0 + b < BC) dsts[o0 + o][(size_t)(b0 + b) * R * n + rj] = acc[o][b].fold(P);
+  }
+}
+
+template <int TO, int TB, int WO, int WB>
+static cudaError_t mac_gemm_t(const HbMacGroup& g, const HbPrime* primes, int n, int R, int BC,
+                              cudaStream_t st) {
+  const size_t smem = sizeof(void*) * (size_t)(g.nterms + g.nout * g.nterms + g.nout);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm<TO, TB, WO, WB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 block(32, 8);
+  dim3 grid(R * (n / 32), (g.nout + TO * WO - 1) / (TO * WO), (BC + TB * WB - 1) / (TB * WB));
+  k_mac_gemm<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mac_gemm(const void* cts, const void* pts, const void* dsts, int nterms,
+                            int nout, const HbPrime* primes, int n, int R, int BC,
+                            cudaStream_t st) {
+  if (nout <= 0 || nterms <= 0) return cudaSuccess;
+  HbMacGroup g;
+  g.cts = reinterpret_cast<const u64* const*>(cts);
+  g.pts = reinterpret_cast<const u64* const*>(pts);
+  g.dsts = reinterpret_cast<u64* const*>(dsts);
+  g.nterms = nterms;
+  g.nout = nout;
+  if (BC <= 2) return mac_gemm_t<4, 2, 8, 1>(g, primes, n, R, BC, st);
+  const char* v = getenv("HEAR_B200_MAC_TILE");
+  if (v && v[0] == '8') return mac_gemm_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
+  if (v && v[0] == '2') return mac_gemm_t<2, 8, 4, 2>(g, primes, n, R, BC, st);
+  return mac_gemm_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
+}
+
+}  // namespace hb
+
+namespace hb {
+
+// fp64-pipe variant of k_mac_gemm for rings whose primes are all < 2^42:
+// each product a*c is reduced exactly to a balanced residue with 6 fp64 ops
+// (modarith.cuh fmod_mul with q = round(a * (c/p)) from a*pinv), summed in
+// double (|sum| < 2^53 for < 2^9 terms), canonicalised once at the end.
+template <int TO, int TB, int WO, int WB>
+__global__ void __launch_bounds__(256)
+k_mac_gemm_f64(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  extern __shared__ const u64* ptrs[];
+  const int T = g.nterms, O = g.nout;
+  for (int i = threadIdx.x + threadIdx.y * 32; i < T + O * T + O; i += 256) {
+    if (i < T) ptrs[i] = g.cts[i];
+    else if (i < T + O * T) ptrs[i] = g.pts[i - T];
+    else ptrs[i] = g.dsts[i - T - O * T];
+  }
+  __syncthreads();
+  const u64* const* cts = ptrs;
+  const u64* const* pts = ptrs + T;
+  u64* const* dsts = const_cast<u64* const*>(ptrs + T + O * T);
+  const int nchunk = n / 32;
+  const int r = blockIdx.x / nchunk;
+  const int j = (blockIdx.x % nchunk) * 32 + threadIdx.x;
+  const int w = threadIdx.y;
+  const int o0 = (blockIdx.y * WO + w / WB) * TO;
+  const int b0 = (blockIdx.z * WB + w % WB) * TB;
+  if (o0 >= O || b0 >= BC) return;
+  const HbPrime P = primes[r];
+  const double p = P.pd, pinv = P.pinv;
+  const size_t rj = (size_t)r * n + j;
+  double acc[TO][TB];
+#pragma unroll
+  for (int o = 0; o < TO; ++o)
+#pragma unroll
+    for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
+  for (int t = 0; t < T; ++t) {
+    double c[TB];
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+      c[b] = (b0 + b < BC) ? u64_to_f(__ldg(cts[t] + (size_t)(b0 + b) * R * n + rj)) : 0.0;
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      const double a = (o0 + o < O) ? u64_to_f(__ldg(pts[(size_t)(o0 + o) * T + t] + rj)) : 0.0;
+      const double aq = a * pinv;
+#pragma unroll
+      for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a, aq, p);
+    }
+    if ((t & 255) == 255) {
+#pragma unroll
+      for (int o = 0; o < TO; ++o)
+#pragma unroll
+        for (int b = 0; b < TB; ++b) acc[o][b] = fmod_reduce(acc[o][b], p, pinv);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < TO; ++o) {
+    if (o0 + o >= O) continue;
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+      if (b0 + b < BC) dsts[o0 + o][(size_t)(b0 + b) * R * n + rj] = fmod_canon(acc[o][b], p, pinv);
+  }
+}
+
+template <int TO, int TB, int WO, int WB>
+static cudaError_t mac_gemm_f64_t(const HbMacGroup& g, const HbPrime* primes, int n, int R, int BC,
+                                  cudaStream_t st) {
+  const size_t smem = sizeof(void*) * (size_t)(g.nterms + g.nout * g.nterms + g.nout);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm_f64<TO, TB, WO, WB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 block(32, 8);
+  dim3 grid(R * (n / 32), (g.nout + TO * WO - 1) / (TO * WO), (BC + TB * WB - 1) / (TB * WB));
+  k_mac_gemm_f64<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mac_gemm_f64(const void* cts, const void* pts, const void* dsts, int nterms,
+                                int nout, const HbPrime* primes, int n, int R, int BC,
+                                cudaStream_t st) {
+  if (nout <= 0 || nterms <= 0) return cudaSuccess;
+  HbMacGroup g;
+  g.cts = reinterpret_cast<const u64* const*>(cts);
+  g.pts = reinterpret_cast<const u64* const*>(pts);
+  g.dsts = reinterpret_cast<u64* const*>(dsts);
+  g.nterms = nterms;
+  g.nout = nout;
+  if (BC <= 2) return mac_gemm_f64_t<4, 2, 8, 1>(g, primes, n, R, BC, st);
+  if (BC <= 8) return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
+  const char* v = getenv("HEAR_B200_MAC_TILE");
+  if (v && v[0] == '4') return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
+  return mac_gemm_f64_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
+}
+
+// fp64 variant of the clip-blocked key-switch inner product.
+__global__ void __launch_bounds__(256)
+k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
+                int nb) {
+  const HbKsTask2 tk = tasks[blockIdx.y];
+  const int b = blockIdx.z * blockDim.y + threadIdx.y;
+  const int j = 2 * (blockIdx.x * 32 + threadIdx.x);
+  if (j >= n || b >= nb) return;
+  const HbPrime P = primes[tk.prime];
+  const double p = P.pd, pinv = P.pinv;
+  int s0 = j, s1 = j + 1;
+  if (tk.perm) {
+    const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+    s0 = pp.x;
+    s1 = pp.y;
+  }
+  const u64* de = tk.de + b * tk.de_bstride;
+  double b0 = 0, b1 = 0, a0 = 0, a1 = 0;
+  for (int i = 0; i < tk.ndig; ++i) {
+    const u64* d = de + i * tk.de_dstride;
+    const double x0 = u64_to_f(__ldg(d + s0)), x1 = u64_to_f(__ldg(d + s1));
+    const double q0 = x0 * pinv, q1 = x1 * pinv;
+    const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
+    const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
+    b0 += fmod_mul(u64_to_f(kb.x), x0, q0, p);
+    b1 += fmod_mul(u64_to_f(kb.y), x1, q1, p);
+    a0 += fmod_mul(u64_to_f(ka.x), x0, q0, p);
+    a1 += fmod_mul(u64_to_f(ka.y), x1, q1, p);
+  }
+  ulonglong2 rb, ra;
+  rb.x = fmod_canon(b0, p, pinv);
+  rb.y = fmod_canon(b1, p, pinv);
+  ra.x = fmod_canon(a0, p, pinv);
+  ra.y = fmod_canon(a1, p, pinv);
+  *reinterpret_cast<ulonglong2*>(tk.out_b + b * tk.out_bstride + j) = rb;
+  *reinterpret_cast<ulonglong2*>(tk.out_a + b * tk.out_bstride + j) = ra;
+}
+
+cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const HbPrime* primes,
+                                 int n, cudaStream_t st) {
+  if (ntasks <= 0 || nb <= 0) return cudaSuccess;
+  const int by = nb < 8 ? nb : 8;
+  dim3 block(32, by);
+  dim3 grid((n / 2 + 31) / 32, ntasks, (nb + by - 1) / by);
+  k_ks_inner2_f64<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
   return cudaGetLastError();
 }
 

@@ -91,3 +91,16 @@ struct HbFftTables {
   const double2* twist; // [n2]:   zeta^k = e^{i pi k / N}
   const int* slot_pos;  // [n2]:   m_j, slot j -> DFT bin
 };
+
+// Clip-blocked key-switch inner product task (ops.cu k_ks_inner2).
+struct HbKsTask2 {
+  const u64* de;      // clip 0, digit 0, row r
+  const u64* kb;      // digit 0 key row (krow[r])
+  const u64* ka;
+  u64* out_b;         // clip 0
+  u64* out_a;
+  const int* perm;
+  long long de_bstride, de_dstride, key_stride, out_bstride;
+  int ndig;
+  int prime;
+};

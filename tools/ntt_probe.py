@@ -1,7 +1,6 @@
 """Run the key-switch ModUp NTT launch a few times (ncu target)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
 from paper_2104_09164_b200.ckks.engine import CkksBackend
 from paper_2104_09164_b200.ckks.params import gen_params
 import bench
