@@ -51,6 +51,8 @@ struct hb_ring {
   HbTw* tw_inv_dev;
   HbTwD* twd_fwd_dev;
   HbTwD* twd_inv_dev;
+  double* tw1_fwd_dev;
+  double* tw1_inv_dev;
   std::vector<HbPrime> primes_host;
   int last_err;
 };
@@ -87,6 +89,7 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->primes_dev = nullptr;
   r->tw_fwd_dev = r->tw_inv_dev = nullptr;
   r->twd_fwd_dev = r->twd_inv_dev = nullptr;
+  r->tw1_fwd_dev = r->tw1_inv_dev = nullptr;
   r->dev.logn = logn;
   r->dev.n = n;
   r->dev.nprimes = nprimes;
@@ -126,6 +129,7 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.use_f64 = (f64 && !(force && force[0] == '1')) ? 1 : 0;
   std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
   std::vector<HbTwD> tfd((size_t)nprimes * n), tid((size_t)nprimes * n);
+  std::vector<double> t1f((size_t)nprimes * n), t1i((size_t)nprimes * n);
   for (int i = 0; i < nprimes; ++i) {
     const double pd = (double)primes[i];
     for (int j = 0; j < n; ++j) {
@@ -138,6 +142,8 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
       tfd[k].wq = (double)psi[k] / pd;
       tid[k].w = (double)ipsi[k];
       tid[k].wq = (double)ipsi[k] / pd;
+      t1f[k] = (double)psi[k];
+      t1i[k] = (double)ipsi[k];
     }
   }
   cudaError_t e;
@@ -151,7 +157,11 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
       (e = cudaMalloc(&r->twd_fwd_dev, sizeof(HbTwD) * tfd.size())) ||
       (e = cudaMalloc(&r->twd_inv_dev, sizeof(HbTwD) * tid.size())) ||
       (e = cudaMemcpy(r->twd_fwd_dev, tfd.data(), sizeof(HbTwD) * tfd.size(), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(r->twd_inv_dev, tid.data(), sizeof(HbTwD) * tid.size(), cudaMemcpyHostToDevice))) {
+      (e = cudaMemcpy(r->twd_inv_dev, tid.data(), sizeof(HbTwD) * tid.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMalloc(&r->tw1_fwd_dev, sizeof(double) * t1f.size())) ||
+      (e = cudaMalloc(&r->tw1_inv_dev, sizeof(double) * t1i.size())) ||
+      (e = cudaMemcpy(r->tw1_fwd_dev, t1f.data(), sizeof(double) * t1f.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(r->tw1_inv_dev, t1i.data(), sizeof(double) * t1i.size(), cudaMemcpyHostToDevice))) {
     fail(e, "hb_ring_create");
     delete r;
     return nullptr;
@@ -161,6 +171,8 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.tw_inv = r->tw_inv_dev;
   r->dev.twd_fwd = r->twd_fwd_dev;
   r->dev.twd_inv = r->twd_inv_dev;
+  r->dev.tw1_fwd = r->tw1_fwd_dev;
+  r->dev.tw1_inv = r->tw1_inv_dev;
   return r;
 }
 
@@ -171,6 +183,8 @@ void hb_ring_destroy(hb_ring* r) {
   cudaFree(r->tw_inv_dev);
   cudaFree(r->twd_fwd_dev);
   cudaFree(r->twd_inv_dev);
+  cudaFree(r->tw1_fwd_dev);
+  cudaFree(r->tw1_inv_dev);
   delete r;
 }
 

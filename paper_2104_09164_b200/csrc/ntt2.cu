@@ -23,12 +23,24 @@
 // c ^ ((c>>3)&7) ^ (((c>>6)&1)<<2), conflict-free both for the stride-8
 // 16-element groups (8-byte accesses, lanes span two blocks per half-warp)
 // and for the contiguous 8-element groups (16-byte accesses).
+#include <cstdlib>
+#include <type_traits>
 #include "ntt_common.cuh"
 
 namespace hb {
 
 constexpr int TILE = 4096;
 constexpr int THREADS2 = 256;
+// rows per launch pair (keeps the intermediate L2-resident); env override
+static int ntt_chunk() {
+  static int c = -1;
+  if (c < 0) {
+    const char* v = getenv("HEAR_B200_NTT_CHUNK");
+    c = v ? atoi(v) : 512;
+    if (c <= 0) c = 1 << 30;
+  }
+  return c;
+}
 
 HB_DEV int swz_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
 HB_DEV int swz(int j) { return (swz_chunk(j >> 1) << 1) | (j & 1); }
@@ -60,7 +72,7 @@ HB_DEV u64 as_bits(typename Pol::T v) {
 // Column pass: stages [0, S1) forward, or [7, 7+S1) inverse.  M = 2^S1
 // elements per column (stride 128), CW = TILE / M columns per CTA.
 template <class Pol, int LOGN, int MODE, bool FWD>
-__global__ void __launch_bounds__(THREADS2)
+__global__ void __launch_bounds__(THREADS2, 3)
 k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
   constexpr int GQ = M / 16;  // 16-element groups per column
@@ -146,7 +158,7 @@ k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
 //   inverse: stages 0..2 on contiguous groups of 8, then 3..6 on stride-8
 //            groups of 16; lazy intermediate store.
 template <class Pol, int LOGN, int MODE, bool FWD>
-__global__ void __launch_bounds__(THREADS2)
+__global__ void __launch_bounds__(THREADS2, 3)
 k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, NT = N / TILE;
   typedef typename Pol::T V;
@@ -181,12 +193,45 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
   __syncthreads();
   const int blk = t >> 3, cc = t & 7;   // stride-8 groups: 8 per block, 32 blocks
   const int gblk = tile * 32 + blk;     // global 128-block index
+  // fp64 policy: the tile's 32*127 twiddles (7 stages) are staged once in
+  // smem with coalesced loads, so butterflies never wait on L2.
+  constexpr bool SMTW = std::is_same<Pol, PolF64>::value;
+  extern __shared__ double tws[];        // dynamic: 4064 doubles when SMTW
+  const double pinv = P.pinv;
+  if (SMTW) {
+    const double* t1 = (FWD ? R.tw1_fwd : R.tw1_inv) + (size_t)tk.dst_prime * N;
+#pragma unroll
+    for (int e = 0; e < 7; ++e) {
+      // forward stage S1+e: 32<<e entries from 2^(S1+e) + tile*(32<<e);
+      // inverse stage e:    2048>>e entries from (N>>(e+1)) + tile*(2048>>e)
+      const int len = FWD ? (32 << e) : (2048 >> e);
+      const int off = FWD ? 32 * ((1 << e) - 1) : 4096 - (4096 >> e);
+      const int src0 = FWD ? (1 << (S1 + e)) + tile * len : (N >> (e + 1)) + tile * len;
+      for (int k = t; k < len; k += THREADS2) tws[off + k] = __ldg(t1 + src0 + k);
+    }
+    __syncthreads();
+  }
+  auto fetch_f = [&](int s, int i) {
+    const int e = s - S1, len = 32 << e;
+    const double w = tws[32 * ((1 << e) - 1) + i - tile * len];
+    return HbTwD{w, w * pinv};
+  };
+  auto fetch_i = [&](int r, int i) {
+    const int len = 2048 >> r;
+    const double w = tws[4096 - (4096 >> r) + i - tile * len];
+    return HbTwD{w, w * pinv};
+  };
   auto stride8 = [&](bool fwd) {
     V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[swz(blk * 128 + u * 8 + cc)];
-    if (fwd) fwd_group<Pol, 4>(x, S1, gblk, tw, pol);
-    else inv_group<Pol, 4>(x, 3, gblk, LOGN, tw, pol);
+    if constexpr (SMTW) {
+      if (fwd) fwd_group_f<Pol, 4>(x, S1, gblk, fetch_f, pol);
+      else inv_group_f<Pol, 4>(x, 3, gblk, fetch_i, pol);
+    } else {
+      if (fwd) fwd_group<Pol, 4>(x, S1, gblk, tw, pol);
+      else inv_group<Pol, 4>(x, 3, gblk, LOGN, tw, pol);
+    }
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[swz(blk * 128 + u * 8 + cc)] = fwd ? x[u] : pol.inv_round_end(x[u]);
   };
@@ -204,8 +249,13 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
         x[2 * v + 1] = sm[2 * pc + 1];
       }
       const int G = (tile * 32 + b2) * 16 + G8;
-      if (fwd) fwd_group<Pol, 3>(x, S1 + 4, G, tw, pol);
-      else inv_group<Pol, 3>(x, 0, G, LOGN, tw, pol);
+      if constexpr (SMTW) {
+        if (fwd) fwd_group_f<Pol, 3>(x, S1 + 4, G, fetch_f, pol);
+        else inv_group_f<Pol, 3>(x, 0, G, fetch_i, pol);
+      } else {
+        if (fwd) fwd_group<Pol, 3>(x, S1 + 4, G, tw, pol);
+        else inv_group<Pol, 3>(x, 0, G, LOGN, tw, pol);
+      }
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int pc = swz_chunk((e0 >> 1) + v);
@@ -272,8 +322,16 @@ template <int LOGN, bool F64, int MODE>
 static cudaError_t fwd2_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   typedef typename std::conditional<F64, PolF64, PolU64>::type Pol;
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
-  k_ntt2_cols<Pol, LOGN, MODE, true><<<count * NCH, THREADS2, 0, st>>>(tasks, R);
-  k_ntt2_blocks<Pol, LOGN, MODE, true><<<count * ((1 << LOGN) / TILE), THREADS2, 0, st>>>(tasks, R);
+  const size_t dyn = F64 ? 4064 * sizeof(double) : 0;
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt2_blocks<Pol, LOGN, MODE, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  const int CH = ntt_chunk();
+  for (int c0 = 0; c0 < count; c0 += CH) {   // chunks keep the intermediate in L2
+    const int c = count - c0 < CH ? count - c0 : CH;
+    k_ntt2_cols<Pol, LOGN, MODE, true><<<c * NCH, THREADS2, 0, st>>>(tasks + c0, R);
+    k_ntt2_blocks<Pol, LOGN, MODE, true><<<c * ((1 << LOGN) / TILE), THREADS2, dyn, st>>>(tasks + c0, R);
+  }
   return cudaGetLastError();
 }
 
@@ -281,9 +339,17 @@ template <int LOGN, bool F64>
 static cudaError_t inv2_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   typedef typename std::conditional<F64, PolF64, PolU64>::type Pol;
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
-  k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false><<<count * ((1 << LOGN) / TILE), THREADS2, 0, st>>>(tasks, R);
-  // the column pass reads the block pass's lazy output from dst
-  k_ntt2_cols<Pol, LOGN, FWD_PLAIN, false><<<count * NCH, THREADS2, 0, st>>>(tasks, R);
+  const size_t dyn = F64 ? 4064 * sizeof(double) : 0;
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  const int CH = ntt_chunk();
+  for (int c0 = 0; c0 < count; c0 += CH) {
+    const int c = count - c0 < CH ? count - c0 : CH;
+    k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false><<<c * ((1 << LOGN) / TILE), THREADS2, dyn, st>>>(tasks + c0, R);
+    // the column pass reads the block pass's lazy output from dst
+    k_ntt2_cols<Pol, LOGN, FWD_PLAIN, false><<<c * NCH, THREADS2, 0, st>>>(tasks + c0, R);
+  }
   return cudaGetLastError();
 }
 

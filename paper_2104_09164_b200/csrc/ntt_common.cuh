@@ -91,6 +91,34 @@ struct PolF64 {
   HB_DEV u64 inv_final(T x) const { return fmod_canon(fmod_mul(x, ninv, ninvq, p), p, pinv); }
 };
 
+// Butterfly groups with a caller-supplied twiddle fetch (stage, group index)
+// -> Pol::Tw; used by the block pass, which stages its twiddles in smem.
+template <class Pol, int K, class F>
+HB_DEV void fwd_group_f(typename Pol::T* x, int s0, int G, F fetch, const Pol& pol) {
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int h = 1 << (K - 1 - st);
+#pragma unroll
+    for (int u = 0; u < (1 << K); ++u) {
+      if (u & h) continue;
+      pol.fwd(x[u], x[u + h], fetch(s0 + st, G * ((1 << K) / (2 * h)) + u / (2 * h)));
+    }
+  }
+}
+
+template <class Pol, int K, class F>
+HB_DEV void inv_group_f(typename Pol::T* x, int r0, int G, F fetch, const Pol& pol) {
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int r = r0 + st, hh = 1 << st;
+#pragma unroll
+    for (int u = 0; u < (1 << K); ++u) {
+      if (u & hh) continue;
+      pol.inv(x[u], x[u + hh], fetch(r, ((G << (r0 + K)) >> (r + 1)) + u / (2 * hh)));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Butterfly groups.
 

@@ -24,6 +24,8 @@ struct HbRing {
   const HbTw* tw_inv;     // [nprimes][n]  psi^-brv(j)  (true inverse)
   const HbTwD* twd_fwd;   // fp64 copies of the two tables
   const HbTwD* twd_inv;
+  const double* tw1_fwd;  // fp64 powers only (8 B entries, staged in smem by ntt2.cu)
+  const double* tw1_inv;
 };
 
 // One row-polynomial transform.  Field meaning depends on the kernel mode;
