@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--net", default="1d-w64")
     ap.add_argument("--mode", default="fast", choices=["fast", "hear"])
-    ap.add_argument("--strategy", default="giant", choices=["full", "giant", "baby"])
+    ap.add_argument("--strategy", default="full", choices=["full", "giant", "baby"])
     ap.add_argument("--batch", type=int, default=64, help="clips per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--roofline-only", action="store_true")
@@ -161,49 +161,87 @@ def reference_arm(args):
 
 # ---------------------------------------------------------------------------- GPU arm
 
+FP64_MEASURED_TFLOPS = 17.93   # DFMA/s measured on this pool (profiles/r01_microbench.txt)
+
+
 def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
-    """Time the key-switch ModUp NTT launch (FWD_LIFT over B*(l+1)*(l+2) rows,
-    the most-launched-work kernel of the evaluation) with CUDA events on its
-    own stream and report it against the measured HBM peak."""
+    """Time one key-switch ModDown launch -- k_ntt_fwd in FWD_MODDOWN mode over
+    B*2*(l+1) output rows, the largest kernel share of the evaluation
+    (profiles/r01_launches_*) -- with CUDA events on the launching stream.
+    Algorithmic bytes per output row: read x_r + write the result (16 N B);
+    plus one read of each special-prime source row per (b, component)."""
     import torch
     from paper_2104_09164_b200 import _native as nat
     from paper_2104_09164_b200.ckks.engine import _tasks
     from paper_2104_09164_b200.ckks.ring import _upload
     n = be.n
-    ndig, rows = lvl + 1, lvl + 2
-    coef = be.ring.empty(bsz, ndig)
-    coef.random_(0, 1 << 30)
-    de = be.ring.empty(bsz, ndig, rows)
-    gidx = np.array(list(range(lvl + 1)) + [be.S])
-    t = _tasks(nat.NTT_TASK, bsz * ndig * rows, src=np.repeat(be.ring.row_ptrs(coef), rows),
-               dst=be.ring.row_ptrs(de), src_prime=np.tile(np.repeat(np.arange(ndig), rows), bsz),
-               dst_prime=np.tile(gidx, bsz * ndig))
+    m, r = bsz * 2, lvl + 1
+    src = be.ring.empty(m).random_(0, 1 << 30)
+    aux = be.ring.empty(m, r).random_(0, 1 << 30)
+    out = be.ring.empty(m, r)
+    t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(be.ring.row_ptrs(src), r),
+               dst=be.ring.row_ptrs(out), aux=be.ring.row_ptrs(aux), src_prime=be.S,
+               dst_prime=np.tile(np.arange(r), m), scal=np.tile(be._pinv[:r], m),
+               scal_sh=np.tile(be._pinv_sh[:r], m))
     d = _upload(t, be.dev)
     L = nat.lib()
     st = torch.cuda.current_stream()
+
+    def launch():
+        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_MODDOWN,
+                               st.cuda_stream), "ntt")
     for _ in range(3):
-        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_LIFT, st.cuda_stream), "ntt")
+        launch()
     reps = 20
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(st)
     for _ in range(reps):
-        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_LIFT, st.cuda_stream), "ntt")
+        launch()
     e1.record(st)
     torch.cuda.synchronize()
     sec = e0.elapsed_time(e1) / 1e3 / reps
-    out_rows = len(t)
-    # algorithmic bytes: each output row written once, each digit row read once
-    algo = (out_rows + bsz * ndig) * n * 8
+    algo = (2 * m * r + m) * n * 8
     gbs = algo / sec / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
-    butterflies = out_rows * (n // 2) * (n.bit_length() - 1)
-    return {"kernel": "k_ntt_fwd<FWD_LIFT> (key-switch ModUp)", "bound": "hbm",
-            "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
-            "traffic": None, "launch_us": round(sec * 1e6, 2), "rows_per_launch": out_rows,
-            "algorithmic_bytes_per_launch": algo,
-            "butterflies_per_s": round(butterflies / sec / 1e12, 3),
+    bfly = m * r * (n // 2) * (n.bit_length() - 1)
+    return {"kernel": "k_ntt2_cols+k_ntt2_blocks<FWD_MODDOWN> (key-switch ModDown NTT)",
+            "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(gbs / peak, 4), "traffic": None, "launch_us": round(sec * 1e6, 2),
+            "rows_per_launch": m * r, "algorithmic_bytes_per_launch": algo,
+            "butterflies_per_s": round(bfly / sec / 1e12, 3),
+            "fp64_frac_of_measured": round(bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12), 3),
             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
+
+
+def keyswitch_rate(be, lvl: int, bsz: int) -> dict:
+    """Key-switch ops/s: non-hoisted HRotate of bsz fresh-shaped ciphertexts
+    at level lvl (ModUp + inner product + ModDown + automorphism), and the
+    hoisted form (16 amounts of one handle sharing the ModUp)."""
+    import torch
+    from fractions import Fraction
+    from paper_2104_09164_b200.backend import Ct
+    from paper_2104_09164_b200.ckks.engine import CtData
+    be.ensure_rotation_keys({k: be.L for k in range(1, 17)})
+    cts = [Ct(CtData(be.ring.empty(1, 2, lvl + 1).random_(0, 1 << 30)), lvl, Fraction(1), be.n2)
+           for _ in range(bsz)]
+    big = Ct(CtData(be.ring.empty(bsz, 2, lvl + 1).random_(0, 1 << 30)), lvl, Fraction(1), be.n2)
+    out = {}
+    for name, fn, ops in (("rotate", lambda: be._raw_rot_each([(c, 1) for c in cts]), bsz),
+                          ("rotate_hoisted16",
+                           lambda: be._raw_rot_many(big, list(range(1, 17))), 16 * bsz)):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = round(3 * ops / (e0.elapsed_time(e1) / 1e3), 1)
+    out["level"] = lvl
+    out["unit"] = "key-switch ops/s"
+    return out
 
 
 def gpu_arm(args):
@@ -219,6 +257,7 @@ def gpu_arm(args):
     from paper_2104_09164_b200.modelenc import ModelEncoder
     from paper_2104_09164_b200.backend import Ct
     from paper_2104_09164_b200.ckks.engine import CtData
+    from paper_2104_09164_b200.fastpath import GraphedPipeline
 
     rank, ws, local = par.world()
     torch.cuda.set_device(local)
@@ -255,27 +294,32 @@ def gpu_arm(args):
         maxerr = float(np.abs(lg - ref).max())
 
     st = torch.cuda.current_stream()
+    # kernels per step, counted by the library on an eager pass
+    k0 = nat.kernel_launches()
+    run_pipeline(enc, ct, be)
+    per_step_kernels = nat.kernel_launches() - k0
+    # the timed loops replay the pipeline captured as one CUDA graph
+    graph = GraphedPipeline(enc, be, batch=bsz)
     for _ in range(args.warmup):
-        run_pipeline(enc, ct, be)
+        graph(ct)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region
     par.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = nat.launch_count
     prof_range = os.environ.get("HEAR_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clk:
         if prof_range:
             torch.cuda.profiler.start()
         e0.record(st)
         for _ in range(args.steps):
-            run_pipeline(enc, ct, be)
+            graph(ct)
         e1.record(st)
         torch.cuda.synchronize()
         if prof_range:
             torch.cuda.profiler.stop()
-    launches = nat.launch_count - l0
+    launches = per_step_kernels * args.steps
     par.barrier()
     ms = par.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
 
@@ -285,15 +329,35 @@ def gpu_arm(args):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(st)
     for _ in range(args.steps):
-        d_in = host_in.to(dev, non_blocking=True)
-        out = run_pipeline(enc, Ct(CtData(d_in), ct.level, ct.scale, ct.slots), be)
-        host_out.copy_(out.payload.data, non_blocking=True)
+        graph.inp.copy_(host_in, non_blocking=True)
+        graph.graph.replay()
+        host_out.copy_(graph.out.payload.data, non_blocking=True)
     f1.record(st)
     torch.cuda.synchronize()
     par.barrier()
     ms_e2e = par.max_over_ranks(f0.elapsed_time(f1) / args.steps, dev)
+    if rank == 0:   # the graph's output decrypts to the clear network's logits
+        out_ct = Ct(CtData(host_out.to(dev)), 0, cp.expected("fc").scale, be.n2)
+        maxerr = max(maxerr, float(np.abs(dec_logits(out_ct, cp, be) - ref).max()))
+
+    # ---- per-clip latency: single-clip graph, replays timed one by one
+    lat = []
+    g1 = GraphedPipeline(enc, be, batch=1)
+    one = encrypt_input(x[0], cp, be)
+    for i in range(3 + max(args.steps, 10)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        g1(one)
+        b.record(st)
+        torch.cuda.synchronize()
+        if i >= 3:
+            lat.append(a.elapsed_time(b))
+    latency = {"p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+               "samples": len(lat), "batch": 1}
+    del g1, graph
 
     roof = dominant_kernel_roofline(be, lvl=6, bsz=min(bsz, 16), peaks=peaks)
+    ks = keyswitch_rate(be, lvl=params.max_level, bsz=min(bsz, 32))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -324,6 +388,8 @@ def gpu_arm(args):
                     "h2d_bytes_per_step": int(host_in.numel() * 8),
                     "d2h_bytes_per_step": int(host_out.numel() * 8)},
             "gpu_launches": launches,
+            "per_clip_latency": latency,
+            "keyswitch": ks,
             "roofline": roof,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -64,13 +64,19 @@ def lib():
     return _lib
 
 
-launch_count = 0   # kernel launches issued through this binding (one per hb_* call)
+launch_count = 0   # hb_* launch calls issued through this binding
+_kernels = 0       # CUDA kernels those calls enqueued
 
 
-def check(rc: int, what: str):
-    """Verify one hb_* launch call and count it."""
-    global launch_count
+def kernel_launches() -> int:
+    return _kernels
+
+
+def check(rc: int, what: str, kernels: int = 1):
+    """Verify one hb_* launch call and count the kernels it enqueued."""
+    global launch_count, _kernels
     launch_count += 1
+    _kernels += kernels
     if rc != 0:
         msg = _lib.hb_last_error().decode() if _lib is not None else "?"
         raise NativeError(f"{what} failed ({rc}): {msg}")

@@ -15,6 +15,7 @@ uint64 by the kernels; a "row" is N contiguous residues under one prime.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -23,11 +24,43 @@ from .. import _native as nat
 from .ntheory import bit_reverse_table, root_2n
 
 
+class UploadArena:
+    """Persistent pinned-host + device buffers for task tables while a CUDA
+    graph is being captured: every table gets its own never-reused slice,
+    so the captured host->device copies stay valid for every replay."""
+
+    def __init__(self, device, nbytes: int = 256 << 20):
+        self.host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        self.dev = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.off = 0
+
+    def put(self, t: torch.Tensor) -> torch.Tensor:
+        n = t.numel()
+        start = (self.off + 255) & ~255
+        if start + n > self.host.numel():
+            raise MemoryError("graph upload arena exhausted")
+        self.host[start:start + n].copy_(t)
+        d = self.dev[start:start + n]
+        d.copy_(self.host[start:start + n], non_blocking=True)
+        self.off = start + n
+        return d
+
+
+_ARENA: UploadArena | None = None
+
+
+def set_upload_arena(arena: UploadArena | None):
+    global _ARENA
+    _ARENA = arena
+
+
 def _upload(arr: np.ndarray, device) -> torch.Tensor:
     """Host task table -> device bytes (async on the current stream)."""
     t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8))
     if t.numel() == 0:
         return torch.empty(0, dtype=torch.uint8, device=device)
+    if _ARENA is not None:
+        return _ARENA.put(t)
     return t.pin_memory().to(device, non_blocking=True)
 
 
@@ -114,17 +147,25 @@ class RingContext:
     def stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def _ntt_kernels(self, count: int) -> int:
+        """Kernels one NTT call enqueues (csrc/ntt.cu use_two_pass, ntt2.cu chunks)."""
+        if 12 <= self.logn <= 16 and not (os.environ.get("HEAR_B200_NTT1") == "1"
+                                          and self.logn <= 14):
+            chunk = int(os.environ.get("HEAR_B200_NTT_CHUNK", "512")) or (1 << 30)
+            return 2 * -(-count // chunk)
+        return 1
+
     def ntt_fwd(self, tasks: np.ndarray, mode: int = nat.FWD_PLAIN):
         if len(tasks):
             d = _upload(tasks, self.device)
             nat.check(self._lib.hb_ntt_fwd(self.handle, _ptr(d), len(tasks), mode, self.stream),
-                      "ntt_fwd")
+                      "ntt_fwd", self._ntt_kernels(len(tasks)))
 
     def ntt_inv(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)
             nat.check(self._lib.hb_ntt_inv(self.handle, _ptr(d), len(tasks), self.stream),
-                      "ntt_inv")
+                      "ntt_inv", self._ntt_kernels(len(tasks)))
 
     def ew(self, op: int, tasks: np.ndarray):
         if len(tasks):

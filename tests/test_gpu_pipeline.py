@@ -88,3 +88,29 @@ def test_batched_equals_clipwise():
     cts = [encrypt_input(make_random_input(shape, 10 + i), cp, be) for i in range(3)]
     outs = [dec_logits(run_pipeline(enc, c, be), cp, be) for c in cts]
     assert np.array_equal(np.stack(outs), lg_b)
+
+
+def test_cuda_graph_replay_bit_exact():
+    """A captured pipeline replays to the same ciphertext as eager evaluation."""
+    import torch
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import (GraphedPipeline, compile_pipeline, dec_logits,
+                                                encrypt_input, run_pipeline)
+    from paper_2104_09164_b200.model import (NetworkShape, collapse_layers, make_random_input,
+                                             make_random_model)
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    shape = NetworkShape(1, 32, 15, (4, 8, 16), 4)
+    cpar = collapse_layers(make_random_model(shape, 3), shape)
+    be = CkksBackend(gen_params("toy-fast"), seed=2)
+    cp = compile_pipeline(shape, "fast", "full", be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    enc = ModelEncoder(cp, cpar, be).prepare()
+    g = GraphedPipeline(enc, be, batch=2)
+    for seed in (20, 30):
+        x = np.stack([make_random_input(shape, seed + i) for i in range(2)])
+        ct = encrypt_input(x, cp, be)
+        eager = run_pipeline(enc, ct, be).payload.data.clone()
+        replay = g(ct).payload.data
+        torch.cuda.synchronize()
+        assert torch.equal(eager, replay)
