@@ -109,7 +109,7 @@ CRT_TASK = np.dtype([("rows", "<u8"), ("out", "<u8")])
 FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64 = 0, 1, 2, 3
 # element-wise ops (csrc/ops.cu EwOp)
 EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PERM, \
-    EW_SUB_SCALED = range(9)
+    EW_SUB_SCALED, EW_PERM_ADD = range(10)
 
 
 def _check_layouts():

@@ -68,12 +68,16 @@ class CtData:
 
 
 class _Ksk:
-    __slots__ = ("b", "a", "lmax")
+    __slots__ = ("b", "a", "lmax", "bp", "ap")
 
     def __init__(self, b, a, lmax):
-        self.b = b          # [ndig, lmax+2, N] device
+        self.b = b          # [ndig, lmax+2, N] device (reference layout)
         self.a = a
         self.lmax = lmax
+        # rotation keys only: columns pre-permuted by the inverse Galois
+        # permutation, so the inner product needs no gather (see _ks_apply_many)
+        self.bp = None
+        self.ap = None
 
 
 class KeyMaterial:
@@ -283,6 +287,30 @@ class CkksBackend(BackendBase):
             sg = self.ring.coeff_automorphism(self.keys.s_coeffs, g)
             target = self._coeffs_to_ntt(self._dev(sg)[None], self._full_gidx(lmax))[0]
             self.keys.rot[amount] = self._make_ksk(target, lmax)
+            self._permute_key(amount)
+
+    def _permute_key(self, amount: int):
+        """K'[m] = K[pi^-1(m)] for every key row: with it the rotation's inner
+        product reads the digits in natural order and the Galois gather moves
+        to one pass after ModDown (ModDown commutes with the automorphism)."""
+        key = self.keys.rot[amount]
+        perm = self.ring.ntt_perm(self.ring.galois_element(amount))
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(len(perm), dtype=perm.dtype)
+        pinv = torch.from_numpy(inv).to(self.dev)
+        rp = self.ring.row_ptrs
+        key.bp, key.ap = torch.empty_like(key.b), torch.empty_like(key.a)
+        for src, dst in ((key.b, key.bp), (key.a, key.ap)):
+            rows = src.numel() // self.n
+            self._ew(nat.EW_PERM, rp(dst), rp(src), np.full(rows, pinv.data_ptr(), dtype=np.uint64),
+                     primes=np.zeros(rows, dtype=np.int64))
+
+    def finish_keys(self):
+        """Derive the permuted rotation keys after keys were received from
+        another rank (parallel.replicate_keys)."""
+        for amount, key in self.keys.rot.items():
+            if key.bp is None:
+                self._permute_key(amount)
 
     # ------------------------------------------------------------------ codec
 
@@ -552,20 +580,27 @@ class CkksBackend(BackendBase):
         parts = []
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
         perms = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
+        late = []   # (job, perm, c0 ptrs) whose Galois gather runs after ModDown
         for j, job in enumerate(jobs):
             key, perm, addend, gather_c0 = job[:4]
             off = job[4] if len(job) > 4 else 0
             if key.lmax < lvl:
                 raise LevelScaleError(f"key switching key trimmed to level {key.lmax}, need {lvl}")
             krow = np.array(list(range(lvl + 1)) + [key.lmax + 1])
-            kbr = rp(key.b).reshape(key.b.shape[0], key.lmax + 2)[0, krow]
-            kar = rp(key.a).reshape(key.a.shape[0], key.lmax + 2)[0, krow]
+            prepermuted = perm is not None and key.bp is not None
+            kb_t, ka_t = (key.bp, key.ap) if prepermuted else (key.b, key.a)
+            kbr = rp(kb_t).reshape(kb_t.shape[0], key.lmax + 2)[0, krow]
+            kar = rp(ka_t).reshape(ka_t.shape[0], key.lmax + 2)[0, krow]
             parts.append(_tasks(
                 nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
-                out_a=ipr[j, 0, 1], perm=perm.data_ptr() if perm is not None else 0,
+                out_a=ipr[j, 0, 1],
+                perm=perm.data_ptr() if perm is not None and not prepermuted else 0,
                 de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
                 key_stride=(key.lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
                 prime=gidx))
+            if prepermuted:
+                late.append((j, perm, addend[:, 0] if addend is not None else None))
+                continue
             if addend is not None:
                 add[j] = addend
                 if gather_c0 and perm is not None:
@@ -585,7 +620,41 @@ class CkksBackend(BackendBase):
                    add=add.ravel(), perm=perms.ravel())
         self.ring.ntt_fwd(t, nat.FWD_MODDOWN)
         out = out.reshape(nj, bsz, 2, r, self.n)
-        return [out[j] for j in range(nj)]
+        res = [out[j] for j in range(nj)]
+        if late:
+            # ModDown(x o pi) = ModDown(x) o pi: gather the rotation now,
+            # c0' = md_b[pi] + c0[pi], c1' = md_a[pi]
+            fin = self.ring.empty(len(late), bsz, 2, r)
+            finr = rp(fin).reshape(len(late), bsz, 2, r)
+            outr = rp(out).reshape(nj, bsz, 2, r)
+            d0, a0, b0, p0, d1, a1, p1 = [], [], [], [], [], [], []
+            for q, (j, perm, c0) in enumerate(late):
+                pp = np.full(bsz * r, perm.data_ptr(), dtype=np.uint64)
+                if c0 is not None:
+                    d0.append(finr[q, :, 0].ravel())
+                    a0.append(outr[j, :, 0].ravel())
+                    b0.append(np.asarray(c0, dtype=np.uint64).ravel())
+                    p0.append(pp)
+                else:
+                    d1.append(finr[q, :, 0].ravel())
+                    a1.append(outr[j, :, 0].ravel())
+                    p1.append(pp)
+                d1.append(finr[q, :, 1].ravel())
+                a1.append(outr[j, :, 1].ravel())
+                p1.append(pp)
+            if d0:
+                nrow = sum(len(x) for x in d0)
+                self.ring.ew(nat.EW_PERM_ADD, _tasks(
+                    nat.EW_TASK, nrow, dst=np.concatenate(d0), a=np.concatenate(a0),
+                    b=np.concatenate(b0), c=np.concatenate(p0),
+                    prime=np.tile(np.arange(r), nrow // r)))
+            nrow = sum(len(x) for x in d1)
+            self.ring.ew(nat.EW_PERM, _tasks(
+                nat.EW_TASK, nrow, dst=np.concatenate(d1), a=np.concatenate(a1),
+                b=np.concatenate(p1), prime=np.tile(np.arange(r), nrow // r)))
+            for q, (j, _, _) in enumerate(late):
+                res[j] = fin[q]
+        return res
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)

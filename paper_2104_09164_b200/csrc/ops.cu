@@ -20,6 +20,8 @@ enum EwOp : int {
   EW_COPY = 6,      // dst = a
   EW_PERM = 7,      // dst = a[perm]  (b reinterpreted as int32 perm)
   EW_SUB_SCALED = 8,// dst = (a - b) * scal              (ring.py:210 sub_scaled_inv)
+  EW_PERM_ADD = 9,  // dst = a[perm] + b[perm]  (c reinterpreted as int32 perm): the
+                    // Galois gather of a rotation applied after ModDown (engine.py:350)
 };
 
 constexpr int EW_THREADS = 256;
@@ -63,6 +65,11 @@ k_ew(const HbEwTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__
       const int* perm = reinterpret_cast<const int*>(tk.b);
       r.x = __ldg(tk.a + __ldg(perm + j));
       r.y = __ldg(tk.a + __ldg(perm + j + 1));
+    } else if (OP == EW_PERM_ADD) {
+      const int* perm = reinterpret_cast<const int*>(tk.c);
+      const int2 pp = __ldg(reinterpret_cast<const int2*>(perm + j));
+      r.x = add_mod(__ldg(tk.a + pp.x), __ldg(tk.b + pp.x), p);
+      r.y = add_mod(__ldg(tk.a + pp.y), __ldg(tk.b + pp.y), p);
     }
     *reinterpret_cast<ulonglong2*>(tk.dst + j) = r;
   }
@@ -89,6 +96,7 @@ cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* 
     HB_EW_CASE(EW_COPY)
     HB_EW_CASE(EW_PERM)
     HB_EW_CASE(EW_SUB_SCALED)
+    HB_EW_CASE(EW_PERM_ADD)
 #undef HB_EW_CASE
     default: return cudaErrorInvalidValue;
   }

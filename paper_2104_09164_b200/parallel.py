@@ -62,6 +62,8 @@ def replicate_keys(backend, src: int = 0):
     if dist.get_rank() != src:
         backend.alloc_keys(manifest)
     broadcast_tensors([t for _, t in backend.key_tensors()], src)
+    if dist.get_rank() != src and hasattr(backend, "finish_keys"):
+        backend.finish_keys()
 
 
 def max_over_ranks(value: float, device=None) -> float:
