@@ -17,7 +17,8 @@ LIB = os.path.join(LIBDIR, "libhear_b200.so")
 SOURCES = ["ntt.cu", "ntt2.cu", "ops.cu", "fft.cu", "cabi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + \
+    os.environ.get("HB_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:

@@ -31,6 +31,9 @@ namespace hb {
 
 constexpr int TILE = 4096;
 constexpr int THREADS2 = 256;
+#ifndef HB_NTT2_MINB
+#define HB_NTT2_MINB 3
+#endif
 // rows per launch pair (keeps the intermediate L2-resident); env override
 static int ntt_chunk() {
   static int c = -1;
@@ -72,7 +75,7 @@ HB_DEV u64 as_bits(typename Pol::T v) {
 // Column pass: stages [0, S1) forward, or [7, 7+S1) inverse.  M = 2^S1
 // elements per column (stride 128), CW = TILE / M columns per CTA.
 template <class Pol, int LOGN, int MODE, bool FWD>
-__global__ void __launch_bounds__(THREADS2, 3)
+__global__ void __launch_bounds__(THREADS2, HB_NTT2_MINB)
 k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
   constexpr int GQ = M / 16;  // 16-element groups per column
@@ -158,7 +161,7 @@ k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
 //   inverse: stages 0..2 on contiguous groups of 8, then 3..6 on stride-8
 //            groups of 16; lazy intermediate store.
 template <class Pol, int LOGN, int MODE, bool FWD>
-__global__ void __launch_bounds__(THREADS2, 3)
+__global__ void __launch_bounds__(THREADS2, HB_NTT2_MINB)
 k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, NT = N / TILE;
   typedef typename Pol::T V;
