@@ -11,6 +11,7 @@
 //            launch, copy out and synchronise.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -33,6 +34,9 @@ cudaError_t launch_mac_gemm(const void*, const void*, const void*, int, int, con
 cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int, const HbPrime*,
                                 int, int, int, cudaStream_t);
 cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, const HbRing&, int,
+                               int, cudaStream_t);
+cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
 struct HbCrtTask;
 cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
@@ -53,6 +57,8 @@ struct hb_ring {
   HbTwD* twd_inv_dev;
   double* tw1_fwd_dev;
   double* tw1_inv_dev;
+  double* chunk_dev = nullptr;
+  std::vector<double> chunk_host;
   std::vector<HbPrime> primes_host;
   int last_err;
 };
@@ -127,6 +133,30 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   for (int i = 0; i < nprimes; ++i) f64 = f64 && primes[i] < (1ull << 42);
   const char* force = getenv("HEAR_B200_INT_NTT");
   r->dev.use_f64 = (f64 && !(force && force[0] == '1')) ? 1 : 0;
+  // chunked dot products: B = max prime bits, three w-bit limbs (w = ceil(B/3)),
+  // F terms per exact fp64 accumulation with F * 2^(B+w) + 2^B <= 2^53
+  {
+    int B = 0;
+    for (int i = 0; i < nprimes; ++i) B = std::max(B, 64 - __builtin_clzll(primes[i]));
+    const int w = (B + 2) / 3;
+    const int room = 53 - B - w - 1;
+    // opt-in: measured no faster than fmod_mul products (the dot-product
+    // kernels are load-latency bound, profiles/r01_*), kept for experiments
+    const char* on = getenv("HEAR_B200_CHUNK");
+    r->dev.chunk_w = w;
+    r->dev.chunk_fold = (r->dev.use_f64 && room >= 1 && (on && on[0] == '1'))
+                            ? (1 << std::min(room, 8)) : 0;
+    r->chunk_host.resize((size_t)nprimes * 4);
+    for (int i = 0; i < nprimes; ++i) {
+      const unsigned long long p = primes[i];
+      const unsigned long long s1 = (unsigned long long)(((unsigned __int128)1 << w) % p);
+      const unsigned long long s2 = (unsigned long long)(((unsigned __int128)s1 * s1) % p);
+      r->chunk_host[4 * i + 0] = (double)s1;
+      r->chunk_host[4 * i + 1] = (double)s1 / (double)p;
+      r->chunk_host[4 * i + 2] = (double)s2;
+      r->chunk_host[4 * i + 3] = (double)s2 / (double)p;
+    }
+  }
   std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
   std::vector<HbTwD> tfd((size_t)nprimes * n), tid((size_t)nprimes * n);
   std::vector<double> t1f((size_t)nprimes * n), t1i((size_t)nprimes * n);
@@ -173,6 +203,13 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.twd_inv = r->twd_inv_dev;
   r->dev.tw1_fwd = r->tw1_fwd_dev;
   r->dev.tw1_inv = r->tw1_inv_dev;
+  if (cudaMalloc(&r->chunk_dev, sizeof(double) * r->chunk_host.size()) ||
+      cudaMemcpy(r->chunk_dev, r->chunk_host.data(), sizeof(double) * r->chunk_host.size(),
+                 cudaMemcpyHostToDevice)) {
+    snprintf(g_err, sizeof(g_err), "hb_ring_create: chunk constants upload failed");
+    return nullptr;
+  }
+  r->dev.chunk_consts = r->chunk_dev;
   return r;
 }
 
@@ -185,6 +222,7 @@ void hb_ring_destroy(hb_ring* r) {
   cudaFree(r->twd_inv_dev);
   cudaFree(r->tw1_fwd_dev);
   cudaFree(r->tw1_inv_dev);
+  cudaFree(r->chunk_dev);
   delete r;
 }
 
@@ -253,6 +291,8 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
   cudaError_t e = (old && old[0] == '1')
       ? launch_mac_shared(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
                           (cudaStream_t)stream)
+      : r->dev.chunk_fold
+      ? launch_mac_gemm_c3(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream)
       : r->dev.use_f64
       ? launch_mac_gemm_f64(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
                             (cudaStream_t)stream)
@@ -262,7 +302,9 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
 }
 
 int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {
-  cudaError_t e = r->dev.use_f64
+  cudaError_t e = r->dev.chunk_fold
+      ? launch_ks_inner_c3(tasks, count, nb, r->dev, (cudaStream_t)stream)
+      : r->dev.use_f64
       ? launch_ks_inner2_f64(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream)
       : launch_ks_inner2(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_inner2") : 0;

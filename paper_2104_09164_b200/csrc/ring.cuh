@@ -26,6 +26,12 @@ struct HbRing {
   const HbTwD* twd_inv;
   const double* tw1_fwd;  // fp64 powers only (8 B entries, staged in smem by ntt2.cu)
   const double* tw1_inv;
+  // chunked exact dot products (ops.cu k_mac_gemm_c3): ciphertext residues
+  // split into three chunk_w-bit limbs; products summed exactly in fp64 for
+  // chunk_fold terms between reductions (0 = disabled for this ring)
+  int chunk_w;
+  int chunk_fold;
+  const double* chunk_consts;  // [nprimes][4]: 2^w mod p, fl(./p), 2^2w mod p, fl(./p)
 };
 
 // One row-polynomial transform.  Field meaning depends on the kernel mode;

@@ -153,3 +153,24 @@ def test_integer_ntt_policy_bit_exact(golden):
     assert digest(*be.export(be._raw_rescale(A))) == g["ops"]["6"]["rescale"]
     m = be._raw_rot_many(A, [1, 5])
     assert digest(*be.export(m[5])) == g["ops"]["6"]["rot_many_5"]
+
+
+def test_chunked_dot_products_bit_exact(golden):
+    """The opt-in chunked fp64 dot products (csrc/dot.cu) equal the default path."""
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    os.environ["HEAR_B200_CHUNK"] = "1"
+    try:
+        be = CkksBackend(gen_params("toy-fast"), seed=7)
+    finally:
+        del os.environ["HEAR_B200_CHUNK"]
+    g = golden["toy-fast"]
+    ps = be.params
+    be.ensure_rotation_keys({int(a): l for a, l in g["rot_levels"].items()})
+    for lvl in (12, 6):
+        A = be.import_ct(*rand_ct(ps, lvl, 100 + lvl), lvl, ps.msg_scale)
+        B = be.import_ct(*rand_ct(ps, lvl, 200 + lvl), lvl, ps.msg_scale)
+        assert digest(*be.export(be._raw_mult(A, B))) == g["ops"][str(lvl)]["mult"]
+    m = be._raw_rot_many(A, [1, 5])
+    assert digest(*be.export(m[5])) == g["ops"]["6"]["rot_many_5"]
