@@ -226,6 +226,19 @@ def hconv(cts: list, weights: ConvWeights, plan: ConvPlan, backend: BackendBase,
     for j0 in range(0, plan.n_o, j_chunk):
         js = range(j0, min(plan.n_o, j0 + j_chunk))
         jobs, rot_amt, owner = [], [], []
+        if plan.strategy == "full":
+            # no partial-sum rotations: each output is one accumulation over all
+            # f*ell_i*m products (same mult_plain/add counts as the per-tap
+            # partials plus their sum, and the same exact modular sum), and
+            # every output shares the same hoisted term list -> one MAC group
+            fj = []
+            for j in js:
+                pts = weights.for_output(j)
+                fj.append([(pre[i][(taps[k] + blocks[l]) % n2], pts[(i, k, l)])
+                           for k in range(plan.f) for l in range(plan.ell_i)
+                           for i in range(plan.m)])
+            outs += backend.rescale_each(backend.mac_many(fj))
+            continue
         for j in js:
             pts = weights.for_output(j)
             if plan.strategy == "baby":

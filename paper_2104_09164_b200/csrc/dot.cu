@@ -51,12 +51,12 @@ k_mac_gemm_c3(HbMacGroupC g, const HbPrime* __restrict__ primes, const double* _
   const u64* const* cts = ptrs;
   const u64* const* pts = ptrs + T;
   u64* const* dsts = const_cast<u64* const*>(ptrs + T + O * T);
-  const int nchunk = n / 32;
-  const int r = blockIdx.x / nchunk;
-  const int j = (blockIdx.x % nchunk) * 32 + threadIdx.x;
+  const int nchunk = n / 32;   // grid order as ops.cu k_mac_gemm (positions slowest)
+  const int r = blockIdx.z / nchunk;
+  const int j = (blockIdx.z % nchunk) * 32 + threadIdx.x;
   const int wi = threadIdx.y;
   const int o0 = (blockIdx.y * WO + wi / WB) * TO;
-  const int b0 = (blockIdx.z * WB + wi % WB) * TB;
+  const int b0 = (blockIdx.x * WB + wi % WB) * TB;
   if (o0 >= O || b0 >= BC) return;
   const HbPrime P = primes[r];
   const double p = P.pd, pinv = P.pinv;
@@ -114,12 +114,21 @@ template <int TO, int TB, int WO, int WB>
 static cudaError_t mac_c3_t(const HbMacGroupC& g, const HbPrime* primes, const double* cc, int w,
                             int fold, int n, int R, int BC, cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(g.nterms + g.nout * g.nterms + g.nout);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 200 * 1024) {   // pointer tables too large for smem: split the outputs
+    if (g.nout <= 1) return cudaErrorInvalidValue;
+    HbMacGroupC a = g, b = g;
+    a.nout = g.nout / 2;
+    b.nout = g.nout - a.nout;
+    b.pts = g.pts + (size_t)a.nout * g.nterms;
+    b.dsts = g.dsts + a.nout;
+    cudaError_t e = mac_c3_t<TO, TB, WO, WB>(a, primes, cc, w, fold, n, R, BC, st);
+    return e != cudaSuccess ? e : mac_c3_t<TO, TB, WO, WB>(b, primes, cc, w, fold, n, R, BC, st);
+  }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm_c3<TO, TB, WO, WB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
-  dim3 grid(R * (n / 32), (g.nout + TO * WO - 1) / (TO * WO), (BC + TB * WB - 1) / (TB * WB));
+  dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
   k_mac_gemm_c3<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, cc, w, fold, n, R, BC);
   return cudaGetLastError();
 }
@@ -146,8 +155,8 @@ __global__ void __launch_bounds__(256)
 k_ks_inner_c3(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes,
               const double* __restrict__ cconst, int w, int fold, int n, int nb) {
   const HbKsTask2 tk = tasks[blockIdx.y];
-  const int b = blockIdx.z * blockDim.y + threadIdx.y;
-  const int j = 2 * (blockIdx.x * 32 + threadIdx.x);
+  const int b = blockIdx.x * blockDim.y + threadIdx.y;    // grid order as ops.cu k_ks_inner2
+  const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
   if (j >= n || b >= nb) return;
   const HbPrime P = primes[tk.prime];
   const double p = P.pd, pinv = P.pinv;
@@ -206,7 +215,7 @@ cudaError_t launch_ks_inner_c3(const void* tasks, int ntasks, int nb, const HbRi
   if (ntasks <= 0 || nb <= 0) return cudaSuccess;
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
-  dim3 grid((R.n / 2 + 31) / 32, ntasks, (nb + by - 1) / by);
+  dim3 grid((nb + by - 1) / by, ntasks, (R.n / 2 + 31) / 32);
   k_ks_inner_c3<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), R.primes,
                                         R.chunk_consts, R.chunk_w, R.chunk_fold, R.n, nb);
   return cudaGetLastError();

@@ -501,8 +501,10 @@ __global__ void __launch_bounds__(256)
 k_ks_inner2(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
             int nb) {
   const HbKsTask2 tk = tasks[blockIdx.y];
-  const int b = blockIdx.z * blockDim.y + threadIdx.y;
-  const int j = 2 * (blockIdx.x * 32 + threadIdx.x);
+  // grid: x = clip group (fastest), y = task, z = coefficient chunk (slowest):
+  // the clips of one key row run back to back, so the key is read from HBM once
+  const int b = blockIdx.x * blockDim.y + threadIdx.y;
+  const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
   if (j >= n || b >= nb) return;
   const HbPrime P = primes[tk.prime];
   int s0 = j, s1 = j + 1;
@@ -538,7 +540,7 @@ cudaError_t launch_ks_inner2(const void* tasks, int ntasks, int nb, const HbPrim
   if (ntasks <= 0 || nb <= 0) return cudaSuccess;
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
-  dim3 grid((n / 2 + 31) / 32, ntasks, (nb + by - 1) / by);
+  dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
   k_ks_inner2<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
   return cudaGetLastError();
 }
@@ -571,12 +573,15 @@ k_mac_gemm(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int B
   const u64* const* pts = ptrs + T;
   u64* const* dsts = const_cast<u64* const*>(ptrs + T + O * T);
 
+  // grid: x = clip-component tile (fastest), y = output tile, z = coefficient
+  // chunk (slowest) -> CTAs that share a plaintext/ciphertext chunk run
+  // back to back and hit it in L2 instead of re-reading HBM
   const int nchunk = n / 32;
-  const int r = blockIdx.x / nchunk;
-  const int j = (blockIdx.x % nchunk) * 32 + threadIdx.x;
+  const int r = blockIdx.z / nchunk;
+  const int j = (blockIdx.z % nchunk) * 32 + threadIdx.x;
   const int w = threadIdx.y;
   const int o0 = (blockIdx.y * WO + w / WB) * TO;
-  const int b0 = (blockIdx.z * WB + w % WB) * TB;
+  const int b0 = (blockIdx.x * WB + w % WB) * TB;
   if (o0 >= O || b0 >= BC) return;
   const HbPrime P = primes[r];
   const size_t rj = (size_t)r * n + j;
@@ -612,12 +617,21 @@ template <int TO, int TB, int WO, int WB>
 static cudaError_t mac_gemm_t(const HbMacGroup& g, const HbPrime* primes, int n, int R, int BC,
                               cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(g.nterms + g.nout * g.nterms + g.nout);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 200 * 1024) {   // pointer tables too large for smem: split the outputs
+    if (g.nout <= 1) return cudaErrorInvalidValue;
+    HbMacGroup a = g, b = g;
+    a.nout = g.nout / 2;
+    b.nout = g.nout - a.nout;
+    b.pts = g.pts + (size_t)a.nout * g.nterms;
+    b.dsts = g.dsts + a.nout;
+    cudaError_t e = mac_gemm_t<TO, TB, WO, WB>(a, primes, n, R, BC, st);
+    return e != cudaSuccess ? e : mac_gemm_t<TO, TB, WO, WB>(b, primes, n, R, BC, st);
+  }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm<TO, TB, WO, WB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
-  dim3 grid(R * (n / 32), (g.nout + TO * WO - 1) / (TO * WO), (BC + TB * WB - 1) / (TB * WB));
+  dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
   k_mac_gemm<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
   return cudaGetLastError();
 }
@@ -661,12 +675,15 @@ k_mac_gemm_f64(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, i
   const u64* const* cts = ptrs;
   const u64* const* pts = ptrs + T;
   u64* const* dsts = const_cast<u64* const*>(ptrs + T + O * T);
+  // grid: x = clip-component tile (fastest), y = output tile, z = coefficient
+  // chunk (slowest) -> CTAs that share a plaintext/ciphertext chunk run
+  // back to back and hit it in L2 instead of re-reading HBM
   const int nchunk = n / 32;
-  const int r = blockIdx.x / nchunk;
-  const int j = (blockIdx.x % nchunk) * 32 + threadIdx.x;
+  const int r = blockIdx.z / nchunk;
+  const int j = (blockIdx.z % nchunk) * 32 + threadIdx.x;
   const int w = threadIdx.y;
   const int o0 = (blockIdx.y * WO + w / WB) * TO;
-  const int b0 = (blockIdx.z * WB + w % WB) * TB;
+  const int b0 = (blockIdx.x * WB + w % WB) * TB;
   if (o0 >= O || b0 >= BC) return;
   const HbPrime P = primes[r];
   const double p = P.pd, pinv = P.pinv;
@@ -708,12 +725,21 @@ template <int TO, int TB, int WO, int WB>
 static cudaError_t mac_gemm_f64_t(const HbMacGroup& g, const HbPrime* primes, int n, int R, int BC,
                                   cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(g.nterms + g.nout * g.nterms + g.nout);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 200 * 1024) {   // pointer tables too large for smem: split the outputs
+    if (g.nout <= 1) return cudaErrorInvalidValue;
+    HbMacGroup a = g, b = g;
+    a.nout = g.nout / 2;
+    b.nout = g.nout - a.nout;
+    b.pts = g.pts + (size_t)a.nout * g.nterms;
+    b.dsts = g.dsts + a.nout;
+    cudaError_t e = mac_gemm_f64_t<TO, TB, WO, WB>(a, primes, n, R, BC, st);
+    return e != cudaSuccess ? e : mac_gemm_f64_t<TO, TB, WO, WB>(b, primes, n, R, BC, st);
+  }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm_f64<TO, TB, WO, WB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
-  dim3 grid(R * (n / 32), (g.nout + TO * WO - 1) / (TO * WO), (BC + TB * WB - 1) / (TB * WB));
+  dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
   k_mac_gemm_f64<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
   return cudaGetLastError();
 }
@@ -740,8 +766,10 @@ __global__ void __launch_bounds__(256)
 k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
                 int nb) {
   const HbKsTask2 tk = tasks[blockIdx.y];
-  const int b = blockIdx.z * blockDim.y + threadIdx.y;
-  const int j = 2 * (blockIdx.x * 32 + threadIdx.x);
+  // grid: x = clip group (fastest), y = task, z = coefficient chunk (slowest):
+  // the clips of one key row run back to back, so the key is read from HBM once
+  const int b = blockIdx.x * blockDim.y + threadIdx.y;
+  const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
   if (j >= n || b >= nb) return;
   const HbPrime P = primes[tk.prime];
   const double p = P.pd, pinv = P.pinv;
@@ -778,7 +806,7 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
   if (ntasks <= 0 || nb <= 0) return cudaSuccess;
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
-  dim3 grid((n / 2 + 31) / 32, ntasks, (nb + by - 1) / by);
+  dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
   k_ks_inner2_f64<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
   return cudaGetLastError();
 }

@@ -174,3 +174,25 @@ def test_chunked_dot_products_bit_exact(golden):
         assert digest(*be.export(be._raw_mult(A, B))) == g["ops"][str(lvl)]["mult"]
     m = be._raw_rot_many(A, [1, 5])
     assert digest(*be.export(m[5])) == g["ops"]["6"]["rot_many_5"]
+
+
+def test_prepermuted_rotation_keys_bit_exact(golden):
+    """Opt-in pre-permuted rotation keys give the reference's rotations."""
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    os.environ["HEAR_B200_PREPERM"] = "1"
+    try:
+        be = CkksBackend(gen_params("toy-fast"), seed=7)
+        g = golden["toy-fast"]
+        be.ensure_rotation_keys({int(a): l for a, l in g["rot_levels"].items()})
+    finally:
+        del os.environ["HEAR_B200_PREPERM"]
+    ps = be.params
+    for lvl in (6, 2):
+        A = be.import_ct(*rand_ct(ps, lvl, 100 + lvl), lvl, ps.msg_scale)
+        m = be._raw_rot_many(A, [1, 5])
+        assert digest(*be.export(m[5])) == g["ops"][str(lvl)]["rot_many_5"]
+        assert digest(*be.export(m[1])) == g["ops"][str(lvl)]["rot_many_1"]
+    A = be.import_ct(*rand_ct(ps, 2, 102), 2, ps.msg_scale)
+    assert digest(*be.export(be._raw_rot(A, 2047))) == g["ops"]["2"]["rot_2047"]
