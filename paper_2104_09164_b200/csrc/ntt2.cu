@@ -173,27 +173,6 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
   const Pol pol(P);
   const typename Pol::Tw* tw = FWD ? Pol::fwd_table(R, tk.dst_prime) : Pol::inv_table(R, tk.dst_prime);
   const int t = threadIdx.x;
-  // coalesced stage-in of the 4096-element tile (16-byte chunks)
-  {
-    const u64* srcp = (FWD ? (const u64*)tk.dst : tk.src) + base;
-#pragma unroll
-    for (int k = 0; k < TILE / 2 / THREADS2; ++k) {
-      const int ch = t + k * THREADS2;
-      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(srcp) + ch);
-      V a, b;
-      if (FWD) {
-        a = as_val<Pol>(v.x);
-        b = as_val<Pol>(v.y);
-      } else {
-        a = pol.from_canon(v.x);
-        b = pol.from_canon(v.y);
-      }
-      const int pc = swz_chunk(ch);
-      sm[2 * pc] = a;
-      sm[2 * pc + 1] = b;
-    }
-  }
-  __syncthreads();
   const int blk = t >> 3, cc = t & 7;   // stride-8 groups: 8 per block, 32 blocks
   const int gblk = tile * 32 + blk;     // global 128-block index
   // fp64 policy: the tile's 32*127 twiddles (7 stages) are staged once in
@@ -224,21 +203,22 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
     const double w = tws[4096 - (4096 >> r) + i - tile * len];
     return HbTwD{w, w * pinv};
   };
-  auto stride8 = [&](bool fwd) {
-    V x[16];
+  const u64 p = P.p;
+  if (FWD) {
+    // round 1 (stages S1..S1+3): stride-8 groups straight from the column
+    // pass's lazy intermediate in dst, result to smem
+    {
+      V x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = sm[swz(blk * 128 + u * 8 + cc)];
-    if constexpr (SMTW) {
-      if (fwd) fwd_group_f<Pol, 4>(x, S1, gblk, fetch_f, pol);
-      else inv_group_f<Pol, 4>(x, 3, gblk, fetch_i, pol);
-    } else {
-      if (fwd) fwd_group<Pol, 4>(x, S1, gblk, tw, pol);
-      else inv_group<Pol, 4>(x, 3, gblk, LOGN, tw, pol);
+      for (int u = 0; u < 16; ++u) x[u] = as_val<Pol>(__ldg(tk.dst + base + blk * 128 + u * 8 + cc));
+      if constexpr (SMTW) fwd_group_f<Pol, 4>(x, S1, gblk, fetch_f, pol);
+      else fwd_group<Pol, 4>(x, S1, gblk, tw, pol);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) sm[swz(blk * 128 + u * 8 + cc)] = x[u];
     }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) sm[swz(blk * 128 + u * 8 + cc)] = fwd ? x[u] : pol.inv_round_end(x[u]);
-  };
-  auto contig8 = [&](bool fwd, bool final_fwd) {
+    __syncthreads();
+    // round 2 (stages S1+4..S1+6): contiguous groups of 8 from smem, canonical,
+    // fused epilogue, 16-byte stores straight to dst
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int g2 = t + q * THREADS2;          // 512 groups of 8
@@ -252,69 +232,66 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
         x[2 * v + 1] = sm[2 * pc + 1];
       }
       const int G = (tile * 32 + b2) * 16 + G8;
-      if constexpr (SMTW) {
-        if (fwd) fwd_group_f<Pol, 3>(x, S1 + 4, G, fetch_f, pol);
-        else inv_group_f<Pol, 3>(x, 0, G, fetch_i, pol);
-      } else {
-        if (fwd) fwd_group<Pol, 3>(x, S1 + 4, G, tw, pol);
-        else inv_group<Pol, 3>(x, 0, G, LOGN, tw, pol);
+      if constexpr (SMTW) fwd_group_f<Pol, 3>(x, S1 + 4, G, fetch_f, pol);
+      else fwd_group<Pol, 3>(x, S1 + 4, G, tw, pol);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const size_t j = base + e0 + 2 * v;
+        ulonglong2 o;
+        o.x = pol.fwd_final(x[2 * v]);
+        o.y = pol.fwd_final(x[2 * v + 1]);
+        if (MODE == FWD_MODDOWN) {
+          const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
+          o.x = mul_shoup(sub_mod(ax.x, o.x, p), tk.scal, tk.scal_sh, p);
+          o.y = mul_shoup(sub_mod(ax.y, o.y, p), tk.scal, tk.scal_sh, p);
+          if (tk.add) {
+            int s0 = (int)j, s1 = (int)j + 1;
+            if (tk.perm) {
+              const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+              s0 = pp.x;
+              s1 = pp.y;
+            }
+            o.x = add_mod(o.x, __ldg(tk.add + s0), p);
+            o.y = add_mod(o.y, __ldg(tk.add + s1), p);
+          }
+        }
+        *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
       }
+    }
+  } else {
+    // round 1 (stages 0..2): contiguous groups of 8 straight from src
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int g2 = t + q * THREADS2;
+      const int b2 = g2 >> 4, G8 = g2 & 15;
+      const int e0 = b2 * 128 + G8 * 8;
+      V x[8];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const ulonglong2 in = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base + e0) + v);
+        x[2 * v] = pol.from_canon(in.x);
+        x[2 * v + 1] = pol.from_canon(in.y);
+      }
+      const int G = (tile * 32 + b2) * 16 + G8;
+      if constexpr (SMTW) inv_group_f<Pol, 3>(x, 0, G, fetch_i, pol);
+      else inv_group<Pol, 3>(x, 0, G, LOGN, tw, pol);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int pc = swz_chunk((e0 >> 1) + v);
-        if (final_fwd) {
-          u64* smu = reinterpret_cast<u64*>(sm);
-          smu[2 * pc] = pol.fwd_final(x[2 * v]);
-          smu[2 * pc + 1] = pol.fwd_final(x[2 * v + 1]);
-        } else {
-          sm[2 * pc] = fwd ? x[2 * v] : pol.inv_round_end(x[2 * v]);
-          sm[2 * pc + 1] = fwd ? x[2 * v + 1] : pol.inv_round_end(x[2 * v + 1]);
-        }
+        sm[2 * pc] = pol.inv_round_end(x[2 * v]);
+        sm[2 * pc + 1] = pol.inv_round_end(x[2 * v + 1]);
       }
     }
-  };
-  if (FWD) {
-    stride8(true);
     __syncthreads();
-    contig8(true, true);
-  } else {
-    contig8(false, false);
-    __syncthreads();
-    stride8(false);
-  }
-  __syncthreads();
-  // coalesced store (forward: canonical + fused epilogue; inverse: lazy)
-  const u64* smu = reinterpret_cast<const u64*>(sm);
-  const u64 p = P.p;
+    // round 2 (stages 3..6): stride-8 groups from smem, lazy result to dst
+    V x[16];
 #pragma unroll
-  for (int k = 0; k < TILE / 2 / THREADS2; ++k) {
-    const int ch = t + k * THREADS2;
-    const int pc = swz_chunk(ch);
-    ulonglong2 v;
-    if (FWD) {
-      v.x = smu[2 * pc];
-      v.y = smu[2 * pc + 1];
-      if (MODE == FWD_MODDOWN) {
-        const size_t j = base + 2 * ch;
-        const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
-        v.x = mul_shoup(sub_mod(ax.x, v.x, p), tk.scal, tk.scal_sh, p);
-        v.y = mul_shoup(sub_mod(ax.y, v.y, p), tk.scal, tk.scal_sh, p);
-        if (tk.add) {
-          int s0 = (int)j, s1 = (int)j + 1;
-          if (tk.perm) {
-            const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
-            s0 = pp.x;
-            s1 = pp.y;
-          }
-          v.x = add_mod(v.x, __ldg(tk.add + s0), p);
-          v.y = add_mod(v.y, __ldg(tk.add + s1), p);
-        }
-      }
-    } else {
-      v.x = as_bits<Pol>(sm[2 * pc]);
-      v.y = as_bits<Pol>(sm[2 * pc + 1]);
-    }
-    reinterpret_cast<ulonglong2*>(tk.dst + base)[ch] = v;
+    for (int u = 0; u < 16; ++u) x[u] = sm[swz(blk * 128 + u * 8 + cc)];
+    if constexpr (SMTW) inv_group_f<Pol, 4>(x, 3, gblk, fetch_i, pol);
+    else inv_group<Pol, 4>(x, 3, gblk, LOGN, tw, pol);
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      tk.dst[base + blk * 128 + u * 8 + cc] = as_bits<Pol>(pol.inv_round_end(x[u]));
   }
 }
 

@@ -756,9 +756,11 @@ cudaError_t launch_mac_gemm_f64(const void* cts, const void* pts, const void* ds
   g.nout = nout;
   if (BC <= 2) return mac_gemm_f64_t<4, 2, 8, 1>(g, primes, n, R, BC, st);
   if (BC <= 8) return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
+  // 4x4 tiles measured fastest on the conv shapes (tools/mac_sweep.sh): 4x8
+  // needs ~156 registers (one CTA per SM), too few warps to cover load latency
   const char* v = getenv("HEAR_B200_MAC_TILE");
-  if (v && v[0] == '4') return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
-  return mac_gemm_f64_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
+  if (v && v[0] == '8') return mac_gemm_f64_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
+  return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
 }
 
 // fp64 variant of the clip-blocked key-switch inner product.
