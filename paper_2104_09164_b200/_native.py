@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhear_b200.so")
+LIB_PATH = os.environ.get("HEAR_B200_LIB") or os.path.join(_HERE, "lib", "libhear_b200.so")
 
 _lib = None
 
