@@ -123,7 +123,7 @@ def cpu_oracle_run(args, n_clips: int, warm: int = 0):
     be = OracleCkks(gen_params(profile_of(args.mode)), seed=0)
     cp = compile_pipeline(shape, args.mode, args.strategy, be.params)
     be.ensure_rotation_keys(cp.rotations)
-    enc = ModelEncoder(cp, cpar, be)
+    enc = ModelEncoder(cp, cpar, be).prepare()   # model encoding is setup, not per clip
     cts = [encrypt_input(make_random_input(shape, 1000 + i), cp, be) for i in range(warm + n_clips)]
     for i in range(warm):
         run_pipeline(enc, cts[i], be)
