@@ -224,6 +224,30 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
       const int g2 = t + q * THREADS2;          // 512 groups of 8
       const int b2 = g2 >> 4, G8 = g2 & 15;
       const int e0 = b2 * 128 + G8 * 8;
+      // ModDown epilogue operands are issued before the butterflies so their
+      // HBM latency overlaps the fp64 work (profiled: these loads were the
+      // block pass's top stall)
+      ulonglong2 ax[4];
+      u64 ad[8];
+      if (MODE == FWD_MODDOWN) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          ax[v] = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + base + e0 + 2 * v));
+        if (tk.add) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const size_t j = base + e0 + 2 * v;
+            int s0 = (int)j, s1 = (int)j + 1;
+            if (tk.perm) {
+              const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+              s0 = pp.x;
+              s1 = pp.y;
+            }
+            ad[2 * v] = __ldg(tk.add + s0);
+            ad[2 * v + 1] = __ldg(tk.add + s1);
+          }
+        }
+      }
       V x[8];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -241,18 +265,11 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
         o.x = pol.fwd_final(x[2 * v]);
         o.y = pol.fwd_final(x[2 * v + 1]);
         if (MODE == FWD_MODDOWN) {
-          const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
-          o.x = mul_shoup(sub_mod(ax.x, o.x, p), tk.scal, tk.scal_sh, p);
-          o.y = mul_shoup(sub_mod(ax.y, o.y, p), tk.scal, tk.scal_sh, p);
+          o.x = mul_shoup(sub_mod(ax[v].x, o.x, p), tk.scal, tk.scal_sh, p);
+          o.y = mul_shoup(sub_mod(ax[v].y, o.y, p), tk.scal, tk.scal_sh, p);
           if (tk.add) {
-            int s0 = (int)j, s1 = (int)j + 1;
-            if (tk.perm) {
-              const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
-              s0 = pp.x;
-              s1 = pp.y;
-            }
-            o.x = add_mod(o.x, __ldg(tk.add + s0), p);
-            o.y = add_mod(o.y, __ldg(tk.add + s1), p);
+            o.x = add_mod(o.x, ad[2 * v], p);
+            o.y = add_mod(o.y, ad[2 * v + 1], p);
           }
         }
         *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
