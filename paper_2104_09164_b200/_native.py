@@ -106,7 +106,7 @@ TENSOR_TASK = np.dtype([("a0", "<u8"), ("a1", "<u8"), ("b0", "<u8"), ("b1", "<u8
 CRT_TASK = np.dtype([("rows", "<u8"), ("out", "<u8")])
 
 # NTT fused modes (csrc/ntt.cu FwdMode)
-FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64 = 0, 1, 2, 3
+FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER = 0, 1, 2, 3, 4
 # element-wise ops (csrc/ops.cu EwOp)
 EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PERM, \
     EW_SUB_SCALED, EW_PERM_ADD = range(10)

@@ -619,6 +619,25 @@ class CkksBackend(BackendBase):
         self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=iprows[:, lvl + 1], dst=rp(spc),
                                  dst_prime=sprime, src_prime=sprime))
         out = self.ring.empty(m, r)
+        if late and len(late) == nj and self.ring.two_pass:
+            # pre-permuted rotations: ModDown of the natural-order inner product
+            # (ModDown commutes with the automorphism), c0 added at the source
+            # index, result scattered through the inverse Galois map:
+            #   c0'[inv[j]] = ModDown(b')[j] + c0[j],  c1'[inv[j]] = ModDown(a')[j]
+            inv = np.zeros((nj, bsz, 2, r), dtype=np.uint64)
+            addn = np.zeros((nj, bsz, 2, r), dtype=np.uint64)
+            for j, perm, c0 in late:
+                inv[j] = self.ring.perm_inv_for(perm).data_ptr()
+                if c0 is not None:
+                    addn[j, :, 0] = c0
+            t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out),
+                       aux=iprows[:, :r].ravel(),
+                       src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
+                       scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
+                       add=addn.ravel(), perm=inv.ravel())
+            self.ring.ntt_fwd(t, nat.FWD_MODDOWN_SCATTER)
+            out = out.reshape(nj, bsz, 2, r, self.n)
+            return [out[j] for j in range(nj)]
         t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out),
                    aux=iprows[:, :r].ravel(),
                    src_prime=self.S, dst_prime=np.tile(np.arange(r), m),

@@ -133,6 +133,33 @@ class RingContext:
             self._perm_dev[g] = torch.from_numpy(self.ntt_perm(g)).to(self.device)
         return self._perm_dev[g]
 
+    def perm_inv_dev(self, g: int) -> torch.Tensor:
+        """Inverse of ntt_perm(g) (scatter index of a pre-permuted rotation)."""
+        key = -g
+        if key not in self._perm_dev:
+            perm = self.ntt_perm(g)
+            inv = np.empty_like(perm)
+            inv[perm] = np.arange(len(perm), dtype=perm.dtype)
+            self._perm_dev[key] = torch.from_numpy(inv).to(self.device)
+            self._perm_dev[("inv", self.perm_dev(g).data_ptr())] = self._perm_dev[key]
+        return self._perm_dev[key]
+
+    def perm_inv_for(self, perm: torch.Tensor) -> torch.Tensor:
+        """Inverse permutation of a tensor returned by perm_dev."""
+        hit = self._perm_dev.get(("inv", perm.data_ptr()))
+        if hit is None:
+            for g, t in list(self._perm_dev.items()):
+                if isinstance(g, int) and g > 0 and t.data_ptr() == perm.data_ptr():
+                    return self.perm_inv_dev(g)
+            raise KeyError("unknown permutation")
+        return hit
+
+    @property
+    def two_pass(self) -> bool:
+        """The default two-pass transform (csrc/ntt2.cu) is in use."""
+        return 12 <= self.logn <= 16 and not (os.environ.get("HEAR_B200_NTT1") == "1"
+                                              and self.logn <= 14)
+
     def coeff_automorphism(self, coeffs: np.ndarray, g: int) -> np.ndarray:
         """X -> X^g on signed integer coefficients."""
         k = np.arange(self.n, dtype=np.int64)

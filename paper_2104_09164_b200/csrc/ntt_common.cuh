@@ -11,6 +11,9 @@ enum FwdMode : int {
   FWD_LIFT = 1,      // src mod src_prime: centred lift then reduce (ModUp digit)
   FWD_MODDOWN = 2,   // FWD_LIFT, then dst = (aux - ntt) * scal (+ add[perm])
   FWD_I64 = 3,       // src holds signed int64 coefficients (encoder output)
+  FWD_MODDOWN_SCATTER = 4,  // FWD_MODDOWN whose result lands at dst[perm[j]] and
+                            // whose addend is read at j: a rotation computed on
+                            // pre-permuted keys (two-pass transform only)
 };
 
 // ---------------------------------------------------------------------------
