@@ -69,6 +69,9 @@ int hear_pw_sub(hb_ring* ring, unsigned long long* out, const unsigned long long
 int hb_ntt_fwd(hb_ring* ring, const void* tasks, int count, int mode, void* stream);
 /* Inverse NTT over row tasks (ring.py:120, true inverse twiddles).            */
 int hb_ntt_inv(hb_ring* ring, const void* tasks, int count, void* stream);
+/* Kernel launches one hb_ntt_fwd / hb_ntt_inv call of `count` rows enqueues
+ * (launch accounting; no reference counterpart).                             */
+int hb_ntt_kernels(hb_ring* ring, int count);
 /* Element-wise op `op` over HbEwTask rows: 0 add (ring.py:159), 1 sub
  * (ring.py:167), 2 mul (ring.py:127), 3 scalar mul (ring.py:175), 4 a*b+c
  * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,

@@ -42,6 +42,7 @@ def lib():
         L.hb_sizeof_task.argtypes = [i32]
         L.hb_ntt_fwd.argtypes = [vp, vp, i32, i32, vp]
         L.hb_ntt_inv.argtypes = [vp, vp, i32, vp]
+        L.hb_ntt_kernels.argtypes = [vp, i32]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_mac.argtypes = [vp, vp, i32, vp, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]

@@ -175,12 +175,8 @@ class RingContext:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def _ntt_kernels(self, count: int) -> int:
-        """Kernels one NTT call enqueues (csrc/ntt.cu use_two_pass, ntt2.cu chunks)."""
-        if 12 <= self.logn <= 16 and not (os.environ.get("HEAR_B200_NTT1") == "1"
-                                          and self.logn <= 14):
-            chunk = int(os.environ.get("HEAR_B200_NTT_CHUNK", "512")) or (1 << 30)
-            return 2 * -(-count // chunk)
-        return 1
+        """Kernels one NTT call enqueues (csrc/ntt.cu ntt_kernels)."""
+        return int(self._lib.hb_ntt_kernels(self.handle, count))
 
     def ntt_fwd(self, tasks: np.ndarray, mode: int = nat.FWD_PLAIN):
         if len(tasks):

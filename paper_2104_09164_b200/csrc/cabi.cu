@@ -21,6 +21,7 @@
 namespace hb {
 cudaError_t launch_ntt_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
 cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
+int ntt_kernels(const HbRing&, int);
 cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
@@ -57,6 +58,8 @@ struct hb_ring {
   HbTwD* twd_inv_dev;
   double* tw1_fwd_dev;
   double* tw1_inv_dev;
+  HbTwD* tw3_fwd_dev = nullptr;
+  HbTwD* tw3_inv_dev = nullptr;
   double* chunk_dev = nullptr;
   std::vector<double> chunk_host;
   std::vector<HbPrime> primes_host;
@@ -176,8 +179,31 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
       t1i[k] = (double)ipsi[k];
     }
   }
+  // plane-major fine-stage tables (ring.cuh tw3_fwd / tw3_inv)
+  std::vector<HbTwD> t3f((size_t)nprimes * n), t3i((size_t)nprimes * n);
+  if (logn >= 6) {
+    const int n8 = n / 8;
+    const int off_inv[3] = {0, 4, 6};
+    for (int i = 0; i < nprimes; ++i) {
+      const size_t b = (size_t)i * n;
+      for (int e = 0; e < 3; ++e)
+        for (int ii = 0; ii < (1 << e); ++ii)
+          for (int G = 0; G < n8; ++G)
+            t3f[b + (size_t)((1 << e) - 1 + ii) * n8 + G] =
+                tfd[b + ((size_t)1 << (logn - 3 + e)) + ((size_t)G << e) + ii];
+      for (int rr = 0; rr < 3; ++rr)
+        for (int ii = 0; ii < (1 << (2 - rr)); ++ii)
+          for (int G = 0; G < n8; ++G)
+            t3i[b + (size_t)(off_inv[rr] + ii) * n8 + G] =
+                tid[b + (n >> (rr + 1)) + ((size_t)G << (2 - rr)) + ii];
+    }
+  }
   cudaError_t e;
-  if ((e = cudaMalloc(&r->primes_dev, sizeof(HbPrime) * nprimes)) ||
+  if ((e = cudaMalloc(&r->tw3_fwd_dev, sizeof(HbTwD) * t3f.size())) ||
+      (e = cudaMalloc(&r->tw3_inv_dev, sizeof(HbTwD) * t3i.size())) ||
+      (e = cudaMemcpy(r->tw3_fwd_dev, t3f.data(), sizeof(HbTwD) * t3f.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(r->tw3_inv_dev, t3i.data(), sizeof(HbTwD) * t3i.size(), cudaMemcpyHostToDevice)) ||
+      (e = cudaMalloc(&r->primes_dev, sizeof(HbPrime) * nprimes)) ||
       (e = cudaMalloc(&r->tw_fwd_dev, sizeof(HbTw) * tf.size())) ||
       (e = cudaMalloc(&r->tw_inv_dev, sizeof(HbTw) * ti.size())) ||
       (e = cudaMemcpy(r->primes_dev, r->primes_host.data(), sizeof(HbPrime) * nprimes,
@@ -203,6 +229,8 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.twd_inv = r->twd_inv_dev;
   r->dev.tw1_fwd = r->tw1_fwd_dev;
   r->dev.tw1_inv = r->tw1_inv_dev;
+  r->dev.tw3_fwd = r->tw3_fwd_dev;
+  r->dev.tw3_inv = r->tw3_inv_dev;
   if (cudaMalloc(&r->chunk_dev, sizeof(double) * r->chunk_host.size()) ||
       cudaMemcpy(r->chunk_dev, r->chunk_host.data(), sizeof(double) * r->chunk_host.size(),
                  cudaMemcpyHostToDevice)) {
@@ -222,6 +250,8 @@ void hb_ring_destroy(hb_ring* r) {
   cudaFree(r->twd_inv_dev);
   cudaFree(r->tw1_fwd_dev);
   cudaFree(r->tw1_inv_dev);
+  cudaFree(r->tw3_fwd_dev);
+  cudaFree(r->tw3_inv_dev);
   cudaFree(r->chunk_dev);
   delete r;
 }
@@ -254,6 +284,8 @@ int hb_ntt_inv(hb_ring* r, const void* tasks, int count, void* stream) {
   cudaError_t e = launch_ntt_inv((const HbNttTask*)tasks, count, r->dev, (cudaStream_t)stream);
   return e ? fail(e, "hb_ntt_inv") : 0;
 }
+
+int hb_ntt_kernels(hb_ring* r, int count) { return ntt_kernels(r->dev, count); }
 
 int hb_ew(hb_ring* r, int op, const void* tasks, int count, void* stream) {
   cudaError_t e = launch_ew(op, (const HbEwTask*)tasks, count, r->dev.primes, r->dev.n,

@@ -270,6 +270,9 @@ static cudaError_t launch_inv_t(const HbNttTask* tasks, int count, const HbRing&
 }
 
 bool ntt2_supported(int logn);
+bool ntt3_supported(const HbRing& R);
+cudaError_t launch_ntt3_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
+cudaError_t launch_ntt3_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ntt2_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
 cudaError_t launch_ntt2_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 
@@ -284,9 +287,19 @@ static bool use_two_pass(int logn) {
   return ntt2_supported(logn) && !(force1 && logn <= 14);
 }
 
+int ntt2_chunk();
+
+int ntt_kernels(const HbRing& R, int count) {
+  if (count <= 0) return 0;
+  if (ntt3_supported(R)) return 1;
+  if (use_two_pass(R.logn)) return 2 * ((count + ntt2_chunk() - 1) / ntt2_chunk());
+  return 1;
+}
+
 cudaError_t launch_ntt_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,
                            cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
+  if (ntt3_supported(R)) return launch_ntt3_fwd(tasks, count, R, mode, st);
   if (use_two_pass(R.logn)) return launch_ntt2_fwd(tasks, count, R, mode, st);
   switch (R.logn) {
     case 10: return launch_fwd_t<10>(tasks, count, R, mode, st);
@@ -300,6 +313,7 @@ cudaError_t launch_ntt_fwd(const HbNttTask* tasks, int count, const HbRing& R, i
 
 cudaError_t launch_ntt_inv(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
+  if (ntt3_supported(R)) return launch_ntt3_inv(tasks, count, R, st);
   if (use_two_pass(R.logn)) return launch_ntt2_inv(tasks, count, R, st);
   switch (R.logn) {
     case 10: return launch_inv_t<10>(tasks, count, R, st);

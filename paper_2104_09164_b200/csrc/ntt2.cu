@@ -385,6 +385,8 @@ static cudaError_t fwd2_mode(const HbNttTask* tasks, int count, const HbRing& R,
   }
 }
 
+int ntt2_chunk() { return ntt_chunk(); }
+
 bool ntt2_supported(int logn) { return logn >= 12 && logn <= 16; }
 
 cudaError_t launch_ntt2_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,

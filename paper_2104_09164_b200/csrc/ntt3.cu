@@ -1,0 +1,479 @@
+// Cluster-fused negacyclic NTT (default for fp64 rings at N = 2^13, 2^14).
+//
+// Same transform and fused modes as ntt2.cu (hear/ckks/ring.py:71-124, true
+// inverse), same split of the stages into a column pass (stages 0..S1-1 over
+// the M = N/128 elements of each of the 128 columns) and a block pass (the
+// last 7 stages inside each 128-element block) -- but the two passes run in
+// ONE launch: a thread-block cluster of CL = N/4096 CTAs owns one row.
+//
+//   forward  CTA k runs the column pass on columns [k*CW, (k+1)*CW) in its
+//            local 32 KB buffer, then pushes every (block, column-pair) chunk
+//            to the CTA that owns the block's tile (tile t = blocks
+//            32t..32t+31) with st.async into that CTA's receive buffer
+//            (DSMEM); each CTA waits on its own mbarrier for the 32 KB it
+//            receives, runs the block pass and stores with the fused
+//            epilogue (ModUp lift / ModDown / scatter as ntt2.cu).
+//   inverse  the mirror image: block pass on tile t, push to the column
+//            owners, column pass, N^-1 fused in the store.
+//
+// The exchange is producer/consumer through mbarrier transaction counts:
+// no cluster-wide barrier with release/acquire fences in the data path (the
+// cooperative-groups cluster.sync version profiled 16 % of its stall samples
+// on MEMBAR.ALL.GPU / ERRBAR / the barrier wait, and its CCTL.IVALL dropped
+// the twiddles from L1).  The only cluster barrier makes the mbarrier
+// initialisation visible and is split around the first pass.  The lazy
+// intermediate never touches L2/HBM (the two-pass kernels write and re-read
+// it: 256 KB per row).  Shared memory per CTA: 64 KB + 8 B.
+#include <cstdint>
+#include <cstdlib>
+#include <type_traits>
+#include "ntt_common.cuh"
+
+namespace hb {
+
+namespace {
+
+constexpr int TILE3 = 4096;
+constexpr int THREADS3 = 256;
+constexpr int SMEM3 = 2 * TILE3 * 8 + 16;   // local buffer, receive buffer, mbarrier
+#ifndef HB_NTT3_MINB
+#define HB_NTT3_MINB 3
+#endif
+
+HB_DEV int swz3_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
+// block layout (as ntt2.cu): element j of the 4096-element tile
+HB_DEV int bsw(int j) { return (swz3_chunk(j >> 1) << 1) | (j & 1); }
+// column layout: element (m, c) of the CW-column slice; the XOR spreads the
+// four blocks a pulling warp touches over distinct banks
+template <int CW>
+HB_DEV int csw(int m, int c) { return m * CW + (c ^ (((m & 3) << 3) & (CW - 1))); }
+
+// ---- cluster / DSMEM primitives (PTX)
+HB_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+HB_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+HB_DEV uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// thread 0: one arrival expecting `bytes` of st.async traffic, made visible
+// to the cluster; every thread then arrives (relaxed) on the cluster barrier
+HB_DEV void xchg_init(uint64_t* mbar, uint32_t bytes) {
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_addr(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+HB_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// 16-byte push into a peer's shared memory, counted on the peer's mbarrier
+HB_DEV void st_async16(uint32_t raddr, uint32_t rmbar, double a, double b) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(
+          raddr),
+      "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar)
+      : "memory");
+}
+HB_DEV void mbar_wait0(uint64_t* mbar) {
+  const uint32_t a = smem_addr(mbar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(a)
+      : "memory");
+}
+
+template <class Pol, int MODE>
+HB_DEV typename Pol::T ld_src(const HbNttTask& tk, const Pol& pol, u64 ps, u64 ps_half, size_t j) {
+  const u64 x = __ldg(tk.src + j);
+  if (MODE == FWD_PLAIN) return pol.from_canon(x);
+  if (MODE == FWD_I64) return pol.from_signed((i64)x);
+  return pol.from_lift(x, ps, ps_half);
+}
+
+// Column-pass round plan: group/element mapping shared by both directions.
+//   round rd covers local stages [4rd, 4rd+K); a thread owns gpt groups of
+//   2^K elements of column c; element u of group gid sits at row m.
+template <int S1, bool FWD>
+struct ColPlan {
+  static constexpr int M = 1 << S1, GQ = M / 16, NR = (S1 + 3) / 4;
+  static HB_DEV int K(int rd) { return rd == NR - 1 ? S1 - rd * 4 : 4; }
+  static HB_DEV int tl(int rd) { return FWD ? (M >> (rd * 4 + K(rd))) : (1 << (rd * 4)); }
+  static HB_DEV int m_of(int rd, int gq, int q) {
+    const int k = K(rd), t = tl(rd);
+    const int gsel = q >> k, u = q & ((1 << k) - 1);
+    const int gid = gq + gsel * GQ;
+    return (gid / t) * (t << k) + (gid % t) + u * t;
+  }
+  static HB_DEV bool owns(int rd, int q) { return (q >> K(rd)) < (16 >> K(rd)); }
+};
+
+template <class Pol, int S1, bool FWD>
+HB_DEV void col_butterflies(typename Pol::T* x, int rd, int gq, int logn,
+                            const typename Pol::Tw* tw, const Pol& pol) {
+  typedef ColPlan<S1, FWD> CP;
+  const int K = CP::K(rd), tl = CP::tl(rd), gpt = 16 >> K, s0 = rd * 4;
+#pragma unroll
+  for (int gsel = 0; gsel < 16; ++gsel) {
+    if (gsel >= gpt) break;
+    const int gid = gq + gsel * CP::GQ;
+    if (FWD) {
+      if (K == 4) fwd_group<Pol, 4>(x + gsel * 16, s0, gid / tl, tw, pol);
+      else if (K == 3) fwd_group<Pol, 3>(x + gsel * 8, s0, gid / tl, tw, pol);
+      else if (K == 2) fwd_group<Pol, 2>(x + gsel * 4, s0, gid / tl, tw, pol);
+      else fwd_group<Pol, 1>(x + gsel * 2, s0, gid / tl, tw, pol);
+    } else {
+      if (K == 4) inv_group<Pol, 4>(x + gsel * 16, s0 + 7, gid / tl, logn, tw, pol);
+      else if (K == 3) inv_group<Pol, 3>(x + gsel * 8, s0 + 7, gid / tl, logn, tw, pol);
+      else if (K == 2) inv_group<Pol, 2>(x + gsel * 4, s0 + 7, gid / tl, logn, tw, pol);
+      else inv_group<Pol, 1>(x + gsel * 2, s0 + 7, gid / tl, logn, tw, pol);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward.
+template <class Pol, int LOGN, int MODE>
+__global__ void __launch_bounds__(THREADS3, HB_NTT3_MINB)
+k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
+  constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1, CW = TILE3 / M, CL = N / TILE3;
+  typedef ColPlan<S1, true> CP;
+  typedef typename Pol::T V;
+  extern __shared__ __align__(16) unsigned char smraw3[];
+  V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
+  V* rb = sm + TILE3;                     // received block tile
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(rb + TILE3);
+  xchg_init(&mbar, TILE3 * sizeof(V));
+  const int rank = (int)cluster_rank();
+  const HbNttTask tk = tasks[blockIdx.x / CL];
+  const HbPrime P = R.primes[tk.dst_prime];
+  const Pol pol(P);
+  const typename Pol::Tw* tw = Pol::fwd_table(R, tk.dst_prime);
+  const int t = threadIdx.x;
+  u64 ps = 0, ps_half = 0;
+  if (MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER) {
+    ps = R.primes[tk.src_prime].p;
+    ps_half = ps >> 1;
+  }
+  // ---- column pass over columns [rank*CW, rank*CW + CW)
+  const int cg0 = rank * CW;
+  {
+    const int c = t % CW, gq = t / CW;
+    V x[16];
+#pragma unroll
+    for (int rd = 0; rd < CP::NR; ++rd) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (!CP::owns(rd, q)) break;
+        const int m = CP::m_of(rd, gq, q);
+        x[q] = rd == 0 ? ld_src<Pol, MODE>(tk, pol, ps, ps_half, (size_t)m * 128 + cg0 + c)
+                       : sm[csw<CW>(m, c)];
+      }
+      col_butterflies<Pol, S1, true>(x, rd, gq, LOGN, tw, pol);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (!CP::owns(rd, q)) break;
+        sm[csw<CW>(CP::m_of(rd, gq, q), c)] = x[q];
+      }
+      __syncthreads();
+    }
+  }
+  // ---- push (block m, columns 2k, 2k+1) to the owner of block m's tile
+  cluster_wait();   // peers' mbarriers are initialised
+  {
+    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(&mbar);
+#pragma unroll
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+      const int k = t + i * THREADS3;
+      const int m = k / (CW / 2), c = 2 * (k % (CW / 2));
+      const double2 v = *reinterpret_cast<const double2*>(sm + csw<CW>(m, c));
+      const uint32_t dst = m >> 5;
+      st_async16(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), v.x, v.y);
+    }
+  }
+  mbar_wait0(&mbar);
+  // ---- block pass over blocks [rank*32, rank*32 + 32)
+  {
+    const int blk = t >> 3, cc = t & 7;
+    V x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = rb[bsw(blk * 128 + u * 8 + cc)];
+    fwd_group<Pol, 4>(x, S1, rank * 32 + blk, tw, pol);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) rb[bsw(blk * 128 + u * 8 + cc)] = x[u];
+  }
+  __syncthreads();
+  const size_t base = (size_t)rank * TILE3;
+  constexpr int N8 = N / 8;
+  const HbTwD* t3 = R.tw3_fwd + (size_t)tk.dst_prime * N;
+  // stage S1+4+e, entry (G << e) + i: plane-major table, lanes contiguous
+  auto fetch_fine = [&](int s, int idx) {
+    const int e = s - (S1 + 4), ii = idx & ((1 << e) - 1);
+    const double2 w = __ldg(reinterpret_cast<const double2*>(t3 + (((1 << e) - 1 + ii) * N8 + (idx >> e))));
+    return HbTwD{w.x, w.y};
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int g2 = t + q * THREADS3;          // 512 groups of 8
+    const int b2 = g2 >> 4, G8 = g2 & 15;
+    const int e0 = b2 * 128 + G8 * 8;
+    V x[8];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int pc = swz3_chunk((e0 >> 1) + v);
+      x[2 * v] = rb[2 * pc];
+      x[2 * v + 1] = rb[2 * pc + 1];
+    }
+    fwd_group_f<Pol, 3>(x, S1 + 4, (rank * 32 + b2) * 16 + G8, fetch_fine, pol);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {   // canonical residues back in place
+      const int pc = swz3_chunk((e0 >> 1) + v);
+      rb[2 * pc] = __longlong_as_double((long long)pol.fwd_final(x[2 * v]));
+      rb[2 * pc + 1] = __longlong_as_double((long long)pol.fwd_final(x[2 * v + 1]));
+    }
+  }
+  __syncthreads();
+  // ---- epilogue on 16-byte chunks, lanes contiguous (coalesced HBM traffic)
+  const u64 p = P.p;
+  constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
+#pragma unroll 4
+  for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+    const int k = t + i * THREADS3;
+    const size_t j = base + 2 * k;
+    const int pc = swz3_chunk(k);
+    ulonglong2 o;
+    o.x = (u64)__double_as_longlong(rb[2 * pc]);
+    o.y = (u64)__double_as_longlong(rb[2 * pc + 1]);
+    if (MD) {
+      const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
+      o.x = mul_shoup(sub_mod(ax.x, o.x, p), tk.scal, tk.scal_sh, p);
+      o.y = mul_shoup(sub_mod(ax.y, o.y, p), tk.scal, tk.scal_sh, p);
+      if (tk.add) {
+        u64 a0, a1;
+        if (MODE == FWD_MODDOWN && tk.perm) {
+          const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+          a0 = __ldg(tk.add + pp.x);
+          a1 = __ldg(tk.add + pp.y);
+        } else {
+          const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
+          a0 = a2.x;
+          a1 = a2.y;
+        }
+        o.x = add_mod(o.x, a0, p);
+        o.y = add_mod(o.y, a1, p);
+      }
+    }
+    if (MODE == FWD_MODDOWN_SCATTER) {
+      const int2 sc = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+      tk.dst[sc.x] = o.x;
+      tk.dst[sc.y] = o.y;
+    } else {
+      *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Inverse.
+template <class Pol, int LOGN>
+__global__ void __launch_bounds__(THREADS3, HB_NTT3_MINB)
+k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
+  constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1, CW = TILE3 / M, CL = N / TILE3;
+  typedef ColPlan<S1, false> CP;
+  typedef typename Pol::T V;
+  extern __shared__ __align__(16) unsigned char smraw3[];
+  V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
+  V* rb = sm + TILE3;                     // received column slice
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(rb + TILE3);
+  xchg_init(&mbar, TILE3 * sizeof(V));
+  const int rank = (int)cluster_rank();
+  const HbNttTask tk = tasks[blockIdx.x / CL];
+  const HbPrime P = R.primes[tk.dst_prime];
+  const Pol pol(P);
+  const typename Pol::Tw* tw = Pol::inv_table(R, tk.dst_prime);
+  const int t = threadIdx.x;
+  const size_t base = (size_t)rank * TILE3;
+  // ---- block pass on tile `rank`: coalesced 16-byte loads into the
+  // swizzled tile, stages 0..2 (contiguous 8), 3..6 (stride 8)
+#pragma unroll
+  for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+    const int k = t + i * THREADS3;
+    const ulonglong2 in = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base) + k);
+    const int pc = swz3_chunk(k);
+    sm[2 * pc] = pol.from_canon(in.x);
+    sm[2 * pc + 1] = pol.from_canon(in.y);
+  }
+  __syncthreads();
+  constexpr int N8 = N / 8;
+  const HbTwD* t3 = R.tw3_inv + (size_t)tk.dst_prime * N;
+  // stage r, entry (G << (2-r)) + i: plane-major table, lanes contiguous
+  auto fetch_fine = [&](int r, int idx) {
+    const int sh = 2 - r, ii = idx & ((1 << sh) - 1);
+    const int off = r == 0 ? 0 : (r == 1 ? 4 : 6);
+    const double2 w = __ldg(reinterpret_cast<const double2*>(t3 + ((off + ii) * N8 + (idx >> sh))));
+    return HbTwD{w.x, w.y};
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int g2 = t + q * THREADS3;
+    const int b2 = g2 >> 4, G8 = g2 & 15;
+    const int e0 = b2 * 128 + G8 * 8;
+    V x[8];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int pc = swz3_chunk((e0 >> 1) + v);
+      x[2 * v] = sm[2 * pc];
+      x[2 * v + 1] = sm[2 * pc + 1];
+    }
+    inv_group_f<Pol, 3>(x, 0, (rank * 32 + b2) * 16 + G8, fetch_fine, pol);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int pc = swz3_chunk((e0 >> 1) + v);
+      sm[2 * pc] = pol.inv_round_end(x[2 * v]);
+      sm[2 * pc + 1] = pol.inv_round_end(x[2 * v + 1]);
+    }
+  }
+  __syncthreads();
+  {
+    const int blk = t >> 3, cc = t & 7;
+    V x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = sm[bsw(blk * 128 + u * 8 + cc)];
+    inv_group<Pol, 4>(x, 3, rank * 32 + blk, LOGN, tw, pol);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) sm[bsw(blk * 128 + u * 8 + cc)] = pol.inv_round_end(x[u]);
+  }
+  __syncthreads();
+  // ---- push (block m, columns 2k, 2k+1) to the owner of those columns
+  cluster_wait();
+  {
+    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(&mbar);
+#pragma unroll
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+      const int k = t + i * THREADS3;
+      const int ml = k >> 6, col = 2 * (k & 63);
+      const double2 v = *reinterpret_cast<const double2*>(sm + bsw(ml * 128 + col));
+      const uint32_t dst = col / CW;
+      st_async16(mapa(rb0 + 8u * csw<CW>(rank * 32 + ml, col % CW), dst), mapa(mb0, dst), v.x,
+                 v.y);
+    }
+  }
+  mbar_wait0(&mbar);
+  // ---- column pass over columns [rank*CW, rank*CW + CW)
+  const int c = t % CW, gq = t / CW, cg0 = rank * CW;
+  V x[16];
+#pragma unroll
+  for (int rd = 0; rd < CP::NR; ++rd) {
+    V* buf = rd == 0 ? rb : sm;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (!CP::owns(rd, q)) break;
+      x[q] = buf[csw<CW>(CP::m_of(rd, gq, q), c)];
+    }
+    col_butterflies<Pol, S1, false>(x, rd, gq, LOGN, tw, pol);
+    const bool last = rd == CP::NR - 1;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (!CP::owns(rd, q)) break;
+      const int m = CP::m_of(rd, gq, q);
+      if (last) tk.dst[(size_t)m * 128 + cg0 + c] = pol.inv_final(x[q]);
+      else sm[csw<CW>(m, c)] = pol.inv_round_end(x[q]);
+    }
+    if (!last) __syncthreads();
+  }
+}
+
+template <int LOGN, int MODE>
+cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  constexpr int CL = (1 << LOGN) / TILE3;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * CL);
+  cfg.blockDim = dim3(THREADS3);
+  cfg.dynamicSmemBytes = SMEM3;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaFuncSetAttribute(k_ntt3_fwd<PolF64, LOGN, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k_ntt3_fwd<PolF64, LOGN, MODE>, tasks, R);
+}
+
+template <int LOGN>
+cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  constexpr int CL = (1 << LOGN) / TILE3;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * CL);
+  cfg.blockDim = dim3(THREADS3);
+  cfg.dynamicSmemBytes = SMEM3;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaFuncSetAttribute(k_ntt3_inv<PolF64, LOGN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k_ntt3_inv<PolF64, LOGN>, tasks, R);
+}
+
+template <int LOGN>
+cudaError_t fwd3_mode(const HbNttTask* tasks, int count, const HbRing& R, int mode,
+                      cudaStream_t st) {
+  switch (mode) {
+    case FWD_PLAIN: return fwd3_t<LOGN, FWD_PLAIN>(tasks, count, R, st);
+    case FWD_LIFT: return fwd3_t<LOGN, FWD_LIFT>(tasks, count, R, st);
+    case FWD_MODDOWN: return fwd3_t<LOGN, FWD_MODDOWN>(tasks, count, R, st);
+    case FWD_I64: return fwd3_t<LOGN, FWD_I64>(tasks, count, R, st);
+    case FWD_MODDOWN_SCATTER: return fwd3_t<LOGN, FWD_MODDOWN_SCATTER>(tasks, count, R, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+// fp64 rings at N = 2^13 / 2^14 (clusters of 2 / 4 CTAs); HEAR_B200_NTT3=0
+// falls back to the two-pass kernels.
+bool ntt3_supported(const HbRing& R) {
+  static int off = -1;
+  if (off < 0) {
+    const char* v = getenv("HEAR_B200_NTT3");
+    off = (v && v[0] == '0') ? 1 : 0;
+  }
+  return !off && R.use_f64 && (R.logn == 13 || R.logn == 14);
+}
+
+cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,
+                            cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  switch (R.logn) {
+    case 13: return fwd3_mode<13>(tasks, count, R, mode, st);
+    case 14: return fwd3_mode<14>(tasks, count, R, mode, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_ntt3_inv(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  switch (R.logn) {
+    case 13: return inv3_t<13>(tasks, count, R, st);
+    case 14: return inv3_t<14>(tasks, count, R, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hb

@@ -26,6 +26,13 @@ struct HbRing {
   const HbTwD* twd_inv;
   const double* tw1_fwd;  // fp64 powers only (8 B entries, staged in smem by ntt2.cu)
   const double* tw1_inv;
+  // fine-stage twiddles of the cluster NTT (ntt3.cu), plane-major so that a
+  // warp's lanes (consecutive groups G) read consecutive entries:
+  //   fwd stage logn-3+e, entry (G << e) + i  at  ((2^e - 1) + i) * n/8 + G
+  //   inv stage r,        entry (G << (2-r)) + i  at  (off[r] + i) * n/8 + G,
+  //   off = {0, 4, 6}
+  const HbTwD* tw3_fwd;   // [nprimes][n] (7n/8 used)
+  const HbTwD* tw3_inv;
   // chunked exact dot products (ops.cu k_mac_gemm_c3): ciphertext residues
   // split into three chunk_w-bit limbs; products summed exactly in fp64 for
   // chunk_fold terms between reductions (0 = disabled for this ring)

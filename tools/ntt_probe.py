@@ -1,8 +1,12 @@
-"""Run the key-switch ModUp NTT launch a few times (ncu target)."""
-import sys, os
+"""Time the key-switch ModDown NTT launch (bench.dominant_kernel_roofline)
+at the bench's shape; ncu target.   python tools/ntt_probe.py [lvl] [bsz]"""
+import os
+import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_09164_b200.ckks.engine import CkksBackend
 from paper_2104_09164_b200.ckks.params import gen_params
 import bench
-be = CkksBackend(gen_params("fast-hear"), seed=0)
-print(bench.dominant_kernel_roofline(be, lvl=6, bsz=16, peaks={}))
+lvl = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+bsz = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+be = CkksBackend(gen_params("fast-hear"), seed=0, keygen=False)
+print(bench.dominant_kernel_roofline(be, lvl=lvl, bsz=bsz, peaks={}))
