@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libhear_b200.so")
-SOURCES = ["ntt.cu", "ntt2.cu", "ntt3.cu", "ops.cu", "dot.cu", "fft.cu", "cabi.cu"]
+SOURCES = ["ntt.cu", "ntt2.cu", "ntt3.cu", "ops.cu", "mac.cu", "dot.cu", "fft.cu", "cabi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + \
@@ -34,16 +34,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs, log = [], []
-    for src in SOURCES:
+    objs, log, procs = [], [], []
+    for src in SOURCES:   # one nvcc per source, in parallel
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(f"== {src}\n{r.stdout}{r.stderr}")
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                            text=True)))
         objs.append(obj)
+    for src, pr in procs:
+        out, _ = pr.communicate()
+        log.append(f"== {src}\n{out}")
+        if pr.returncode != 0:
+            sys.stderr.write(out)
+            raise RuntimeError(f"nvcc failed on {src}")
     tmp = LIB + ".tmp"
     r = subprocess.run([NVCC, "-shared", *ARCH, *objs, "-o", tmp, "-lcudart"],
                        capture_output=True, text=True)

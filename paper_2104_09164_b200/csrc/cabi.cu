@@ -35,6 +35,8 @@ cudaError_t launch_mac_gemm(const void*, const void*, const void*, int, int, con
 cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int, const HbPrime*,
                                 int, int, int, cudaStream_t);
 cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_mac_pipe(const void*, const void*, const void*, int, int, const HbRing&, int,
+                            int, cudaStream_t);
 cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, const HbRing&, int,
                                int, cudaStream_t);
 cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
@@ -320,7 +322,14 @@ int hb_ks_inner(hb_ring* r, const void* tasks, int count, void* stream) {
 int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts, int nterms,
                   int nout, int rows, int bc, void* stream) {
   const char* old = getenv("HEAR_B200_MAC_SHARED");
-  cudaError_t e = (old && old[0] == '1')
+  const char* pipe = getenv("HEAR_B200_MAC_PIPE");   // "0": register-prefetch kernels
+  cudaError_t e = cudaErrorNotSupported;
+  if (r->dev.use_f64 && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
+    e = launch_mac_pipe(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) (void)cudaGetLastError();   // term table too large
+  }
+  if (e == cudaErrorNotSupported)
+    e = (old && old[0] == '1')
       ? launch_mac_shared(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
                           (cudaStream_t)stream)
       : r->dev.chunk_fold

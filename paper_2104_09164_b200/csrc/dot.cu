@@ -68,18 +68,32 @@ k_mac_gemm_c3(HbMacGroupC g, const HbPrime* __restrict__ primes, const double* _
 #pragma unroll
     for (int b = 0; b < TB; ++b) acc[o][b][0] = acc[o][b][1] = acc[o][b][2] = 0.0;
   int since = 0;
+  // software pipeline as ops.cu k_mac_gemm_f64: term t+1 in flight
+  u64 cn[TB], an[TO];
+  auto fetch = [&](int t) {
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+      cn[b] = (b0 + b < BC) ? __ldg(cts[t] + (size_t)(b0 + b) * R * n + rj) : 0ull;
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+      an[o] = (o0 + o < O) ? __ldg(pts[(size_t)(o0 + o) * T + t] + rj) : 0ull;
+  };
+  fetch(0);
   for (int t = 0; t < T; ++t) {
-    double c[TB][3];
+    double c[TB][3], av[TO];
 #pragma unroll
     for (int b = 0; b < TB; ++b) {
-      const u64 v = (b0 + b < BC) ? __ldg(cts[t] + (size_t)(b0 + b) * R * n + rj) : 0ull;
+      const u64 v = cn[b];
       c[b][0] = limb(v, 0, mask);
       c[b][1] = limb(v, w, mask);
       c[b][2] = u64_to_f(v >> (2 * w));
     }
 #pragma unroll
+    for (int o = 0; o < TO; ++o) av[o] = u64_to_f(an[o]);
+    if (t + 1 < T) fetch(t + 1);
+#pragma unroll
     for (int o = 0; o < TO; ++o) {
-      const double a = (o0 + o < O) ? u64_to_f(__ldg(pts[(size_t)(o0 + o) * T + t] + rj)) : 0.0;
+      const double a = av[o];
 #pragma unroll
       for (int b = 0; b < TB; ++b) {
         acc[o][b][0] = __fma_rn(a, c[b][0], acc[o][b][0]);

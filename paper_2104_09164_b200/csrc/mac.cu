@@ -1,0 +1,227 @@
+// Layer MAC as a per-coefficient modular GEMM with a cp.async smem pipeline
+// (default for fp64 rings).
+//
+//   dst[o][b] = sum_t pt[o][t] * ct[t][b]   (mod p_r)   at every (r, j)
+//
+// the mult_plain + add chains of one conv / FC layer (hear/convolution.py
+// :276-312, fastpath.py:168-180; engine-side ring.py:127/159 pw_mul/pw_add),
+// bit-identical canonical residues.  The rotated ciphertexts of a layer are
+// GBs (read once from HBM), the plaintexts are shared by every clip (L2).
+//
+// B200 schedule: a CTA owns 32 coefficients of one RNS row, OB outputs and
+// CB clip-components; every term's operand rows (CB ct rows + OB pt rows of
+// 256 B) stream through an S-stage ring of shared-memory buffers with
+// 16-byte cp.async copies, so S-1 terms are in flight while one is
+// multiplied (the register-prefetch kernel in ops.cu stalled 47 % of its
+// samples on the HBM latency of the ct loads, profiles/r01_*).  A warp owns
+// TO x TB outputs per lane; products on the fp64 pipe either as fmod_mul
+// (6 ops, balanced residue) or, when the ring enables chunked dot products,
+// as three exact DFMAs against w-bit limbs of ct (dot.cu).
+#include <cstdint>
+#include "ring.cuh"
+
+namespace hb {
+
+struct HbMacGroupP {
+  const u64* const* cts;
+  const u64* const* pts;
+  u64* const* dsts;
+  int nterms;
+  int nout;
+};
+
+namespace {
+
+HB_DEV uint32_t s_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+HB_DEV void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+HB_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+HB_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+HB_DEV double limb_f(u64 x, int sh, u64 mask) { return u64_to_f((x >> sh) & mask); }
+
+HB_DEV u64 recombine3(double s0, double s1, double s2, const double* cc, double p, double pinv) {
+  const double r0 = fmod_reduce(s0, p, pinv);
+  const double r1 = fmod_mul(fmod_reduce(s1, p, pinv), cc[0], cc[1], p);
+  const double r2 = fmod_mul(fmod_reduce(s2, p, pinv), cc[2], cc[3], p);
+  return fmod_canon(r0 + r1 + r2, p, pinv);
+}
+
+template <int TO, int TB, int WO, int WB, bool C3, int S>
+__global__ void __launch_bounds__(256)
+k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
+  constexpr int OB = TO * WO, CB = TB * WB, ROWS = OB + CB;
+  constexpr int STAGE = ROWS * 32;            // u64 per stage
+  constexpr int CHUNKS = ROWS * 16;           // 16-byte copies per stage
+  extern __shared__ __align__(16) u64 smem_mac[];
+  u64* stages = smem_mac;                     // [S][ROWS][32]
+  const u64** ptab = reinterpret_cast<const u64**>(smem_mac + S * STAGE);
+  const int T = g.nterms, O = g.nout, n = RG.n;
+  const int tid = threadIdx.x + threadIdx.y * 32;
+  const int oc = blockIdx.y * OB, bc = blockIdx.x * CB;   // CTA tile origin
+  // pointer tables of this CTA's tile: ct bases [T], pt bases [OB][T]
+  for (int i = tid; i < T * (1 + OB); i += 256) {
+    if (i < T) {
+      ptab[i] = g.cts[i];
+    } else {
+      const int o = (i - T) / T, t = (i - T) % T;
+      ptab[i] = g.pts[(size_t)(oc + o < O ? oc + o : O - 1) * T + t];
+    }
+  }
+  __syncthreads();
+  const int nchunk = n / 32;
+  const int r = blockIdx.z / nchunk;
+  const int j0 = (blockIdx.z % nchunk) * 32;
+  const size_t rj0 = (size_t)r * n + j0;
+  // copy plan: chunk c -> stage row c/16 (ct rows first), 16-byte part c%16
+  auto issue = [&](int t) {
+    const uint32_t sb = s_addr(stages + (t % S) * STAGE);
+#pragma unroll
+    for (int k = 0; k < (CHUNKS + 255) / 256; ++k) {
+      const int c = tid + k * 256;
+      if (c < CHUNKS) {
+        const int row = c >> 4, part = c & 15;
+        const u64* src;
+        if (row < CB) {
+          const int b = bc + row < BC ? bc + row : BC - 1;
+          src = ptab[t] + (size_t)b * R * n + rj0 + part * 2;
+        } else {
+          src = ptab[T + (row - CB) * T + t] + rj0 + part * 2;
+        }
+        cp16(sb + (uint32_t)(row * 32 + part * 2) * 8u, src);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < T) issue(s);
+    cp_commit();
+  }
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int os = (w / WB) * TO, bs = (w % WB) * TB;   // warp sub-tile in the CTA tile
+  const HbPrime P = RG.primes[r];
+  const double p = P.pd, pinv = P.pinv;
+  const int wbits = RG.chunk_w, fold = RG.chunk_fold;
+  const u64 mask = (1ull << wbits) - 1;
+  constexpr int NA = C3 ? 3 : 1;
+  double acc[TO][TB][NA];
+#pragma unroll
+  for (int o = 0; o < TO; ++o)
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+#pragma unroll
+      for (int k = 0; k < NA; ++k) acc[o][b][k] = 0.0;
+  int since = 0;
+  for (int t = 0; t < T; ++t) {
+    cp_wait<S - 2>();
+    __syncthreads();                 // term t landed for every thread; stage t-1 is free
+    if (t + S - 1 < T) issue(t + S - 1);
+    cp_commit();
+    const u64* st = stages + (t % S) * STAGE;
+    double a[TO];
+#pragma unroll
+    for (int o = 0; o < TO; ++o) a[o] = u64_to_f(st[(CB + os + o) * 32 + lane]);
+    if constexpr (C3) {
+#pragma unroll
+      for (int b = 0; b < TB; ++b) {
+        const u64 v = st[(bs + b) * 32 + lane];
+        const double c0 = limb_f(v, 0, mask), c1 = limb_f(v, wbits, mask);
+        const double c2 = u64_to_f(v >> (2 * wbits));
+#pragma unroll
+        for (int o = 0; o < TO; ++o) {
+          acc[o][b][0] = __fma_rn(a[o], c0, acc[o][b][0]);
+          acc[o][b][1] = __fma_rn(a[o], c1, acc[o][b][1]);
+          acc[o][b][2] = __fma_rn(a[o], c2, acc[o][b][2]);
+        }
+      }
+      if (++since == fold) {
+        since = 0;
+#pragma unroll
+        for (int o = 0; o < TO; ++o)
+#pragma unroll
+          for (int b = 0; b < TB; ++b)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) acc[o][b][k] = fmod_reduce(acc[o][b][k], p, pinv);
+      }
+    } else {
+      double c[TB];
+#pragma unroll
+      for (int b = 0; b < TB; ++b) c[b] = u64_to_f(st[(bs + b) * 32 + lane]);
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const double aq = a[o] * pinv;
+#pragma unroll
+        for (int b = 0; b < TB; ++b) acc[o][b][0] += fmod_mul(c[b], a[o], aq, p);
+      }
+      if ((t & 255) == 255) {
+#pragma unroll
+        for (int o = 0; o < TO; ++o)
+#pragma unroll
+          for (int b = 0; b < TB; ++b) acc[o][b][0] = fmod_reduce(acc[o][b][0], p, pinv);
+      }
+    }
+  }
+  cp_wait<0>();
+  double cc[4] = {0, 0, 0, 0};
+  if constexpr (C3) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * r + k);
+  }
+  const size_t rj = rj0 + lane;
+#pragma unroll
+  for (int o = 0; o < TO; ++o) {
+    const int oo = oc + os + o;
+    if (oo >= O) continue;
+    u64* d = g.dsts[oo];
+#pragma unroll
+    for (int b = 0; b < TB; ++b) {
+      const int bb = bc + bs + b;
+      if (bb >= BC) continue;
+      d[(size_t)bb * R * n + rj] =
+          C3 ? recombine3(acc[o][b][0], acc[o][b][1], acc[o][b][2], cc, p, pinv)
+             : fmod_canon(acc[o][b][0], p, pinv);
+    }
+  }
+}
+
+template <int TO, int TB, int WO, int WB, bool C3, int S>
+cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cudaStream_t st) {
+  constexpr int OB = TO * WO, CB = TB * WB;
+  const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + sizeof(void*) * (size_t)g.nterms * (1 + OB);
+  if (smem > 220 * 1024) return cudaErrorNotSupported;   // caller falls back
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_pipe<TO, TB, WO, WB, C3, S>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 block(32, 8);
+  dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32));
+  k_mac_pipe<TO, TB, WO, WB, C3, S><<<grid, block, smem, st>>>(g, RG, R, BC);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
+cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, int nterms, int nout,
+                            const HbRing& RG, int rows, int BC, cudaStream_t st) {
+  if (nout <= 0 || nterms <= 0) return cudaSuccess;
+  if (!RG.use_f64) return cudaErrorNotSupported;
+  HbMacGroupP g;
+  g.cts = reinterpret_cast<const u64* const*>(cts);
+  g.pts = reinterpret_cast<const u64* const*>(pts);
+  g.dsts = reinterpret_cast<u64* const*>(dsts);
+  g.nterms = nterms;
+  g.nout = nout;
+  if (RG.chunk_fold) {
+    if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
+    return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
+  }
+  if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
+  // output tile sized to the layer so no warp idles on absent outputs
+  if (nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
+  if (nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
+  return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+}
+
+}  // namespace hb

@@ -35,7 +35,7 @@ namespace {
 
 constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
-constexpr int SMEM3 = 2 * TILE3 * 8 + 16;   // local buffer, receive buffer, mbarrier
+constexpr int SMEM3 = 2 * TILE3 * 8 + 16;   // local buffer, receive buffer, 2 mbarriers
 #ifndef HB_NTT3_MINB
 #define HB_NTT3_MINB 3
 #endif
@@ -62,10 +62,12 @@ HB_DEV uint32_t mapa(uint32_t a, uint32_t rank) {
 }
 // thread 0: one arrival expecting `bytes` of st.async traffic, made visible
 // to the cluster; every thread then arrives (relaxed) on the cluster barrier
+// (mbar[1]: the epilogue's bulk prefetch, armed later by its issuer)
 HB_DEV void xchg_init(uint64_t* mbar, uint32_t bytes) {
   if (threadIdx.x == 0) {
     const uint32_t a = smem_addr(mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a + 8) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
                  : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -79,6 +81,18 @@ HB_DEV void st_async16(uint32_t raddr, uint32_t rmbar, double a, double b) {
       "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(
           raddr),
       "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar)
+      : "memory");
+}
+// TMA bulk copy global -> own shared memory, completing on mbar (one thread;
+// the caller orders prior generic-proxy reads of dst before it)
+HB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t d = smem_addr(dst), b = smem_addr(mbar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
       : "memory");
 }
 HB_DEV void mbar_wait0(uint64_t* mbar) {
@@ -148,8 +162,8 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
   V* rb = sm + TILE3;                     // received block tile
-  uint64_t& mbar = *reinterpret_cast<uint64_t*>(rb + TILE3);
-  xchg_init(&mbar, TILE3 * sizeof(V));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(rb + TILE3);
+  xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
@@ -187,7 +201,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   // ---- push (block m, columns 2k, 2k+1) to the owner of block m's tile
   cluster_wait();   // peers' mbarriers are initialised
   {
-    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(&mbar);
+    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(mbar);
 #pragma unroll
     for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
       const int k = t + i * THREADS3;
@@ -197,7 +211,14 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       st_async16(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), v.x, v.y);
     }
   }
-  mbar_wait0(&mbar);
+  constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
+  if (MD) {
+    // the column slice is consumed: prefetch the epilogue's x_r tile into it
+    // (TMA bulk copy) while the block pass runs
+    __syncthreads();
+    if (t == 0) bulk_g2s(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
+  }
+  mbar_wait0(mbar);
   // ---- block pass over blocks [rank*32, rank*32 + 32)
   {
     const int blk = t >> 3, cc = t & 7;
@@ -241,7 +262,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   __syncthreads();
   // ---- epilogue on 16-byte chunks, lanes contiguous (coalesced HBM traffic)
   const u64 p = P.p;
-  constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
+  if (MD) mbar_wait0(mbar + 1);
 #pragma unroll 4
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
     const int k = t + i * THREADS3;
@@ -251,7 +272,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     o.x = (u64)__double_as_longlong(rb[2 * pc]);
     o.y = (u64)__double_as_longlong(rb[2 * pc + 1]);
     if (MD) {
-      const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
+      const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
       o.x = mul_shoup(sub_mod(ax.x, o.x, p), tk.scal, tk.scal_sh, p);
       o.y = mul_shoup(sub_mod(ax.y, o.y, p), tk.scal, tk.scal_sh, p);
       if (tk.add) {
@@ -290,8 +311,8 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
   V* rb = sm + TILE3;                     // received column slice
-  uint64_t& mbar = *reinterpret_cast<uint64_t*>(rb + TILE3);
-  xchg_init(&mbar, TILE3 * sizeof(V));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(rb + TILE3);
+  xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
@@ -353,7 +374,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   // ---- push (block m, columns 2k, 2k+1) to the owner of those columns
   cluster_wait();
   {
-    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(&mbar);
+    const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(mbar);
 #pragma unroll
     for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
       const int k = t + i * THREADS3;
@@ -364,7 +385,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
                  v.y);
     }
   }
-  mbar_wait0(&mbar);
+  mbar_wait0(mbar);
   // ---- column pass over columns [rank*CW, rank*CW + CW)
   const int c = t % CW, gq = t / CW, cg0 = rank * CW;
   V x[16];

@@ -693,17 +693,30 @@ k_mac_gemm_f64(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, i
   for (int o = 0; o < TO; ++o)
 #pragma unroll
     for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
-  for (int t = 0; t < T; ++t) {
-    double c[TB];
+  // software pipeline: term t+1's operands are in flight while term t's
+  // products run (the loads are two-level: smem pointer, then L2)
+  u64 cn[TB], an[TO];
+  auto fetch = [&](int t) {
 #pragma unroll
     for (int b = 0; b < TB; ++b)
-      c[b] = (b0 + b < BC) ? u64_to_f(__ldg(cts[t] + (size_t)(b0 + b) * R * n + rj)) : 0.0;
+      cn[b] = (b0 + b < BC) ? __ldg(cts[t] + (size_t)(b0 + b) * R * n + rj) : 0ull;
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+      an[o] = (o0 + o < O) ? __ldg(pts[(size_t)(o0 + o) * T + t] + rj) : 0ull;
+  };
+  fetch(0);
+  for (int t = 0; t < T; ++t) {
+    double c[TB], a[TO];
+#pragma unroll
+    for (int b = 0; b < TB; ++b) c[b] = u64_to_f(cn[b]);
+#pragma unroll
+    for (int o = 0; o < TO; ++o) a[o] = u64_to_f(an[o]);
+    if (t + 1 < T) fetch(t + 1);
 #pragma unroll
     for (int o = 0; o < TO; ++o) {
-      const double a = (o0 + o < O) ? u64_to_f(__ldg(pts[(size_t)(o0 + o) * T + t] + rj)) : 0.0;
-      const double aq = a * pinv;
+      const double aq = a[o] * pinv;
 #pragma unroll
-      for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a, aq, p);
+      for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a[o], aq, p);
     }
     if ((t & 255) == 255) {
 #pragma unroll

@@ -1,7 +1,6 @@
 #!/bin/bash
-for shape in "64 16 96 4" "64 8 96 8" "32 48 32 4"; do
-  TAG=f64_4x8 python tools/mac_bench.py $shape
-  TAG=f64_4x4 HEAR_B200_MAC_TILE=4 python tools/mac_bench.py $shape
-  TAG=c3_4x4 HEAR_B200_CHUNK=1 python tools/mac_bench.py $shape
-  TAG=c3_2x4 HEAR_B200_CHUNK=1 HEAR_B200_MAC_TILE=2 python tools/mac_bench.py $shape
+# MAC kernel variants on the conv shapes of 1d-w64 (dev tool)
+for shape in "64 16 96 4" "64 8 96 8" "64 32 8 10" "64 4 64 6"; do
+  TAG=pipe_f64 python tools/mac_bench.py $shape
+  TAG=reg_f64 HEAR_B200_MAC_PIPE=0 python tools/mac_bench.py $shape
 done
