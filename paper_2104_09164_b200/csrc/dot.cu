@@ -138,8 +138,8 @@ static cudaError_t mac_c3_t(const HbMacGroupC& g, const HbPrime* primes, const d
     cudaError_t e = mac_c3_t<TO, TB, WO, WB>(a, primes, cc, w, fold, n, R, BC, st);
     return e != cudaSuccess ? e : mac_c3_t<TO, TB, WO, WB>(b, primes, cc, w, fold, n, R, BC, st);
   }
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm_c3<TO, TB, WO, WB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_mac_gemm_c3<TO, TB, WO, WB>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));

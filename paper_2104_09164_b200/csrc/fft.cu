@@ -92,8 +92,8 @@ cudaError_t launch_encode(const double* slots, long long* coeffs, int npoly, dou
                           const HbFftTables& T, int* overflow, cudaStream_t st) {
   if (npoly <= 0) return cudaSuccess;
   const size_t smem = (size_t)T.n2 * sizeof(double2);
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_encode,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_encode, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   k_encode<<<npoly, 512, smem, st>>>(slots, coeffs, scale, T, overflow);
   return cudaGetLastError();
@@ -103,8 +103,8 @@ cudaError_t launch_decode(const double* coeffs, double* slots, int npoly, double
                           const HbFftTables& T, cudaStream_t st) {
   if (npoly <= 0) return cudaSuccess;
   const size_t smem = (size_t)T.n2 * sizeof(double2);
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_decode,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_decode, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   k_decode<<<npoly, 512, smem, st>>>(coeffs, slots, scale, T);
   return cudaGetLastError();

@@ -191,8 +191,8 @@ cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cu
   constexpr int OB = TO * WO, CB = TB * WB;
   const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + sizeof(void*) * (size_t)g.nterms * (1 + OB);
   if (smem > 220 * 1024) return cudaErrorNotSupported;   // caller falls back
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_pipe<TO, TB, WO, WB, C3, S>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, C3, S>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32));

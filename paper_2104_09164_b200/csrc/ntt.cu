@@ -225,8 +225,8 @@ template <int LOGN, int MODE, bool F64>
 static cudaError_t fwd_one(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int N = 1 << LOGN, T = N / 16;
   const size_t smem = (size_t)N * sizeof(u64);
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt_fwd<LOGN, MODE, F64>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt_fwd<LOGN, MODE, F64>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   k_ntt_fwd<LOGN, MODE, F64><<<count, T, smem, st>>>(tasks, R);
   return cudaGetLastError();
@@ -255,8 +255,8 @@ template <int LOGN, bool F64>
 static cudaError_t inv_one(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int N = 1 << LOGN, T = N / 16;
   const size_t smem = (size_t)N * sizeof(u64);
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt_inv<LOGN, F64>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt_inv<LOGN, F64>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   k_ntt_inv<LOGN, F64><<<count, T, smem, st>>>(tasks, R);
   return cudaGetLastError();

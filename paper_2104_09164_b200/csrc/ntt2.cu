@@ -342,8 +342,8 @@ static cudaError_t fwd2_t(const HbNttTask* tasks, int count, const HbRing& R, cu
   typedef typename std::conditional<F64, PolF64, PolU64>::type Pol;
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
   const size_t dyn = F64 ? 4064 * sizeof(double) : 0;
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt2_blocks<Pol, LOGN, MODE, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt2_blocks<Pol, LOGN, MODE, true>, (int)((int)dyn), &smem_cur);
   if (e != cudaSuccess) return e;
   const int CH = ntt_chunk();
   for (int c0 = 0; c0 < count; c0 += CH) {   // chunks keep the intermediate in L2
@@ -359,8 +359,8 @@ static cudaError_t inv2_t(const HbNttTask* tasks, int count, const HbRing& R, cu
   typedef typename std::conditional<F64, PolF64, PolU64>::type Pol;
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
   const size_t dyn = F64 ? 4064 * sizeof(double) : 0;
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false>, (int)((int)dyn), &smem_cur);
   if (e != cudaSuccess) return e;
   const int CH = ntt_chunk();
   for (int c0 = 0; c0 < count; c0 += CH) {

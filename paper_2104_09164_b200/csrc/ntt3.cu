@@ -425,8 +425,8 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaFuncSetAttribute(k_ntt3_fwd<PolF64, LOGN, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(SMEM3), &smem_cur);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_fwd<PolF64, LOGN, MODE>, tasks, R);
 }
@@ -446,8 +446,8 @@ cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaFuncSetAttribute(k_ntt3_inv<PolF64, LOGN>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ntt3_inv<PolF64, LOGN>, (int)(SMEM3), &smem_cur);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_inv<PolF64, LOGN>, tasks, R);
 }

@@ -627,8 +627,8 @@ static cudaError_t mac_gemm_t(const HbMacGroup& g, const HbPrime* primes, int n,
     cudaError_t e = mac_gemm_t<TO, TB, WO, WB>(a, primes, n, R, BC, st);
     return e != cudaSuccess ? e : mac_gemm_t<TO, TB, WO, WB>(b, primes, n, R, BC, st);
   }
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm<TO, TB, WO, WB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_mac_gemm<TO, TB, WO, WB>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
@@ -748,8 +748,8 @@ static cudaError_t mac_gemm_f64_t(const HbMacGroup& g, const HbPrime* primes, in
     cudaError_t e = mac_gemm_f64_t<TO, TB, WO, WB>(a, primes, n, R, BC, st);
     return e != cudaSuccess ? e : mac_gemm_f64_t<TO, TB, WO, WB>(b, primes, n, R, BC, st);
   }
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_mac_gemm_f64<TO, TB, WO, WB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_mac_gemm_f64<TO, TB, WO, WB>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));

@@ -41,6 +41,16 @@ struct HbRing {
   const double* chunk_consts;  // [nprimes][4]: 2^w mod p, fl(./p), 2^2w mod p, fl(./p)
 };
 
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more
+// than already granted (cudaFuncSetAttribute on every launch costs host time
+// in eager, launch-bound phases).  `cur` is a per-instantiation static.
+inline cudaError_t smem_attr_once(const void* fn, int bytes, int* cur) {
+  if (bytes <= *cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) *cur = bytes;
+  return e;
+}
+
 // One row-polynomial transform.  Field meaning depends on the kernel mode;
 // see ntt.cu.
 struct HbNttTask {
