@@ -35,7 +35,8 @@ namespace {
 
 constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
-constexpr int SMEM3 = 2 * TILE3 * 8 + 16;   // local buffer, receive buffer, 2 mbarriers
+// local buffer, receive buffer, staged twiddles (ntt3 TW3 x 16 B), 2 mbarriers
+constexpr int SMEM3 = 2 * TILE3 * 8 + 607 * 16 + 16;
 #ifndef HB_NTT3_MINB
 #define HB_NTT3_MINB 3
 #endif
@@ -128,9 +129,8 @@ struct ColPlan {
   static HB_DEV bool owns(int rd, int q) { return (q >> K(rd)) < (16 >> K(rd)); }
 };
 
-template <class Pol, int S1, bool FWD>
-HB_DEV void col_butterflies(typename Pol::T* x, int rd, int gq, int logn,
-                            const typename Pol::Tw* tw, const Pol& pol) {
+template <class Pol, int S1, bool FWD, class F>
+HB_DEV void col_butterflies(typename Pol::T* x, int rd, int gq, F fetch, const Pol& pol) {
   typedef ColPlan<S1, FWD> CP;
   const int K = CP::K(rd), tl = CP::tl(rd), gpt = 16 >> K, s0 = rd * 4;
 #pragma unroll
@@ -138,16 +138,47 @@ HB_DEV void col_butterflies(typename Pol::T* x, int rd, int gq, int logn,
     if (gsel >= gpt) break;
     const int gid = gq + gsel * CP::GQ;
     if (FWD) {
-      if (K == 4) fwd_group<Pol, 4>(x + gsel * 16, s0, gid / tl, tw, pol);
-      else if (K == 3) fwd_group<Pol, 3>(x + gsel * 8, s0, gid / tl, tw, pol);
-      else if (K == 2) fwd_group<Pol, 2>(x + gsel * 4, s0, gid / tl, tw, pol);
-      else fwd_group<Pol, 1>(x + gsel * 2, s0, gid / tl, tw, pol);
+      if (K == 4) fwd_group_f<Pol, 4>(x + gsel * 16, s0, gid / tl, fetch, pol);
+      else if (K == 3) fwd_group_f<Pol, 3>(x + gsel * 8, s0, gid / tl, fetch, pol);
+      else if (K == 2) fwd_group_f<Pol, 2>(x + gsel * 4, s0, gid / tl, fetch, pol);
+      else fwd_group_f<Pol, 1>(x + gsel * 2, s0, gid / tl, fetch, pol);
     } else {
-      if (K == 4) inv_group<Pol, 4>(x + gsel * 16, s0 + 7, gid / tl, logn, tw, pol);
-      else if (K == 3) inv_group<Pol, 3>(x + gsel * 8, s0 + 7, gid / tl, logn, tw, pol);
-      else if (K == 2) inv_group<Pol, 2>(x + gsel * 4, s0 + 7, gid / tl, logn, tw, pol);
-      else inv_group<Pol, 1>(x + gsel * 2, s0 + 7, gid / tl, logn, tw, pol);
+      if (K == 4) inv_group_f<Pol, 4>(x + gsel * 16, s0 + 7, gid / tl, fetch, pol);
+      else if (K == 3) inv_group_f<Pol, 3>(x + gsel * 8, s0 + 7, gid / tl, fetch, pol);
+      else if (K == 2) inv_group_f<Pol, 2>(x + gsel * 4, s0 + 7, gid / tl, fetch, pol);
+      else inv_group_f<Pol, 1>(x + gsel * 2, s0 + 7, gid / tl, fetch, pol);
     }
+  }
+}
+
+// Shared-memory twiddles of one CTA (TW3 entries, 16 B each): the column
+// stages (table entries 1..M-1, shared by every column) and the four block
+// stages of this CTA's tile that run on stride-8 groups of 16 (forward
+// stages S1..S1+3 / inverse stages 3..6: 32+64+128+256 entries).  Staged
+// once with coalesced loads so the butterflies read them with LDS at
+// (mostly) immediate offsets instead of 64-bit-addressed broadcast LDGs.
+constexpr int TWC = 127, TW3 = TWC + 480;
+
+template <int LOGN, bool FWD>
+HB_DEV void stage_twiddles(HbTwD* tws, const HbTwD* tab, int rank) {
+  constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1;
+  for (int k = threadIdx.x; k < TW3; k += THREADS3) {
+    int idx;
+    if (k < TWC) {
+      idx = 1 + (k < M - 1 ? k : 0);
+    } else {
+      const int kb = k - TWC;
+      if (FWD) {   // stage S1+e: 32 << e entries from 2^(S1+e) + rank*(32 << e)
+        const int e = kb < 32 ? 0 : kb < 96 ? 1 : kb < 224 ? 2 : 3;
+        idx = (1 << (S1 + e)) + rank * (32 << e) + (kb - 32 * ((1 << e) - 1));
+      } else {     // stage r = 3..6: 4096 >> (r+1) entries from N>>(r+1) + rank*(4096>>(r+1))
+        const int r = kb < 256 ? 3 : kb < 384 ? 4 : kb < 448 ? 5 : 6;
+        const int off = r == 3 ? 0 : r == 4 ? 256 : r == 5 ? 384 : 448;
+        idx = (N >> (r + 1)) + rank * (4096 >> (r + 1)) + (kb - off);
+      }
+    }
+    const double2 w = __ldg(reinterpret_cast<const double2*>(tab + idx));
+    tws[k] = HbTwD{w.x, w.y};
   }
 }
 
@@ -162,13 +193,19 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
   V* rb = sm + TILE3;                     // received block tile
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(rb + TILE3);
+  HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
   xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
   const Pol pol(P);
-  const typename Pol::Tw* tw = Pol::fwd_table(R, tk.dst_prime);
+  stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, tk.dst_prime), rank);
+  auto fetch_col = [&](int s, int idx) { return tws[(1 << s) + idx - 1]; };
+  auto fetch_blk = [&](int s, int idx) {
+    const int e = s - S1;
+    return tws[TWC + 32 * ((1 << e) - 1) + idx - rank * (32 << e)];
+  };
   const int t = threadIdx.x;
   u64 ps = 0, ps_half = 0;
   if (MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER) {
@@ -189,7 +226,8 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         x[q] = rd == 0 ? ld_src<Pol, MODE>(tk, pol, ps, ps_half, (size_t)m * 128 + cg0 + c)
                        : sm[csw<CW>(m, c)];
       }
-      col_butterflies<Pol, S1, true>(x, rd, gq, LOGN, tw, pol);
+      if (rd == 0) __syncthreads();   // staged twiddles visible (src loads already issued)
+      col_butterflies<Pol, S1, true>(x, rd, gq, fetch_col, pol);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         if (!CP::owns(rd, q)) break;
@@ -225,7 +263,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = rb[bsw(blk * 128 + u * 8 + cc)];
-    fwd_group<Pol, 4>(x, S1, rank * 32 + blk, tw, pol);
+    fwd_group_f<Pol, 4>(x, S1, rank * 32 + blk, fetch_blk, pol);
 #pragma unroll
     for (int u = 0; u < 16; ++u) rb[bsw(blk * 128 + u * 8 + cc)] = x[u];
   }
@@ -311,13 +349,19 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
   V* rb = sm + TILE3;                     // received column slice
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(rb + TILE3);
+  HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
   xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
   const Pol pol(P);
-  const typename Pol::Tw* tw = Pol::inv_table(R, tk.dst_prime);
+  stage_twiddles<LOGN, false>(tws, Pol::inv_table(R, tk.dst_prime), rank);
+  auto fetch_col = [&](int r, int idx) { return tws[(N >> (r + 1)) + idx - 1]; };
+  auto fetch_blk = [&](int r, int idx) {
+    const int off = r == 3 ? 0 : r == 4 ? 256 : r == 5 ? 384 : 448;
+    return tws[TWC + off + idx - rank * (4096 >> (r + 1))];
+  };
   const int t = threadIdx.x;
   const size_t base = (size_t)rank * TILE3;
   // ---- block pass on tile `rank`: coalesced 16-byte loads into the
@@ -366,7 +410,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
     V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[bsw(blk * 128 + u * 8 + cc)];
-    inv_group<Pol, 4>(x, 3, rank * 32 + blk, LOGN, tw, pol);
+    inv_group_f<Pol, 4>(x, 3, rank * 32 + blk, fetch_blk, pol);
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[bsw(blk * 128 + u * 8 + cc)] = pol.inv_round_end(x[u]);
   }
@@ -397,7 +441,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
       if (!CP::owns(rd, q)) break;
       x[q] = buf[csw<CW>(CP::m_of(rd, gq, q), c)];
     }
-    col_butterflies<Pol, S1, false>(x, rd, gq, LOGN, tw, pol);
+    col_butterflies<Pol, S1, false>(x, rd, gq, fetch_col, pol);
     const bool last = rd == CP::NR - 1;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {

@@ -796,16 +796,28 @@ k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__
   }
   const u64* de = tk.de + b * tk.de_bstride;
   double b0 = 0, b1 = 0, a0 = 0, a1 = 0;
-  for (int i = 0; i < tk.ndig; ++i) {
+  // two-deep software pipeline over the digits: digit i+1's operands (L2)
+  // are in flight while digit i multiplies
+  u64 xd0, xd1;
+  ulonglong2 kb, ka;
+  auto fetch = [&](int i) {
     const u64* d = de + i * tk.de_dstride;
-    const double x0 = u64_to_f(__ldg(d + s0)), x1 = u64_to_f(__ldg(d + s1));
+    xd0 = __ldg(d + s0);
+    xd1 = __ldg(d + s1);
+    kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
+    ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
+  };
+  fetch(0);
+  for (int i = 0; i < tk.ndig; ++i) {
+    const double x0 = u64_to_f(xd0), x1 = u64_to_f(xd1);
+    const double kb0 = u64_to_f(kb.x), kb1 = u64_to_f(kb.y);
+    const double ka0 = u64_to_f(ka.x), ka1 = u64_to_f(ka.y);
+    if (i + 1 < tk.ndig) fetch(i + 1);
     const double q0 = x0 * pinv, q1 = x1 * pinv;
-    const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
-    const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
-    b0 += fmod_mul(u64_to_f(kb.x), x0, q0, p);
-    b1 += fmod_mul(u64_to_f(kb.y), x1, q1, p);
-    a0 += fmod_mul(u64_to_f(ka.x), x0, q0, p);
-    a1 += fmod_mul(u64_to_f(ka.y), x1, q1, p);
+    b0 += fmod_mul(kb0, x0, q0, p);
+    b1 += fmod_mul(kb1, x1, q1, p);
+    a0 += fmod_mul(ka0, x0, q0, p);
+    a1 += fmod_mul(ka1, x1, q1, p);
   }
   ulonglong2 rb, ra;
   rb.x = fmod_canon(b0, p, pinv);
