@@ -72,6 +72,9 @@ int hb_ntt_inv(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Kernel launches one hb_ntt_fwd / hb_ntt_inv call of `count` rows enqueues
  * (launch accounting; no reference counterpart).                             */
 int hb_ntt_kernels(hb_ring* ring, int count);
+/* 1 when the ring's modular arithmetic runs on the fp64 pipe (every prime
+ * < 2^42 and HEAR_B200_INT_NTT unset), else 0.                              */
+int hb_ring_uses_f64(const hb_ring* ring);
 /* Element-wise op `op` over HbEwTask rows: 0 add (ring.py:159), 1 sub
  * (ring.py:167), 2 mul (ring.py:127), 3 scalar mul (ring.py:175), 4 a*b+c
  * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,
@@ -88,6 +91,15 @@ int hb_mac_strided(hb_ring* ring, const void* outs, int nout, const void* terms,
  * base pointers ([bc, rows, N] ciphertext blocks, [rows, N] plaintexts).     */
 int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* dsts, int nterms,
                   int nout, int rows, int bc, void* stream);
+/* Key-switch inner product of a hoisted rotation group as a per-coefficient
+ * modular GEMM (engine.py:305-351, ring.py:136-156, on pre-permuted keys):
+ * dsts[o][b*dst_bstride + r*N + j] = sum_i de[i][b*de_bstride + r*N + j] *
+ * keys[o*ndig + i][r*N + j] (mod prime_off + r), for o < nout (rotation x
+ * component), b < bc, r < rows.  de, keys, dsts: device arrays of row-block
+ * base pointers.  fp64 rings only.                                          */
+int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* dsts, int ndig,
+               int nout, int rows, int bc, long long de_bstride, long long dst_bstride,
+               int prime_off, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);

@@ -125,10 +125,14 @@ class CkksBackend(BackendBase):
             ps = np.array(chain[:lvl], dtype=np.uint64)
             self._resc.append((inv, shoup_np(inv, ps) if lvl else inv))
         self._crt_cache: dict = {}
-        # opt-in (HEAR_B200_PREPERM=1): rotation inner products on pre-permuted
-        # keys with the Galois gather after ModDown instead of gathering the
-        # digits; bit-identical, measured ~2% slower and 2x rotation-key memory
-        self.preperm = os.environ.get("HEAR_B200_PREPERM", "0") == "1"
+        # rotation inner products on pre-permuted keys (default; HEAR_B200_PREPERM=0
+        # disables): the digits are read in natural order, so a hoisted group
+        # is one GEMM over digits x (rotation, component) and the Galois map is
+        # applied by the ModDown scatter; bit-identical, 2x rotation-key memory
+        self.preperm = os.environ.get("HEAR_B200_PREPERM", "1") == "1"
+        # hoisted groups of at least this many pre-permuted rotations take the
+        # GEMM inner product (ks_gemm) instead of the per-job kernel
+        self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "2"))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -611,7 +615,12 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        self.ring.ks_inner2(np.concatenate(parts), bsz)
+        offs = {job[4] if len(job) > 4 else 0 for job in jobs}
+        if (len(late) == nj and nj >= self.ks_gemm_min and len(offs) == 1
+                and self.ring.use_f64):
+            self._ks_gemm(de, der, lvl, jobs, ipr, bsz, offs.pop())
+        else:
+            self.ring.ks_inner2(np.concatenate(parts), bsz)
         m, r = nj * bsz * 2, lvl + 1
         iprows = rp(ip).reshape(m, rows)
         spc = self.ring.empty(m)
@@ -680,6 +689,29 @@ class CkksBackend(BackendBase):
             for q, (j, _, _) in enumerate(late):
                 res[j] = fin[q]
         return res
+
+    def _ks_gemm(self, de, der, lvl: int, jobs, ipr, bsz: int, off: int):
+        """Inner products of a hoisted group on pre-permuted keys as one
+        per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): the digits of each
+        clip are read once for every rotation of the group, terms = digits,
+        outputs = (rotation, component).  Chain rows and the special row are
+        two launches (the special row's prime and key row differ)."""
+        ndig, rows, n8 = lvl + 1, lvl + 2, np.uint64(8 * self.n)
+        dep = der[off, :, 0]                                    # [ndig] row 0 of each digit
+        kp, kps, dp = [], [], []
+        for j, job in enumerate(jobs):
+            key = job[0]
+            kst = np.uint64((key.lmax + 2)) * n8
+            for t in (key.bp, key.ap):
+                base = np.uint64(t.data_ptr()) + np.arange(ndig, dtype=np.uint64) * kst
+                kp.append(base)
+                kps.append(base + np.uint64(key.lmax + 1) * n8)
+            dp.extend([ipr[j, 0, 0, 0], ipr[j, 0, 1, 0]])
+        kp, kps, dp = np.stack(kp), np.stack(kps), np.array(dp, dtype=np.uint64)
+        de_bs, dst_bs = ndig * rows * self.n, 2 * rows * self.n
+        self.ring.ks_gemm(dep, kp, dp, lvl + 1, bsz, de_bs, dst_bs, 0)
+        sp = np.uint64(lvl + 1) * n8
+        self.ring.ks_gemm(dep + sp, kps, dp + sp, 1, bsz, de_bs, dst_bs, self.S)
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)

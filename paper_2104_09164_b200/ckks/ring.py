@@ -224,6 +224,25 @@ class RingContext:
                                               base + 8 * (nterms + nout * nterms), nterms, nout,
                                               rows, bc, self.stream), "mac_shared")
 
+    @property
+    def use_f64(self) -> bool:
+        """Modular arithmetic on the fp64 pipe (csrc/cabi.cu policy)."""
+        return bool(self._lib.hb_ring_uses_f64(self.handle))
+
+    def ks_gemm(self, de: np.ndarray, keys: np.ndarray, dsts: np.ndarray, rows: int, bc: int,
+                de_bstride: int, dst_bstride: int, prime_off: int):
+        """Hoisted-group key-switch inner product as a per-coefficient GEMM:
+        dsts[o] = sum_i keys[o, i] * de[i] over [bc] clip blocks of rows rows."""
+        nout, ndig = keys.shape
+        if nout:
+            buf = _upload(np.concatenate([de.ravel(), keys.ravel(), dsts.ravel()])
+                          .astype(np.uint64), self.device)
+            base = _ptr(buf)
+            nat.check(self._lib.hb_ks_gemm(self.handle, base, base + 8 * ndig,
+                                           base + 8 * (ndig + nout * ndig), ndig, nout, rows, bc,
+                                           de_bstride, dst_bstride, prime_off, self.stream),
+                      "ks_gemm")
+
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):
             d = _upload(tasks, self.device)

@@ -37,6 +37,8 @@ cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int,
 cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_pipe(const void*, const void*, const void*, int, int, const HbRing&, int,
                             int, cudaStream_t);
+cudaError_t launch_ks_gemm(const void*, const void*, const void*, int, int, const HbRing&, int, int,
+                           long long, long long, int, cudaStream_t);
 cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, const HbRing&, int,
                                int, cudaStream_t);
 cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
@@ -289,6 +291,8 @@ int hb_ntt_inv(hb_ring* r, const void* tasks, int count, void* stream) {
 
 int hb_ntt_kernels(hb_ring* r, int count) { return ntt_kernels(r->dev, count); }
 
+int hb_ring_uses_f64(const hb_ring* r) { return r && r->dev.use_f64 ? 1 : 0; }
+
 int hb_ew(hb_ring* r, int op, const void* tasks, int count, void* stream) {
   cudaError_t e = launch_ew(op, (const HbEwTask*)tasks, count, r->dev.primes, r->dev.n,
                             (cudaStream_t)stream);
@@ -340,6 +344,14 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
       : launch_mac_gemm(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
                         (cudaStream_t)stream);
   return e ? fail(e, "hb_mac_shared") : 0;
+}
+
+int hb_ks_gemm(hb_ring* r, const void* de, const void* keys, const void* dsts, int ndig, int nout,
+               int rows, int bc, long long de_bstride, long long dst_bstride, int prime_off,
+               void* stream) {
+  cudaError_t e = launch_ks_gemm(de, keys, dsts, ndig, nout, r->dev, rows, bc, de_bstride,
+                                 dst_bstride, prime_off, (cudaStream_t)stream);
+  return e ? fail(e, "hb_ks_gemm") : 0;
 }
 
 int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {

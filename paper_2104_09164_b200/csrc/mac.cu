@@ -28,6 +28,9 @@ struct HbMacGroupP {
   u64* const* dsts;
   int nterms;
   int nout;
+  long long ct_bstride;   // elements between clips of a ct / dst block
+  long long dst_bstride;
+  int prime_off;          // prime of row r = prime_off + r
 };
 
 namespace {
@@ -86,7 +89,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
         const u64* src;
         if (row < CB) {
           const int b = bc + row < BC ? bc + row : BC - 1;
-          src = ptab[t] + (size_t)b * R * n + rj0 + part * 2;
+          src = ptab[t] + (size_t)b * g.ct_bstride + rj0 + part * 2;
         } else {
           src = ptab[T + (row - CB) * T + t] + rj0 + part * 2;
         }
@@ -101,7 +104,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   }
   const int lane = threadIdx.x, w = threadIdx.y;
   const int os = (w / WB) * TO, bs = (w % WB) * TB;   // warp sub-tile in the CTA tile
-  const HbPrime P = RG.primes[r];
+  const HbPrime P = RG.primes[g.prime_off + r];
   const double p = P.pd, pinv = P.pinv;
   const int wbits = RG.chunk_w, fold = RG.chunk_fold;
   const u64 mask = (1ull << wbits) - 1;
@@ -167,7 +170,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   double cc[4] = {0, 0, 0, 0};
   if constexpr (C3) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * r + k);
+    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * (g.prime_off + r) + k);
   }
   const size_t rj = rj0 + lane;
 #pragma unroll
@@ -179,7 +182,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     for (int b = 0; b < TB; ++b) {
       const int bb = bc + bs + b;
       if (bb >= BC) continue;
-      d[(size_t)bb * R * n + rj] =
+      d[(size_t)bb * g.dst_bstride + rj] =
           C3 ? recombine3(acc[o][b][0], acc[o][b][1], acc[o][b][2], cc, p, pinv)
              : fmod_canon(acc[o][b][0], p, pinv);
     }
@@ -202,6 +205,19 @@ cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cu
 
 }  // namespace
 
+static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
+                                     cudaStream_t st) {
+  if (RG.chunk_fold) {
+    if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
+    return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
+  }
+  if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
+  // output tile sized to the layer so no warp idles on absent outputs
+  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
+  if (g.nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
+  return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+}
+
 // fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
 cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, int nterms, int nout,
                             const HbRing& RG, int rows, int BC, cudaStream_t st) {
@@ -213,15 +229,30 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
   g.dsts = reinterpret_cast<u64* const*>(dsts);
   g.nterms = nterms;
   g.nout = nout;
-  if (RG.chunk_fold) {
-    if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
-    return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
-  }
-  if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
-  // output tile sized to the layer so no warp idles on absent outputs
-  if (nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
-  if (nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
-  return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+  g.ct_bstride = g.dst_bstride = (long long)rows * RG.n;
+  g.prime_off = 0;
+  return mac_pipe_dispatch(g, RG, rows, BC, st);
+}
+
+// Key-switch inner product of a hoisted rotation group on pre-permuted keys
+// (engine.py:305-351 / ring.py:136-156 with the Galois gather moved after
+// ModDown): terms = digits, outputs = (rotation, component), clips = BC.
+// Row r of the launch runs in prime prime_off + r; clip strides explicit.
+cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* dsts, int ndig, int nout,
+                           const HbRing& RG, int rows, int BC, long long de_bstride,
+                           long long dst_bstride, int prime_off, cudaStream_t st) {
+  if (nout <= 0 || ndig <= 0) return cudaSuccess;
+  if (!RG.use_f64) return cudaErrorNotSupported;
+  HbMacGroupP g;
+  g.cts = reinterpret_cast<const u64* const*>(de);
+  g.pts = reinterpret_cast<const u64* const*>(keys);
+  g.dsts = reinterpret_cast<u64* const*>(dsts);
+  g.nterms = ndig;
+  g.nout = nout;
+  g.ct_bstride = de_bstride;
+  g.dst_bstride = dst_bstride;
+  g.prime_off = prime_off;
+  return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
 }  // namespace hb

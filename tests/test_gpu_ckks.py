@@ -176,18 +176,21 @@ def test_chunked_dot_products_bit_exact(golden):
     assert digest(*be.export(m[5])) == g["ops"]["6"]["rot_many_5"]
 
 
-def test_prepermuted_rotation_keys_bit_exact(golden):
-    """Opt-in pre-permuted rotation keys give the reference's rotations."""
+@pytest.mark.parametrize("preperm", ["1", "0"])
+def test_prepermuted_rotation_keys_bit_exact(golden, preperm):
+    """Pre-permuted rotation keys (default) and the digit-gather path both
+    give the reference's rotations."""
     import os
     from paper_2104_09164_b200.ckks.engine import CkksBackend
     from paper_2104_09164_b200.ckks.params import gen_params
-    os.environ["HEAR_B200_PREPERM"] = "1"
+    os.environ["HEAR_B200_PREPERM"] = preperm
     try:
         be = CkksBackend(gen_params("toy-fast"), seed=7)
         g = golden["toy-fast"]
         be.ensure_rotation_keys({int(a): l for a, l in g["rot_levels"].items()})
     finally:
         del os.environ["HEAR_B200_PREPERM"]
+    assert be.preperm == (preperm == "1")
     ps = be.params
     for lvl in (6, 2):
         A = be.import_ct(*rand_ct(ps, lvl, 100 + lvl), lvl, ps.msg_scale)
@@ -196,3 +199,49 @@ def test_prepermuted_rotation_keys_bit_exact(golden):
         assert digest(*be.export(m[1])) == g["ops"][str(lvl)]["rot_many_1"]
     A = be.import_ct(*rand_ct(ps, 2, 102), 2, ps.msg_scale)
     assert digest(*be.export(be._raw_rot(A, 2047))) == g["ops"]["2"]["rot_2047"]
+
+
+_ORACLE = {}
+
+
+@pytest.mark.parametrize("env", [{}, {"HEAR_B200_KS_GEMM_MIN": "1000"}, {"HEAR_B200_PREPERM": "0"},
+                                 {"HEAR_B200_NTT3": "0"}])
+def test_hoisted_rotations_fast_hear_vs_oracle(env):
+    """N = 2^14 hoisted rotations (cluster NTT, GEMM inner product on
+    pre-permuted keys, ModDown scatter) against the CPU oracle, for every
+    inner-product path; batched clips."""
+    import os
+    from oracle.cpu_engine import OracleCkks
+    from paper_2104_09164_b200.backend import Ct
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    ps = gen_params("fast-hear")
+    amounts = [1, 5, 77, 4000]
+    levels = {a: 12 for a in amounts}
+    if "cpu" not in _ORACLE:
+        cpu = OracleCkks(ps, seed=11)
+        cpu.ensure_rotation_keys(levels)
+        _ORACLE["cpu"] = cpu
+    cpu = _ORACLE["cpu"]
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        gpu = CkksBackend(ps, seed=11)
+        gpu.ensure_rotation_keys(levels)
+        for lvl in (12, 7):
+            cts = [rand_ct(ps, lvl, 40 + lvl + i) for i in range(3)]
+            batch = gpu.import_ct(np.stack([c[0] for c in cts]), np.stack([c[1] for c in cts]),
+                                  lvl, ps.msg_scale)
+            got = gpu._raw_rot_many(batch, amounts)
+            for a in amounts:
+                r = gpu.export(got[a])
+                for i, c in enumerate(cts):
+                    want = cpu._raw_rot(Ct(c, lvl, Fraction(ps.msg_scale), ps.n2), a).payload
+                    assert np.array_equal(r[0][i], want[0]) and np.array_equal(r[1][i], want[1]), \
+                        (env, lvl, a, i)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
