@@ -291,15 +291,24 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     }
     fwd_group_f<Pol, 3>(x, S1 + 4, (rank * 32 + b2) * 16 + G8, fetch_fine, pol);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {   // canonical residues back in place
+    for (int v = 0; v < 4; ++v) {   // back in place: balanced (ModDown) or canonical
       const int pc = swz3_chunk((e0 >> 1) + v);
-      rb[2 * pc] = __longlong_as_double((long long)pol.fwd_final(x[2 * v]));
-      rb[2 * pc + 1] = __longlong_as_double((long long)pol.fwd_final(x[2 * v + 1]));
+      if (MD) {
+        rb[2 * pc] = x[2 * v];
+        rb[2 * pc + 1] = x[2 * v + 1];
+      } else {
+        rb[2 * pc] = __longlong_as_double((long long)pol.fwd_final(x[2 * v]));
+        rb[2 * pc + 1] = __longlong_as_double((long long)pol.fwd_final(x[2 * v + 1]));
+      }
     }
   }
   __syncthreads();
-  // ---- epilogue on 16-byte chunks, lanes contiguous (coalesced HBM traffic)
-  const u64 p = P.p;
+  // ---- epilogue on 16-byte chunks, lanes contiguous (coalesced HBM traffic).
+  // ModDown on the fp64 pipe: (x_r - y) * P^-1 (+ addend) from the balanced
+  // transform output y, one canonicalisation (the integer sub/Shoup/add
+  // chain cost ~30 integer instructions per element)
+  const double pd = P.pd, pinv = P.pinv;
+  const double sd = u64_to_f(tk.scal), sq = sd * pinv;
   if (MD) mbar_wait0(mbar + 1);
 #pragma unroll 4
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
@@ -307,12 +316,10 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     const size_t j = base + 2 * k;
     const int pc = swz3_chunk(k);
     ulonglong2 o;
-    o.x = (u64)__double_as_longlong(rb[2 * pc]);
-    o.y = (u64)__double_as_longlong(rb[2 * pc + 1]);
     if (MD) {
       const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
-      o.x = mul_shoup(sub_mod(ax.x, o.x, p), tk.scal, tk.scal_sh, p);
-      o.y = mul_shoup(sub_mod(ax.y, o.y, p), tk.scal, tk.scal_sh, p);
+      double r0 = fmod_mul(u64_to_f(ax.x) - rb[2 * pc], sd, sq, pd);
+      double r1 = fmod_mul(u64_to_f(ax.y) - rb[2 * pc + 1], sd, sq, pd);
       if (tk.add) {
         u64 a0, a1;
         if (MODE == FWD_MODDOWN && tk.perm) {
@@ -324,9 +331,14 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
           a0 = a2.x;
           a1 = a2.y;
         }
-        o.x = add_mod(o.x, a0, p);
-        o.y = add_mod(o.y, a1, p);
+        r0 += u64_to_f(a0);
+        r1 += u64_to_f(a1);
       }
+      o.x = fmod_canon(r0, pd, pinv);
+      o.y = fmod_canon(r1, pd, pinv);
+    } else {
+      o.x = (u64)__double_as_longlong(rb[2 * pc]);
+      o.y = (u64)__double_as_longlong(rb[2 * pc + 1]);
     }
     if (MODE == FWD_MODDOWN_SCATTER) {
       const int2 sc = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
