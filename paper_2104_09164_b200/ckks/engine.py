@@ -130,9 +130,9 @@ class CkksBackend(BackendBase):
         # is one GEMM over digits x (rotation, component) and the Galois map is
         # applied by the ModDown scatter; bit-identical, 2x rotation-key memory
         self.preperm = os.environ.get("HEAR_B200_PREPERM", "1") == "1"
-        # hoisted groups of at least this many pre-permuted rotations take the
-        # GEMM inner product (ks_gemm) instead of the per-job kernel
-        self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "2"))
+        # key switches of at least this many pre-permuted rotations take the
+        # GEMM inner product (ks_gemm) instead of the per-job kernel (ks_inner2)
+        self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "1"))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -615,10 +615,20 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        offs = {job[4] if len(job) > 4 else 0 for job in jobs}
-        if (len(late) == nj and nj >= self.ks_gemm_min and len(offs) == 1
-                and self.ring.use_f64):
-            self._ks_gemm(de, der, lvl, jobs, ipr, bsz, offs.pop())
+        if len(late) == nj and nj >= self.ks_gemm_min and self.ring.use_f64:
+            # one GEMM per digit set (a hoisted group shares it; rot_each jobs
+            # each bring their own)
+            groups: dict = {}
+            for j, job in enumerate(jobs):
+                groups.setdefault(job[4] if len(job) > 4 else 0, []).append(j)
+            rest = []
+            for off, js in groups.items():
+                if len(js) >= 2 or bsz >= 8:
+                    self._ks_gemm(der, lvl, [jobs[j] for j in js], ipr[js], bsz, off)
+                else:   # a lone small key switch: batch it into one per-job launch
+                    rest.extend(parts[j] for j in js)
+            if rest:
+                self.ring.ks_inner2(np.concatenate(rest), bsz)
         else:
             self.ring.ks_inner2(np.concatenate(parts), bsz)
         m, r = nj * bsz * 2, lvl + 1
@@ -690,7 +700,7 @@ class CkksBackend(BackendBase):
                 res[j] = fin[q]
         return res
 
-    def _ks_gemm(self, de, der, lvl: int, jobs, ipr, bsz: int, off: int):
+    def _ks_gemm(self, der, lvl: int, jobs, ipr, bsz: int, off: int):
         """Inner products of a hoisted group on pre-permuted keys as one
         per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): the digits of each
         clip are read once for every rotation of the group, terms = digits,

@@ -213,6 +213,7 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   }
   if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
   // output tile sized to the layer so no warp idles on absent outputs
+  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
   return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
