@@ -164,31 +164,45 @@ def reference_arm(args):
 FP64_MEASURED_TFLOPS = 17.93   # DFMA/s measured on this pool (profiles/r01_microbench.txt)
 
 
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+
+
 def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
-    """Time one key-switch ModDown launch -- k_ntt_fwd in FWD_MODDOWN mode over
-    B*2*(l+1) output rows, the largest kernel share of the evaluation
-    (profiles/r01_launches_*) -- with CUDA events on the launching stream.
-    Algorithmic bytes per output row: read x_r + write the result (16 N B);
-    plus one read of each special-prime source row per (b, component)."""
+    """Time one rotation ModDown launch -- k_ntt3_fwd<FWD_MODDOWN_SCATTER>, the
+    largest kernel share of the evaluation (profiles/r01_launches_*): the
+    ModDown of bsz clips x 2 components x (l+1) rows of a rotation computed on
+    pre-permuted keys, result scattered through the inverse Galois map, c0
+    added -- with CUDA events on the launching stream.
+    Algorithmic bytes: per output row read x_r (8N) + the perm (4N) + write
+    (8N); per component-0 row read the addend c0 (8N); per (clip, component)
+    one read of the special-prime source row (8N).  `traffic` is the DRAM
+    read+write of the same launch from an ncu --set full capture
+    (tools/roofline_probe.py -> profiles/r01_roofline_traffic.json)."""
     import torch
     from paper_2104_09164_b200 import _native as nat
     from paper_2104_09164_b200.ckks.engine import _tasks
     from paper_2104_09164_b200.ckks.ring import _upload
     n = be.n
     m, r = bsz * 2, lvl + 1
-    src = be.ring.empty(m).random_(0, 1 << 30)
-    aux = be.ring.empty(m, r).random_(0, 1 << 30)
+    g = torch.Generator(device=be.dev).manual_seed(1)
+    src = be.ring.empty(m).random_(0, 1 << 30, generator=g)
+    aux = be.ring.empty(m, r).random_(0, 1 << 30, generator=g)
+    c0 = be.ring.empty(bsz, r).random_(0, 1 << 30, generator=g)
     out = be.ring.empty(m, r)
+    inv = be.ring.perm_inv_for(be.ring.perm_dev(be.ring.galois_element(1)))
+    add = np.zeros((bsz, 2, r), dtype=np.uint64)
+    add[:, 0] = be.ring.row_ptrs(c0).reshape(bsz, r)
     t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(be.ring.row_ptrs(src), r),
                dst=be.ring.row_ptrs(out), aux=be.ring.row_ptrs(aux), src_prime=be.S,
                dst_prime=np.tile(np.arange(r), m), scal=np.tile(be._pinv[:r], m),
-               scal_sh=np.tile(be._pinv_sh[:r], m))
+               scal_sh=np.tile(be._pinv_sh[:r], m), add=add.ravel(),
+               perm=np.full(m * r, inv.data_ptr(), dtype=np.uint64))
     d = _upload(t, be.dev)
     L = nat.lib()
     st = torch.cuda.current_stream()
 
     def launch():
-        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_MODDOWN,
+        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_MODDOWN_SCATTER,
                                st.cuda_stream), "ntt")
     for _ in range(3):
         launch()
@@ -201,13 +215,22 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     e1.record(st)
     torch.cuda.synchronize()
     sec = e0.elapsed_time(e1) / 1e3 / reps
-    algo = (2 * m * r + m) * n * 8
+    algo = (m * r * 20 + bsz * r * 8 + m * 8) * n
     gbs = algo / sec / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     bfly = m * r * (n // 2) * (n.bit_length() - 1)
-    return {"kernel": "k_ntt2_cols+k_ntt2_blocks<FWD_MODDOWN> (key-switch ModDown NTT)",
+    kname = "k_ntt3_fwd<FWD_MODDOWN_SCATTER>"
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            tr = json.load(f)
+        if tr.get("kernel") == kname and tr.get("rows") == m * r and tr.get("n") == n:
+            traffic = tr["dram_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"kernel": kname + " (rotation ModDown: cluster NTT + fused epilogue)",
             "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(gbs / peak, 4), "traffic": None, "launch_us": round(sec * 1e6, 2),
+            "frac": round(gbs / peak, 4), "traffic": traffic, "launch_us": round(sec * 1e6, 2),
             "rows_per_launch": m * r, "algorithmic_bytes_per_launch": algo,
             "butterflies_per_s": round(bfly / sec / 1e12, 3),
             "fp64_frac_of_measured": round(bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12), 3),
@@ -215,31 +238,34 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
 
 
 def keyswitch_rate(be, lvl: int, bsz: int) -> dict:
-    """Key-switch ops/s: non-hoisted HRotate of bsz fresh-shaped ciphertexts
-    at level lvl (ModUp + inner product + ModDown + automorphism), and the
-    hoisted form (16 amounts of one handle sharing the ModUp)."""
+    """Key-switch ops/s at level lvl on one handle of bsz clips: HRotate by
+    one amount (bsz key switches: ModUp + inner product + ModDown +
+    automorphism) and the hoisted form (16 amounts sharing the ModUp).
+    Eager calls timed with CUDA events, best of 3 blocks of 3 calls."""
     import torch
     from fractions import Fraction
     from paper_2104_09164_b200.backend import Ct
     from paper_2104_09164_b200.ckks.engine import CtData
     be.ensure_rotation_keys({k: be.L for k in range(1, 17)})
-    cts = [Ct(CtData(be.ring.empty(1, 2, lvl + 1).random_(0, 1 << 30)), lvl, Fraction(1), be.n2)
-           for _ in range(bsz)]
     big = Ct(CtData(be.ring.empty(bsz, 2, lvl + 1).random_(0, 1 << 30)), lvl, Fraction(1), be.n2)
     out = {}
-    for name, fn, ops in (("rotate", lambda: be._raw_rot_each([(c, 1) for c in cts]), bsz),
+    for name, fn, ops in (("rotate", lambda: be._raw_rot(big, 1), bsz),
                           ("rotate_hoisted16",
                            lambda: be._raw_rot_many(big, list(range(1, 17))), 16 * bsz)):
         fn()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        best = 0.0
         for _ in range(3):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        out[name] = round(3 * ops / (e0.elapsed_time(e1) / 1e3), 1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 3 * ops / (e0.elapsed_time(e1) / 1e3))
+        out[name] = round(best, 1)
     out["level"] = lvl
+    out["clips"] = bsz
     out["unit"] = "key-switch ops/s"
     return out
 
@@ -356,7 +382,7 @@ def gpu_arm(args):
                "samples": len(lat), "batch": 1}
     del g1, graph
 
-    roof = dominant_kernel_roofline(be, lvl=6, bsz=min(bsz, 16), peaks=peaks)
+    roof = dominant_kernel_roofline(be, lvl=params.max_level, bsz=bsz, peaks=peaks)
     ks = keyswitch_rate(be, lvl=params.max_level, bsz=min(bsz, 32))
 
     cpu = None
