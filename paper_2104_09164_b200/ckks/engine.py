@@ -591,6 +591,7 @@ class CkksBackend(BackendBase):
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
         perms = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
         late = []   # (job, perm, c0 ptrs) whose Galois gather runs after ModDown
+        natural = {}   # job -> (kb, ka, lmax): inner product reads the digits in natural order
         for j, job in enumerate(jobs):
             key, perm, addend, gather_c0 = job[:4]
             off = job[4] if len(job) > 4 else 0
@@ -608,6 +609,8 @@ class CkksBackend(BackendBase):
                 de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
                 key_stride=(key.lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
                 prime=gidx))
+            if perm is None or prepermuted:
+                natural[j] = (kb_t, ka_t, key.lmax)
             if prepermuted:
                 late.append((j, perm, addend[:, 0] if addend is not None else None))
                 continue
@@ -615,16 +618,16 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        if len(late) == nj and nj >= self.ks_gemm_min and self.ring.use_f64:
-            # one GEMM per digit set (a hoisted group shares it; rot_each jobs
-            # each bring their own)
+        if natural and nj >= self.ks_gemm_min and self.ring.use_f64:
+            # natural-order inner products as one GEMM per digit set (a hoisted
+            # group shares it; rot_each / relinearisation jobs bring their own)
             groups: dict = {}
-            for j, job in enumerate(jobs):
-                groups.setdefault(job[4] if len(job) > 4 else 0, []).append(j)
-            rest = []
+            for j in natural:
+                groups.setdefault(jobs[j][4] if len(jobs[j]) > 4 else 0, []).append(j)
+            rest = [parts[j] for j in range(nj) if j not in natural]
             for off, js in groups.items():
                 if len(js) >= 2 or bsz >= 8:
-                    self._ks_gemm(der, lvl, [jobs[j] for j in js], ipr[js], bsz, off)
+                    self._ks_gemm(der, lvl, [natural[j] for j in js], ipr[js], bsz, off)
                 else:   # a lone small key switch: batch it into one per-job launch
                     rest.extend(parts[j] for j in js)
             if rest:
@@ -700,22 +703,22 @@ class CkksBackend(BackendBase):
                 res[j] = fin[q]
         return res
 
-    def _ks_gemm(self, der, lvl: int, jobs, ipr, bsz: int, off: int):
-        """Inner products of a hoisted group on pre-permuted keys as one
-        per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): the digits of each
-        clip are read once for every rotation of the group, terms = digits,
-        outputs = (rotation, component).  Chain rows and the special row are
-        two launches (the special row's prime and key row differ)."""
+    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, off: int):
+        """Natural-order key-switch inner products of several jobs on one
+        digit set as one per-coefficient GEMM (csrc/mac.cu launch_ks_gemm):
+        the digits of each clip are read once for every job, terms = digits,
+        outputs = (job, component).  keys: (kb, ka, lmax) per job (pre-permuted
+        rotation keys or the relinearisation key).  Chain rows and the special
+        row are two launches (the special row's prime and key row differ)."""
         ndig, rows, n8 = lvl + 1, lvl + 2, np.uint64(8 * self.n)
         dep = der[off, :, 0]                                    # [ndig] row 0 of each digit
         kp, kps, dp = [], [], []
-        for j, job in enumerate(jobs):
-            key = job[0]
-            kst = np.uint64((key.lmax + 2)) * n8
-            for t in (key.bp, key.ap):
+        for j, (kb, ka, lmax) in enumerate(keys):
+            kst = np.uint64(lmax + 2) * n8
+            for t in (kb, ka):
                 base = np.uint64(t.data_ptr()) + np.arange(ndig, dtype=np.uint64) * kst
                 kp.append(base)
-                kps.append(base + np.uint64(key.lmax + 1) * n8)
+                kps.append(base + np.uint64(lmax + 1) * n8)
             dp.extend([ipr[j, 0, 0, 0], ipr[j, 0, 1, 0]])
         kp, kps, dp = np.stack(kp), np.stack(kps), np.array(dp, dtype=np.uint64)
         de_bs, dst_bs = ndig * rows * self.n, 2 * rows * self.n
