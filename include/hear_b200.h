@@ -91,15 +91,19 @@ int hb_mac_strided(hb_ring* ring, const void* outs, int nout, const void* terms,
  * base pointers ([bc, rows, N] ciphertext blocks, [rows, N] plaintexts).     */
 int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* dsts, int nterms,
                   int nout, int rows, int bc, void* stream);
-/* Key-switch inner product of a hoisted rotation group as a per-coefficient
- * modular GEMM (engine.py:305-351, ring.py:136-156, on pre-permuted keys):
- * dsts[o][b*dst_bstride + r*N + j] = sum_i de[i][b*de_bstride + r*N + j] *
- * keys[o*ndig + i][r*N + j] (mod prime_off + r), for o < nout (rotation x
- * component), b < bc, r < rows.  de, keys, dsts: device arrays of row-block
- * base pointers.  fp64 rings only.                                          */
-int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* dsts, int ndig,
-               int nout, int rows, int bc, long long de_bstride, long long dst_bstride,
-               int prime_off, void* stream);
+/* Key-switch inner products in natural digit order (rotations on pre-permuted
+ * keys, relinearisation) as one per-coefficient modular GEMM (engine.py:
+ * 305-351, ring.py:136-156): for o < nout (job x component), b < bc,
+ * r < rows:  dsts[o][b*dst_bstride + r*N + j] =
+ *   sum_i de[i][b*de_bstride + r*N + j] * K[o*ndig + i][j]   (mod q_r)
+ * with K = keys[..] + r*N for r < rows-1 and K = keys_last[..] (the key's
+ * special row) and the special prime prime_last for r = rows-1.  de is
+ * [ndig] row-block base pointers shared by every job, or [nout/2][ndig]
+ * (each job its own digits) when de_per_job.  Pointer tables live in device
+ * memory.  fp64 rings only.                                                 */
+int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* keys_last,
+               const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
+               long long dst_bstride, int prime_last, int de_per_job, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);

@@ -619,17 +619,13 @@ class CkksBackend(BackendBase):
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
         if natural and nj >= self.ks_gemm_min and self.ring.use_f64:
-            # natural-order inner products as one GEMM per digit set (a hoisted
-            # group shares it; rot_each / relinearisation jobs bring their own)
-            groups: dict = {}
-            for j in natural:
-                groups.setdefault(jobs[j][4] if len(jobs[j]) > 4 else 0, []).append(j)
+            # every natural-order inner product in ONE GEMM launch: a hoisted
+            # group shares its digit set, rot_each / relinearisation jobs bring
+            # their own (one output pair per tile)
+            js = sorted(natural)
+            offs = [jobs[j][4] if len(jobs[j]) > 4 else 0 for j in js]
+            self._ks_gemm(der, lvl, [natural[j] for j in js], ipr[js], bsz, offs)
             rest = [parts[j] for j in range(nj) if j not in natural]
-            for off, js in groups.items():
-                if len(js) >= 2 or bsz >= 8:
-                    self._ks_gemm(der, lvl, [natural[j] for j in js], ipr[js], bsz, off)
-                else:   # a lone small key switch: batch it into one per-job launch
-                    rest.extend(parts[j] for j in js)
             if rest:
                 self.ring.ks_inner2(np.concatenate(rest), bsz)
         else:
@@ -703,15 +699,15 @@ class CkksBackend(BackendBase):
                 res[j] = fin[q]
         return res
 
-    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, off: int):
-        """Natural-order key-switch inner products of several jobs on one
-        digit set as one per-coefficient GEMM (csrc/mac.cu launch_ks_gemm):
-        the digits of each clip are read once for every job, terms = digits,
-        outputs = (job, component).  keys: (kb, ka, lmax) per job (pre-permuted
-        rotation keys or the relinearisation key).  Chain rows and the special
-        row are two launches (the special row's prime and key row differ)."""
+    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
+        """Natural-order key-switch inner products of several jobs as one
+        per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): terms = digits,
+        outputs = (job, component), the special row (its own prime and key
+        row) as the launch's last row.  keys: (kb, ka, lmax) per job
+        (pre-permuted rotation keys or the relinearisation key); offs: the
+        digit set (clip offset into de) of each job -- shared by a hoisted
+        group, else one per job."""
         ndig, rows, n8 = lvl + 1, lvl + 2, np.uint64(8 * self.n)
-        dep = der[off, :, 0]                                    # [ndig] row 0 of each digit
         kp, kps, dp = [], [], []
         for j, (kb, ka, lmax) in enumerate(keys):
             kst = np.uint64(lmax + 2) * n8
@@ -721,10 +717,12 @@ class CkksBackend(BackendBase):
                 kps.append(base + np.uint64(lmax + 1) * n8)
             dp.extend([ipr[j, 0, 0, 0], ipr[j, 0, 1, 0]])
         kp, kps, dp = np.stack(kp), np.stack(kps), np.array(dp, dtype=np.uint64)
-        de_bs, dst_bs = ndig * rows * self.n, 2 * rows * self.n
-        self.ring.ks_gemm(dep, kp, dp, lvl + 1, bsz, de_bs, dst_bs, 0)
-        sp = np.uint64(lvl + 1) * n8
-        self.ring.ks_gemm(dep + sp, kps, dp + sp, 1, bsz, de_bs, dst_bs, self.S)
+        if len(set(offs)) == 1:
+            dep = der[offs[0], :, 0]                    # [ndig] row 0 of each digit
+        else:
+            dep = np.stack([der[o, :, 0] for o in offs])   # [njobs, ndig]
+        self.ring.ks_gemm(dep, kp, kps, dp, rows, bsz, ndig * rows * self.n,
+                          2 * rows * self.n, self.S)
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)

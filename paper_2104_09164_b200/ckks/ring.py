@@ -229,19 +229,23 @@ class RingContext:
         """Modular arithmetic on the fp64 pipe (csrc/cabi.cu policy)."""
         return bool(self._lib.hb_ring_uses_f64(self.handle))
 
-    def ks_gemm(self, de: np.ndarray, keys: np.ndarray, dsts: np.ndarray, rows: int, bc: int,
-                de_bstride: int, dst_bstride: int, prime_off: int):
-        """Hoisted-group key-switch inner product as a per-coefficient GEMM:
-        dsts[o] = sum_i keys[o, i] * de[i] over [bc] clip blocks of rows rows."""
+    def ks_gemm(self, de: np.ndarray, keys: np.ndarray, keys_last: np.ndarray, dsts: np.ndarray,
+                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int):
+        """Natural-order key-switch inner products as one per-coefficient GEMM
+        (csrc/mac.cu launch_ks_gemm): de [ndig] shared or [njobs, ndig] per job,
+        keys / keys_last [nout, ndig], dsts [nout]."""
         nout, ndig = keys.shape
         if nout:
-            buf = _upload(np.concatenate([de.ravel(), keys.ravel(), dsts.ravel()])
-                          .astype(np.uint64), self.device)
+            per_job = int(de.ndim == 2)
+            buf = _upload(np.concatenate([de.ravel(), keys.ravel(), keys_last.ravel(),
+                                          dsts.ravel()]).astype(np.uint64), self.device)
             base = _ptr(buf)
-            nat.check(self._lib.hb_ks_gemm(self.handle, base, base + 8 * ndig,
-                                           base + 8 * (ndig + nout * ndig), ndig, nout, rows, bc,
-                                           de_bstride, dst_bstride, prime_off, self.stream),
-                      "ks_gemm")
+            o1 = base + 8 * de.size
+            o2 = o1 + 8 * keys.size
+            o3 = o2 + 8 * keys.size
+            nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
+                                           de_bstride, dst_bstride, prime_last, per_job,
+                                           self.stream), "ks_gemm")
 
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):

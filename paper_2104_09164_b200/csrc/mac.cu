@@ -30,7 +30,10 @@ struct HbMacGroupP {
   int nout;
   long long ct_bstride;   // elements between clips of a ct / dst block
   long long dst_bstride;
-  int prime_off;          // prime of row r = prime_off + r
+  int prime_off;          // prime of row r = prime_off + r ...
+  const u64* const* pts_last;   // ... except the last row when set: its pt rows
+  int prime_last;               //     (pointers to the row itself) and prime
+  int cts_per_tile;       // cts is [output tile][T] (each tile has its own terms)
 };
 
 namespace {
@@ -64,20 +67,24 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   const int T = g.nterms, O = g.nout, n = RG.n;
   const int tid = threadIdx.x + threadIdx.y * 32;
   const int oc = blockIdx.y * OB, bc = blockIdx.x * CB;   // CTA tile origin
-  // pointer tables of this CTA's tile: ct bases [T], pt bases [OB][T]
-  for (int i = tid; i < T * (1 + OB); i += 256) {
-    if (i < T) {
-      ptab[i] = g.cts[i];
-    } else {
-      const int o = (i - T) / T, t = (i - T) % T;
-      ptab[i] = g.pts[(size_t)(oc + o < O ? oc + o : O - 1) * T + t];
-    }
-  }
-  __syncthreads();
   const int nchunk = n / 32;
   const int r = blockIdx.z / nchunk;
   const int j0 = (blockIdx.z % nchunk) * 32;
   const size_t rj0 = (size_t)r * n + j0;
+  const bool last = g.pts_last != nullptr && r == R - 1;
+  const u64* const* pts = last ? g.pts_last : g.pts;
+  const size_t prow = last ? (size_t)j0 : rj0;            // pt offset of this row
+  // pointer tables of this CTA's tile: ct bases [T], pt bases [OB][T]
+  const u64* const* cts = g.cts + (g.cts_per_tile ? (size_t)blockIdx.y * T : 0);
+  for (int i = tid; i < T * (1 + OB); i += 256) {
+    if (i < T) {
+      ptab[i] = cts[i];
+    } else {
+      const int o = (i - T) / T, t = (i - T) % T;
+      ptab[i] = pts[(size_t)(oc + o < O ? oc + o : O - 1) * T + t];
+    }
+  }
+  __syncthreads();
   // copy plan: chunk c -> stage row c/16 (ct rows first), 16-byte part c%16
   auto issue = [&](int t) {
     const uint32_t sb = s_addr(stages + (t % S) * STAGE);
@@ -91,7 +98,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
           const int b = bc + row < BC ? bc + row : BC - 1;
           src = ptab[t] + (size_t)b * g.ct_bstride + rj0 + part * 2;
         } else {
-          src = ptab[T + (row - CB) * T + t] + rj0 + part * 2;
+          src = ptab[T + (row - CB) * T + t] + prow + part * 2;
         }
         cp16(sb + (uint32_t)(row * 32 + part * 2) * 8u, src);
       }
@@ -104,7 +111,8 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   }
   const int lane = threadIdx.x, w = threadIdx.y;
   const int os = (w / WB) * TO, bs = (w % WB) * TB;   // warp sub-tile in the CTA tile
-  const HbPrime P = RG.primes[g.prime_off + r];
+  const int prime = last ? g.prime_last : g.prime_off + r;
+  const HbPrime P = RG.primes[prime];
   const double p = P.pd, pinv = P.pinv;
   const int wbits = RG.chunk_w, fold = RG.chunk_fold;
   const u64 mask = (1ull << wbits) - 1;
@@ -170,7 +178,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   double cc[4] = {0, 0, 0, 0};
   if constexpr (C3) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * (g.prime_off + r) + k);
+    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * prime + k);
   }
   const size_t rj = rj0 + lane;
 #pragma unroll
@@ -211,7 +219,9 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
     if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
     return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
   }
-  if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
+  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
+  // one (b, a) output pair per tile when every job brings its own digits
+  if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   // output tile sized to the layer so no warp idles on absent outputs
   if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
@@ -232,16 +242,23 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
   g.nout = nout;
   g.ct_bstride = g.dst_bstride = (long long)rows * RG.n;
   g.prime_off = 0;
+  g.pts_last = nullptr;
+  g.prime_last = 0;
+  g.cts_per_tile = 0;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
-// Key-switch inner product of a hoisted rotation group on pre-permuted keys
-// (engine.py:305-351 / ring.py:136-156 with the Galois gather moved after
-// ModDown): terms = digits, outputs = (rotation, component), clips = BC.
-// Row r of the launch runs in prime prime_off + r; clip strides explicit.
-cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* dsts, int ndig, int nout,
-                           const HbRing& RG, int rows, int BC, long long de_bstride,
-                           long long dst_bstride, int prime_off, cudaStream_t st) {
+// Key-switch inner products in natural digit order as one per-coefficient
+// GEMM (engine.py:305-351 / ring.py:136-156; rotations on pre-permuted keys
+// with the Galois map applied after ModDown, and relinearisation): terms =
+// digits, outputs = (job, component), clips = BC, rows 0..rows-2 in chain
+// primes 0..rows-2 and the last row in prime_last with its own key rows
+// (keys_last).  de_per_job: de is [job][ndig] (each job its own digits,
+// one output pair per tile) instead of [ndig] shared by every job.
+cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_last,
+                           const void* dsts, int ndig, int nout, const HbRing& RG, int rows,
+                           int BC, long long de_bstride, long long dst_bstride, int prime_last,
+                           int de_per_job, cudaStream_t st) {
   if (nout <= 0 || ndig <= 0) return cudaSuccess;
   if (!RG.use_f64) return cudaErrorNotSupported;
   HbMacGroupP g;
@@ -252,7 +269,10 @@ cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* dsts, i
   g.nout = nout;
   g.ct_bstride = de_bstride;
   g.dst_bstride = dst_bstride;
-  g.prime_off = prime_off;
+  g.prime_off = 0;
+  g.pts_last = reinterpret_cast<const u64* const*>(keys_last);
+  g.prime_last = prime_last;
+  g.cts_per_tile = de_per_job;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
