@@ -130,9 +130,10 @@ class CkksBackend(BackendBase):
         # is one GEMM over digits x (rotation, component) and the Galois map is
         # applied by the ModDown scatter; bit-identical, 2x rotation-key memory
         self.preperm = os.environ.get("HEAR_B200_PREPERM", "1") == "1"
-        # key switches of at least this many pre-permuted rotations take the
-        # GEMM inner product (ks_gemm) instead of the per-job kernel (ks_inner2)
-        self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "1"))
+        # batched key switches of at least this many clips take the GEMM inner
+        # product (ks_gemm); smaller ones the per-job kernel (ks_inner2), which
+        # has the lower latency at one or two clips
+        self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "8"))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -618,7 +619,7 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        if natural and nj >= self.ks_gemm_min and self.ring.use_f64:
+        if natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
             # every natural-order inner product in ONE GEMM launch: a hoisted
             # group shares its digit set, rot_each / relinearisation jobs bring
             # their own (one output pair per tile)

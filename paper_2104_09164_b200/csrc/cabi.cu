@@ -328,7 +328,9 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
   const char* old = getenv("HEAR_B200_MAC_SHARED");
   const char* pipe = getenv("HEAR_B200_MAC_PIPE");   // "0": register-prefetch kernels
   cudaError_t e = cudaErrorNotSupported;
-  if (r->dev.use_f64 && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
+  // the cp.async pipeline pays off once a layer has several clips per launch;
+  // one or two clip-components run the register-prefetch kernel (lower latency)
+  if (r->dev.use_f64 && bc >= 8 && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
     e = launch_mac_pipe(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) (void)cudaGetLastError();   // term table too large
   }

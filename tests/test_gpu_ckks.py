@@ -204,8 +204,9 @@ def test_prepermuted_rotation_keys_bit_exact(golden, preperm):
 _ORACLE = {}
 
 
-@pytest.mark.parametrize("env", [{}, {"HEAR_B200_KS_GEMM_MIN": "1000"}, {"HEAR_B200_PREPERM": "0"},
-                                 {"HEAR_B200_NTT3": "0"}])
+@pytest.mark.parametrize("env", [{"HEAR_B200_KS_GEMM_MIN": "1"}, {"HEAR_B200_KS_GEMM_MIN": "1000"},
+                                 {"HEAR_B200_PREPERM": "0"},
+                                 {"HEAR_B200_NTT3": "0", "HEAR_B200_KS_GEMM_MIN": "1"}])
 def test_hoisted_rotations_fast_hear_vs_oracle(env):
     """N = 2^14 hoisted rotations (cluster NTT, GEMM inner product on
     pre-permuted keys, ModDown scatter) against the CPU oracle, for every
@@ -245,3 +246,44 @@ def test_hoisted_rotations_fast_hear_vs_oracle(env):
                 del os.environ[k]
             else:
                 os.environ[k] = v
+
+
+@pytest.mark.parametrize("gemm_min", ["1", "1000"])
+def test_rot_each_and_relin_batched_vs_oracle(gemm_min):
+    """Batched key switches with a digit set per job (rot_each over several
+    handles: one GEMM launch, one output pair per tile) and relinearisation,
+    GEMM and per-job inner products, against the CPU oracle at N = 2^14."""
+    import os
+    from oracle.cpu_engine import OracleCkks
+    from paper_2104_09164_b200.backend import Ct
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    ps = gen_params("fast-hear")
+    amounts = [1, 5]
+    if "cpu" not in _ORACLE:
+        cpu = OracleCkks(ps, seed=11)
+        cpu.ensure_rotation_keys({a: 12 for a in [1, 5, 77, 4000]})
+        _ORACLE["cpu"] = cpu
+    cpu = _ORACLE["cpu"]
+    os.environ["HEAR_B200_KS_GEMM_MIN"] = gemm_min
+    try:
+        gpu = CkksBackend(ps, seed=11)
+    finally:
+        del os.environ["HEAR_B200_KS_GEMM_MIN"]
+    gpu.ensure_rotation_keys({a: 12 for a in amounts})
+    lvl = 9
+    cts = [[rand_ct(ps, lvl, 70 + 3 * h + i) for i in range(2)] for h in range(2)]
+    hs = [gpu.import_ct(np.stack([c[0] for c in hc]), np.stack([c[1] for c in hc]), lvl,
+                        ps.msg_scale) for hc in cts]
+    outs = gpu._raw_rot_each([(hs[0], amounts[0]), (hs[1], amounts[1])])
+    for h, (o, a) in enumerate(zip(outs, amounts)):
+        r = gpu.export(o)
+        for i, c in enumerate(cts[h]):
+            want = cpu._raw_rot(Ct(c, lvl, Fraction(ps.msg_scale), ps.n2), a).payload
+            assert np.array_equal(r[0][i], want[0]) and np.array_equal(r[1][i], want[1]), (h, i)
+    m = gpu.export(gpu._raw_mult(hs[0], hs[1]))
+    for i in range(2):
+        A = Ct(cts[0][i], lvl, Fraction(ps.msg_scale), ps.n2)
+        B = Ct(cts[1][i], lvl, Fraction(ps.msg_scale), ps.n2)
+        want = cpu._raw_mult(A, B).payload
+        assert np.array_equal(m[0][i], want[0]) and np.array_equal(m[1][i], want[1]), i

@@ -1,8 +1,14 @@
+#!/bin/bash
+# Round profiling pass (GPU box): launch list of one eager 1d-w64 step and
+# ncu --set full captures of the top kernels.  Summaries: tools/ncu_summary.py
 set -x
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active
-timeout 300 python tools/layer_times.py 1d-w64 full 64 > gpurun_out/layers.txt 2>&1
+python tools/step_profile.py 1d-w64 full 64 > gpurun_out/sp.log 2>&1 || exit 1
 timeout 900 ncu --profile-from-start off --metrics $M --clock-control none --csv --log-file gpurun_out/launches_b64.csv python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_list.log 2>&1
-for k in k_ntt2_blocks k_ntt2_cols k_ks_inner2 k_mac_gemm; do
-timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:$k --launch-skip 40 -c 1 -o gpurun_out/full_$k python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_full_$k.log 2>&1
-done
-ls -la gpurun_out
+python tools/roofline_probe.py > gpurun_out/roof.log 2>&1 && \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ntt3 -s 3 -c 1 -o gpurun_out/full_roofline python tools/roofline_probe.py > gpurun_out/ncu_roof.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_ntt3_fwd<hb::PolF64, .int.14, .int.1>" -s 4 -c 1 -o gpurun_out/full_lift python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_lift.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:k_ntt3_inv -s 8 -c 1 -o gpurun_out/full_inv python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_inv.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.4, .int.4, .int.4" -s 6 -c 1 -o gpurun_out/full_ksgemm python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_ksg.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.4, .int.4, .int.2" -s 0 -c 1 -o gpurun_out/full_mac python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_mac.log 2>&1
+ls gpurun_out
