@@ -382,8 +382,10 @@ def gpu_arm(args):
                "samples": len(lat), "batch": 1}
     del g1, graph
 
-    roof = dominant_kernel_roofline(be, lvl=params.max_level, bsz=bsz, peaks=peaks)
-    ks = keyswitch_rate(be, lvl=params.max_level, bsz=min(bsz, 32))
+    roof = ks = None
+    if rank == 0:   # per-GPU kernel figures; the other ranks hold no secret key
+        roof = dominant_kernel_roofline(be, lvl=params.max_level, bsz=bsz, peaks=peaks)
+        ks = keyswitch_rate(be, lvl=params.max_level, bsz=min(bsz, 32))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

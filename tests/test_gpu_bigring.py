@@ -1,6 +1,7 @@
-"""N = 2^15 / 2^16 rings (BASELINE's microbench and batched configs): the
-two-pass NTT and a key switch on both arithmetic policies (fp64 pipe for
-primes < 2^42, 64-bit Shoup for the 50/60-bit primes) against the CPU oracle."""
+"""N = 2^13 / 2^15 / 2^16 rings (BASELINE's microbench and batched configs,
+and the cluster NTT's 2-CTA variant at 2^13): the NTT and a key switch on
+both arithmetic policies (fp64 pipe for primes < 2^42, 64-bit Shoup for the
+50/60-bit primes) against the CPU oracle."""
 
 from fractions import Fraction
 
@@ -12,8 +13,8 @@ from tests._util import rand_ct, rand_rows
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("logn,bits,special", [(15, [30, 28, 28], 30), (16, [50, 50, 50], 60),
-                                               (16, [36, 33, 33], 36)])
+@pytest.mark.parametrize("logn,bits,special", [(13, [33, 30, 30], 33), (15, [30, 28, 28], 30),
+                                               (16, [50, 50, 50], 60), (16, [36, 33, 33], 36)])
 def test_ntt_and_keyswitch_vs_oracle(logn, bits, special):
     import torch
     from oracle.cpu_engine import OracleCkks
