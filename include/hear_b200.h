@@ -60,12 +60,17 @@ int hear_pw_sub(hb_ring* ring, unsigned long long* out, const unsigned long long
                 const unsigned long long* b, int nrows, const long long* gidx);
 
 /* ---- device task-table kernels --------------------------------------------- */
-/* Forward NTT over `count` row tasks (HbNttTask).  mode 0: plain
- * (ring.py:113); 1: fused centred lift + reduce of a digit row, the ModUp of
- * engine.py:290-303 (ring.py:186-207 + 113); 2: ModUp + sub_scaled_inv +
- * optional Galois-gathered addend, the ModDown / rescale of
+/* Forward NTT over `count` row tasks (HbNttTask, csrc/ring.cuh).  mode 0:
+ * plain (ring.py:113); 1: fused centred lift + reduce of a digit row, the
+ * ModUp of engine.py:290-303 (ring.py:186-207 + 113); 2: ModUp +
+ * sub_scaled_inv + optional Galois-gathered addend, the ModDown / rescale of
  * engine.py:213-227, 263-281, 350; 3: signed int64 coefficients
- * (engine.py:84-88 _coeffs_to_ntt). */
+ * (engine.py:84-88 _coeffs_to_ntt); 4: mode 2 for a rotation computed on
+ * pre-permuted keys, the result scattered through the inverse Galois map
+ * (perm) and the addend read in natural order.  Modes 2/4 add the optional
+ * post-addend `add2` at the destination index (the add of rotate-and-sum,
+ * fastpath.py rot-add, fused).  Clusters of N/4096 CTAs on fp64 rings at
+ * N = 2^13 / 2^14 (csrc/ntt3.cu), else two-pass (csrc/ntt2.cu). */
 int hb_ntt_fwd(hb_ring* ring, const void* tasks, int count, int mode, void* stream);
 /* Inverse NTT over row tasks (ring.py:120, true inverse twiddles).            */
 int hb_ntt_inv(hb_ring* ring, const void* tasks, int count, void* stream);

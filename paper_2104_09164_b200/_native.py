@@ -89,7 +89,7 @@ def check(rc: int, what: str, kernels: int = 1):
 # ---- task-table layouts (csrc/ring.cuh) -------------------------------------
 
 NTT_TASK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("aux", "<u8"), ("add", "<u8"),
-                     ("perm", "<u8"), ("scal", "<u8"), ("scal_sh", "<u8"),
+                     ("perm", "<u8"), ("scal", "<u8"), ("scal_sh", "<u8"), ("add2", "<u8"),
                      ("src_prime", "<i4"), ("dst_prime", "<i4")])
 EW_TASK = np.dtype([("dst", "<u8"), ("a", "<u8"), ("b", "<u8"), ("c", "<u8"),
                     ("scal", "<u8"), ("scal_sh", "<u8"), ("prime", "<i4"), ("_pad", "<i4")])

@@ -632,6 +632,13 @@ class CkksBackend(BackendBase):
         else:
             self.ring.ks_inner2(np.concatenate(parts), bsz)
         m, r = nj * bsz * 2, lvl + 1
+        # optional post-addend per job (job[5]: row pointers [bsz, 2, lvl+1]),
+        # added in the ModDown epilogue at the destination index
+        post = np.zeros((nj, bsz, 2, r), dtype=np.uint64)
+        for j, job in enumerate(jobs):
+            if len(job) > 5 and job[5] is not None:
+                post[j] = job[5]
+        has_post = bool(post.any())
         iprows = rp(ip).reshape(m, rows)
         spc = self.ring.empty(m)
         sprime = np.full(m, self.S)
@@ -653,7 +660,7 @@ class CkksBackend(BackendBase):
                        aux=iprows[:, :r].ravel(),
                        src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
                        scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
-                       add=addn.ravel(), perm=inv.ravel())
+                       add=addn.ravel(), perm=inv.ravel(), add2=post.ravel())
             self.ring.ntt_fwd(t, nat.FWD_MODDOWN_SCATTER)
             out = out.reshape(nj, bsz, 2, r, self.n)
             return [out[j] for j in range(nj)]
@@ -661,7 +668,8 @@ class CkksBackend(BackendBase):
                    aux=iprows[:, :r].ravel(),
                    src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
                    scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
-                   add=add.ravel(), perm=perms.ravel())
+                   add=add.ravel(), perm=perms.ravel(),
+                   add2=(post.ravel() if has_post and not late else 0))
         self.ring.ntt_fwd(t, nat.FWD_MODDOWN)
         out = out.reshape(nj, bsz, 2, r, self.n)
         res = [out[j] for j in range(nj)]
@@ -698,6 +706,12 @@ class CkksBackend(BackendBase):
                 b=np.concatenate(p1), prime=np.tile(np.arange(r), nrow // r)))
             for q, (j, _, _) in enumerate(late):
                 res[j] = fin[q]
+            if has_post:   # gather after ModDown here: the post-addend follows it
+                for j in range(nj):
+                    if post[j].any():
+                        dst = rp(res[j]).reshape(bsz, 2, r)
+                        self._ew(nat.EW_ADD, dst.ravel(), dst.ravel(), post[j].ravel(),
+                                 primes=np.tile(np.arange(r), bsz * 2))
         return res
 
     def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
@@ -867,6 +881,30 @@ class CkksBackend(BackendBase):
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
                     jobs.append((key, perm, add, g, q * bsz))
+                res = self._ks_apply_many(de, lvl, jobs, bsz)
+                del de
+                for q, i in enumerate(chunk):
+                    ct = items[i][0]
+                    out[i] = Ct(CtData(res[q]), lvl, ct.scale, self.n2)
+        return out
+
+    def _raw_rot_add_each(self, items) -> list:
+        """[ct + rot(ct, k)] with the add fused into the rotation's ModDown
+        epilogue (post-addend at the destination index): bit-identical to
+        add(ct, rot(ct, k)) (modular addition), one kernel fewer per item."""
+        out = [None] * len(items)
+        for lvl, idx in self._by_level(items, lambda it: it[0].level).items():
+            bsz = items[idx[0]][0].payload.batch
+            step = self._ks_chunk(bsz, lvl)
+            for c0 in range(0, len(idx), step):
+                chunk = idx[c0:c0 + step]
+                rows = [self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)
+                        for i in chunk]
+                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl)
+                jobs = []
+                for q, i in enumerate(chunk):
+                    key, perm, add, g = self._rot_job(*items[i])
+                    jobs.append((key, perm, add, g, q * bsz, rows[q]))
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de
                 for q, i in enumerate(chunk):

@@ -113,6 +113,7 @@ HB_DEV void ntt_fwd_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P)
         const int src = tk.perm ? __ldg(tk.perm + j) : j;
         v = add_mod(v, __ldg(tk.add + src), p);
       }
+      if (tk.add2) v = add_mod(v, __ldg(tk.add2 + j), p);
     }
     tk.dst[j] = v;
   }

@@ -288,6 +288,12 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
             o.x = add_mod(o.x, ad[2 * v], p);
             o.y = add_mod(o.y, ad[2 * v + 1], p);
           }
+          if (tk.add2) {   // post-addend at the destination index
+            const size_t d0 = MODE == FWD_MODDOWN_SCATTER ? (size_t)sc[v].x : j;
+            const size_t d1 = MODE == FWD_MODDOWN_SCATTER ? (size_t)sc[v].y : j + 1;
+            o.x = add_mod(o.x, __ldg(tk.add2 + d0), p);
+            o.y = add_mod(o.y, __ldg(tk.add2 + d1), p);
+          }
         }
         if (MODE == FWD_MODDOWN_SCATTER) {
           tk.dst[sc[v].x] = o.x;

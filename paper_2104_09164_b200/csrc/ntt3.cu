@@ -316,6 +316,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     const size_t j = base + 2 * k;
     const int pc = swz3_chunk(k);
     ulonglong2 o;
+    int2 sc = make_int2(0, 0);
     if (MD) {
       const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
       double r0 = fmod_mul(u64_to_f(ax.x) - rb[2 * pc], sd, sq, pd);
@@ -334,6 +335,17 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         r0 += u64_to_f(a0);
         r1 += u64_to_f(a1);
       }
+      if (tk.add2) {   // post-addend at the destination index
+        if (MODE == FWD_MODDOWN_SCATTER) {
+          sc = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+          r0 += u64_to_f(__ldg(tk.add2 + sc.x));
+          r1 += u64_to_f(__ldg(tk.add2 + sc.y));
+        } else {
+          const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add2 + j));
+          r0 += u64_to_f(a2.x);
+          r1 += u64_to_f(a2.y);
+        }
+      }
       o.x = fmod_canon(r0, pd, pinv);
       o.y = fmod_canon(r1, pd, pinv);
     } else {
@@ -341,7 +353,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       o.y = (u64)__double_as_longlong(rb[2 * pc + 1]);
     }
     if (MODE == FWD_MODDOWN_SCATTER) {
-      const int2 sc = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
+      if (!tk.add2) sc = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
       tk.dst[sc.x] = o.x;
       tk.dst[sc.y] = o.y;
     } else {

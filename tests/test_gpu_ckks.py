@@ -287,3 +287,36 @@ def test_rot_each_and_relin_batched_vs_oracle(gemm_min):
         B = Ct(cts[1][i], lvl, Fraction(ps.msg_scale), ps.n2)
         want = cpu._raw_mult(A, B).payload
         assert np.array_equal(m[0][i], want[0]) and np.array_equal(m[1][i], want[1]), i
+
+
+@pytest.mark.parametrize("env", [{"HEAR_B200_KS_GEMM_MIN": "1"}, {"HEAR_B200_PREPERM": "0"},
+                                 {"HEAR_B200_NTT3": "0"}])
+def test_fused_rot_add_equals_rot_then_add(env):
+    """ct + rot(ct, k) with the add fused into the ModDown epilogue (scatter,
+    gather and two-pass paths) equals the separate rotation and addition."""
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    ps = gen_params("fast-hear")
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        be = CkksBackend(ps, seed=5)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    be.ensure_rotation_keys({3: 12, 40: 12})
+    lvl = 8
+    cts = [rand_ct(ps, lvl, 90 + i) for i in range(4)]
+    hs = [be.import_ct(np.stack([c[0] for c in cts[2 * h:2 * h + 2]]),
+                       np.stack([c[1] for c in cts[2 * h:2 * h + 2]]), lvl, ps.msg_scale)
+          for h in range(2)]
+    items = [(hs[0], 3), (hs[1], 40)]
+    fused = be.rot_add_each(items)
+    plain = be.add_each(list(zip(hs, be.rot_each(items))))
+    for f, p_ in zip(fused, plain):
+        a, b = be.export(f), be.export(p_)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
