@@ -35,8 +35,9 @@ namespace {
 
 constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
-// local buffer, receive buffer, staged twiddles (ntt3 TW3 x 16 B), 2 mbarriers
-constexpr int SMEM3 = 2 * TILE3 * 8 + 607 * 16 + 16;
+// local buffer, receive buffer, staged twiddles (TW3 x 16 B), 2 mbarriers
+template <int LOGN>
+constexpr int smem3() { return 2 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
 #ifndef HB_NTT3_MINB
 #define HB_NTT3_MINB 3
 #endif
@@ -157,11 +158,10 @@ HB_DEV void col_butterflies(typename Pol::T* x, int rd, int gq, F fetch, const P
 // stages S1..S1+3 / inverse stages 3..6: 32+64+128+256 entries).  Staged
 // once with coalesced loads so the butterflies read them with LDS at
 // (mostly) immediate offsets instead of 64-bit-addressed broadcast LDGs.
-constexpr int TWC = 127, TW3 = TWC + 480;
-
 template <int LOGN, bool FWD>
 HB_DEV void stage_twiddles(HbTwD* tws, const HbTwD* tab, int rank) {
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1;
+  constexpr int TWC = M - 1, TW3 = TWC + 480;
   for (int k = threadIdx.x; k < TW3; k += THREADS3) {
     int idx;
     if (k < TWC) {
@@ -193,6 +193,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
   V* rb = sm + TILE3;                     // received block tile
+  constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
   xchg_init(mbar, TILE3 * sizeof(V));
@@ -373,6 +374,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
   V* rb = sm + TILE3;                     // received column slice
+  constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
   xchg_init(mbar, TILE3 * sizeof(V));
@@ -484,7 +486,7 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * CL);
   cfg.blockDim = dim3(THREADS3);
-  cfg.dynamicSmemBytes = SMEM3;
+  cfg.dynamicSmemBytes = smem3<LOGN>();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -494,7 +496,7 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.attrs = at;
   cfg.numAttrs = 1;
   static int smem_cur = 0;
-  cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(SMEM3), &smem_cur);
+  cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(smem3<LOGN>()), &smem_cur);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_fwd<PolF64, LOGN, MODE>, tasks, R);
 }
@@ -505,7 +507,7 @@ cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * CL);
   cfg.blockDim = dim3(THREADS3);
-  cfg.dynamicSmemBytes = SMEM3;
+  cfg.dynamicSmemBytes = smem3<LOGN>();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -515,7 +517,7 @@ cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.attrs = at;
   cfg.numAttrs = 1;
   static int smem_cur = 0;
-  cudaError_t e = smem_attr_once((const void*)k_ntt3_inv<PolF64, LOGN>, (int)(SMEM3), &smem_cur);
+  cudaError_t e = smem_attr_once((const void*)k_ntt3_inv<PolF64, LOGN>, (int)(smem3<LOGN>()), &smem_cur);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_inv<PolF64, LOGN>, tasks, R);
 }
@@ -543,7 +545,10 @@ bool ntt3_supported(const HbRing& R) {
     const char* v = getenv("HEAR_B200_NTT3");
     off = (v && v[0] == '0') ? 1 : 0;
   }
-  return !off && R.use_f64 && (R.logn == 13 || R.logn == 14);
+  // 2^15 (clusters of 8) compiles and is exact, but at 77 KB of shared memory
+  // per CTA only two CTAs fit an SM and it measured 5-20 % slower than the
+  // two-pass kernels (tools/ntt_modes.py, NTT_MODES_LOGN=15): not selected
+  return !off && R.use_f64 && R.logn >= 13 && R.logn <= 14;
 }
 
 cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,
@@ -552,6 +557,7 @@ cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, 
   switch (R.logn) {
     case 13: return fwd3_mode<13>(tasks, count, R, mode, st);
     case 14: return fwd3_mode<14>(tasks, count, R, mode, st);
+    case 15: return fwd3_mode<15>(tasks, count, R, mode, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -561,6 +567,7 @@ cudaError_t launch_ntt3_inv(const HbNttTask* tasks, int count, const HbRing& R, 
   switch (R.logn) {
     case 13: return inv3_t<13>(tasks, count, R, st);
     case 14: return inv3_t<14>(tasks, count, R, st);
+    case 15: return inv3_t<15>(tasks, count, R, st);
     default: return cudaErrorInvalidValue;
   }
 }

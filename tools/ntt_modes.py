@@ -13,7 +13,13 @@ from paper_2104_09164_b200.ckks.ring import _upload
 
 lvl = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 bsz = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-be = CkksBackend(gen_params("fast-hear"), seed=0, keygen=False)
+if os.environ.get("NTT_MODES_LOGN"):   # custom fp64 ring of the same depth at another N
+    from paper_2104_09164_b200.ckks.params import gen_params_custom
+    lg = int(os.environ["NTT_MODES_LOGN"])
+    ps = gen_params_custom(1 << lg, [33] + [31] * 12, 33, 31)
+else:
+    ps = gen_params("fast-hear")
+be = CkksBackend(ps, seed=0, keygen=False)
 ring, n, S = be.ring, be.n, be.S
 rp = ring.row_ptrs
 r = lvl + 1
