@@ -349,15 +349,46 @@ def gpu_arm(args):
     par.barrier()
     ms = par.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
 
-    # ---- end-to-end timed region (host buffers, copies inside)
+    # ---- end-to-end timed region (host buffers, copies inside).  Every step
+    # copies its input from pinned host memory and reads its result back;
+    # the copies run on a side stream double-buffered against the replays
+    # (step s+1's H2D and step s-1's D2H overlap step s's evaluation)
     par.barrier()
     torch.cuda.synchronize()
+    cs = torch.cuda.Stream(device=dev)
+    stage_in = [torch.empty_like(graph.inp) for _ in range(2)]
+    stage_out = [torch.empty_like(graph.out.payload.data) for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(st)
-    for _ in range(args.steps):
-        graph.inp.copy_(host_in, non_blocking=True)
+    cs.wait_stream(st)
+    with torch.cuda.stream(cs):
+        stage_in[0].copy_(host_in, non_blocking=True)
+        ev_in[0].record(cs)
+    for i in range(args.steps):
+        b = i % 2
+        st.wait_event(ev_in[b])
+        graph.inp.copy_(stage_in[b])
+        ev_free[b].record(st)
+        if i + 1 < args.steps:   # next step's input, into the other staging buffer
+            with torch.cuda.stream(cs):
+                if i >= 1:
+                    cs.wait_event(ev_free[1 - b])
+                stage_in[1 - b].copy_(host_in, non_blocking=True)
+                ev_in[1 - b].record(cs)
         graph.graph.replay()
-        host_out.copy_(graph.out.payload.data, non_blocking=True)
+        if i >= 2:   # step i-2's read-back of this staging buffer is done
+            st.wait_event(ev_d2h[b])
+        stage_out[b].copy_(graph.out.payload.data)
+        ev_out[b].record(st)
+        with torch.cuda.stream(cs):
+            cs.wait_event(ev_out[b])
+            host_out.copy_(stage_out[b], non_blocking=True)
+            ev_d2h[b].record(cs)
+    st.wait_stream(cs)
     f1.record(st)
     torch.cuda.synchronize()
     par.barrier()
