@@ -429,6 +429,10 @@ def gpu_arm(args):
             cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(),
                    "kind": "port", "sample": f"failed: {exc}"}
 
+    if rank == 0 and not maxerr <= 2.0 ** -5:
+        # the documented precision of the encrypted network vs the clear one
+        # (DESIGN.md §2); a larger error means a broken kernel: no number
+        raise SystemExit(f"decrypted logits deviate from the clear network by {maxerr}")
     if rank == 0:
         total = bsz * ws
         line = {

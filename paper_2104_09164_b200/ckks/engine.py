@@ -557,8 +557,6 @@ class CkksBackend(BackendBase):
         rp = self.ring.row_ptrs
         coef = self.ring.empty(bsz, ndig)
         prim = self._row_primes(bsz, ndig)
-        self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                 dst_prime=prim, src_prime=prim))
         de = self.ring.empty(bsz, ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         src = np.repeat(rp(coef), rows)
@@ -567,9 +565,12 @@ class CkksBackend(BackendBase):
         dp = np.tile(gidx, bsz * ndig)
         ident = sp == np.tile(np.tile(np.arange(rows), ndig), bsz)
         lift = ~ident
+        # the inverse transform also copies each input row to its identity
+        # digit position of de (add2), so no separate copy launch
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                 dst_prime=prim, src_prime=prim, add2=dst[ident]))
         self.ring.ntt_fwd(_tasks(nat.NTT_TASK, int(lift.sum()), src=src[lift], dst=dst[lift],
                                  src_prime=sp[lift], dst_prime=dp[lift]), nat.FWD_LIFT)
-        self._ew(nat.EW_COPY, dst[ident], ptrs.ravel(), primes=prim)
         return de
 
     def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None) -> list:

@@ -182,7 +182,11 @@ HB_DEV void ntt_inv_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P)
   const typename Pol::Tw* tw = Pol::inv_table(R, tk.dst_prime);
   const int g = threadIdx.x;
 #pragma unroll 4
-  for (int j = g; j < N; j += T) sm[sw(j)] = pol.from_canon(__ldg(tk.src + j));
+  for (int j = g; j < N; j += T) {
+    const u64 v = __ldg(tk.src + j);
+    if (tk.add2) const_cast<u64*>(tk.add2)[j] = v;   // inverse: verbatim copy of the input row
+    sm[sw(j)] = pol.from_canon(v);
+  }
   __syncthreads();
   {  // round 0: stages 0..3 on contiguous 16-element groups
     V x[16];

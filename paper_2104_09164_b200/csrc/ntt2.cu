@@ -314,6 +314,8 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const ulonglong2 in = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base + e0) + v);
+        if (tk.add2)   // inverse: verbatim copy of the input row
+          reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base + e0)[v] = in;
         x[2 * v] = pol.from_canon(in.x);
         x[2 * v + 1] = pol.from_canon(in.y);
       }

@@ -396,6 +396,8 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
     const int k = t + i * THREADS3;
     const ulonglong2 in = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base) + k);
+    if (tk.add2)   // inverse: verbatim copy of the input row (ModUp identity digit)
+      reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base)[k] = in;
     const int pc = swz3_chunk(k);
     sm[2 * pc] = pol.from_canon(in.x);
     sm[2 * pc + 1] = pol.from_canon(in.y);

@@ -61,9 +61,11 @@ struct HbNttTask {
   const int* perm;  // optional automorphism gather for `add`
   u64 scal;         // epilogue constant (P^-1 / q_l^-1 mod p_dst)
   u64 scal_sh;
-  const u64* add2;  // optional ModDown post-addend, read at the destination
-                    // index (after the Galois gather / scatter): fuses the
-                    // "ct + rot(ct)" add of rotate-and-sum into the epilogue
+  const u64* add2;  // forward ModDown: optional post-addend, read at the
+                    // destination index (after the Galois gather / scatter):
+                    // fuses the "ct + rot(ct)" add of rotate-and-sum.
+                    // inverse: optional second destination receiving the
+                    // input row verbatim (the ModUp identity digit row)
   int src_prime;    // prime of src when it differs from dst_prime (lift)
   int dst_prime;    // prime the transform runs in
 };
