@@ -626,7 +626,17 @@ class CkksBackend(BackendBase):
             # their own (one output pair per tile)
             js = sorted(natural)
             offs = [jobs[j][4] if len(jobs[j]) > 4 else 0 for j in js]
-            self._ks_gemm(der, lvl, [natural[j] for j in js], ipr[js], bsz, offs)
+            keys = [natural[j] for j in js]
+            same_key = all(k[0].data_ptr() == keys[0][0].data_ptr() for k in keys)
+            stacked = (js == list(range(js[0], js[0] + len(js)))
+                       and offs == [offs[0] + q * bsz for q in range(len(js))])
+            if len(js) > 1 and same_key and stacked:
+                # one key over consecutive handles (rotate-and-sum by one amount,
+                # relinearisation of a layer): their digits and outputs are
+                # contiguous, so it is one (b, a) GEMM over all their clips
+                self._ks_gemm(der, lvl, keys[:1], ipr[js[:1]], bsz * len(js), offs[:1])
+            else:
+                self._ks_gemm(der, lvl, keys, ipr[js], bsz, offs)
             rest = [parts[j] for j in range(nj) if j not in natural]
             if rest:
                 self.ring.ks_inner2(np.concatenate(rest), bsz)
