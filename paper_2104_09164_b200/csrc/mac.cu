@@ -18,6 +18,7 @@
 // (6 ops, balanced residue) or, when the ring enables chunked dot products,
 // as three exact DFMAs against w-bit limbs of ct (dot.cu).
 #include <cstdint>
+#include <cstdlib>
 #include "ring.cuh"
 
 namespace hb {
@@ -226,7 +227,17 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
-  return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+  static int tile = -1;   // HEAR_B200_GEMM_TILE: experiment knob for the wide tiles
+  if (tile < 0) {
+    const char* v = getenv("HEAR_B200_GEMM_TILE");
+    tile = v ? atoi(v) : 0;
+  }
+  if (tile == 48) return mac_pipe_t<4, 8, 4, 2, false, 4>(g, RG, rows, BC, st);
+  if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+  // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
+  // operand feeds twice the products of the 4x4 tile; measured +1.6 % on
+  // the bench step (hoisted key-switch GEMM and conv MAC)
+  return mac_pipe_t<8, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
 }
 
 // fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
