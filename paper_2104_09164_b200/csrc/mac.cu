@@ -226,11 +226,14 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   // output tile sized to the layer so no warp idles on absent outputs
   if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
-  if (g.nout <= 8) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
   static int tile = -1;   // HEAR_B200_GEMM_TILE: experiment knob for the wide tiles
   if (tile < 0) {
     const char* v = getenv("HEAR_B200_GEMM_TILE");
     tile = v ? atoi(v) : 0;
+  }
+  if (g.nout <= 8) {
+    if (tile == 44) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
+    return mac_pipe_t<8, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
   }
   if (tile == 48) return mac_pipe_t<4, 8, 4, 2, false, 4>(g, RG, rows, BC, st);
   if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
