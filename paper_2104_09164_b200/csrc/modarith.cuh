@@ -37,24 +37,29 @@ struct HbPrime {
 //
 // Residues are integer-valued doubles in a balanced range; a product a*w is
 // split error-free into hi + lo (hi = fl(aw), lo = fma(a, w, -hi)), the
-// quotient q = round(a * fl(w/p)) comes from one fma against 1.5*2^52, and
+// quotient q = rint(fl(a * fl(w/p))) (below), and
 // r = fma(-q, p, hi) + lo is computed exactly (all intermediate integers are
 // below 2^53), giving r = a*w mod p with |r| <= (1/2 + 2^-7) p for any
-// |a| <= 2^45.  Six fp64 ops, no integer multiplies: the fp64 pipe of B200
-// sustains ~2.6x the 64-bit-Shoup rate of the integer pipe (measured, see
-// DESIGN.md), and it is otherwise idle in this workload.
+// |a| <= 2^45.  No integer multiplies: the fp64 pipe of B200 sustains ~3x
+// the 64-bit-Shoup rate of the integer pipe (measured).
 #define HB_RND_MAGIC 6755399441055744.0  // 1.5 * 2^52
 
+// The quotient is rint(fl(a * wq)): one DMUL on the fp64 pipe plus one FRND
+// (a separate, lower-rate pipe that is otherwise idle) instead of the
+// fma-against-1.5*2^52 / subtract pair -- 5 fp64-pipe ops instead of 6
+// (tools/microbench.cu: 3.36 vs 2.94 T modular products/s).  The rounded
+// product moves q by at most 2^-8 relative to round(a*w/p) for |a| <= 2^45,
+// so |r| stays within (1/2 + 2^-7) p and the remainder is still exact.
 HB_DEV double fmod_mul(double a, double w, double wq, double p) {
   const double hi = a * w;
   const double lo = __fma_rn(a, w, -hi);
-  const double q = __fma_rn(a, wq, HB_RND_MAGIC) - HB_RND_MAGIC;
+  const double q = rint(a * wq);
   return __fma_rn(-q, p, hi) + lo;
 }
 
 // |x| <= 2^51 -> x mod p in (-(1/2 + eps) p, (1/2 + eps) p)
 HB_DEV double fmod_reduce(double x, double p, double pinv) {
-  const double q = __fma_rn(x, pinv, HB_RND_MAGIC) - HB_RND_MAGIC;
+  const double q = rint(x * pinv);
   return __fma_rn(-q, p, x);
 }
 

@@ -31,6 +31,26 @@ __global__ void k_fpmod(double* out, int iters, double w, double wp, double p) {
   double s = 0; for (int i = 0; i < 8; ++i) s += a[i];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// q = rint(a * w/p) with one rounding instruction instead of the magic-number pair
+__global__ void k_fpmod_rint(double* out, int iters, double w, double wp, double p) {
+  double a[8]; for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 7919.0 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double hi = a[i] * w; double lo = fma(a[i], w, -hi);
+      double q = rint(a[i] * wp); double r = fma(-q, p, hi); a[i] = r + lo;
+    }
+  double s = 0; for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_rint(double* out, int iters) {
+  double a[8]; for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1.37 + i * 0.61;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = rint(a[i]) + 0.75;
+  double s = 0; for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 int main() {
   const int blocks = 148 * 8, threads = 256, iters = 4096;
   double* dd; u64* du; cudaMalloc(&dd, blocks * threads * 8); cudaMalloc(&du, blocks * threads * 8);
@@ -44,6 +64,10 @@ int main() {
     cudaEventElapsedTime(&ms, a, b); if (rep) printf("u64 shoup   %.2f T mulmod/s\n", ops / ms / 1e9);
     cudaEventRecord(a); k_fpmod<<<blocks, threads>>>(dd, iters, (double)w, (double)w / p, (double)p); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); if (rep) printf("fp64 mulmod %.2f T mulmod/s\n", ops / ms / 1e9);
+    cudaEventRecord(a); k_fpmod_rint<<<blocks, threads>>>(dd, iters, (double)w, (double)w / p, (double)p); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); if (rep) printf("fp64 mulmod (rint q) %.2f T mulmod/s\n", ops / ms / 1e9);
+    cudaEventRecord(a); k_rint<<<blocks, threads>>>(dd, iters); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); if (rep) printf("rint+add    %.2f T pairs/s\n", ops / ms / 1e9);
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
