@@ -25,28 +25,45 @@ from .ntheory import bit_reverse_table, root_2n
 
 
 class UploadArena:
-    """Persistent pinned-host + device buffers for task tables while a CUDA
-    graph is being captured: every table gets its own never-reused slice,
-    so the captured host->device copies stay valid for every replay."""
+    """Persistent device buffer for task tables while a CUDA graph is being
+    captured: every table gets its own never-reused slice, written once at
+    capture time through a side stream (the capture runs in relaxed mode),
+    so replays read the tables in place and the graph carries no
+    host-to-device copy nodes.  Sized before the capture from a counted
+    eager pass (no allocation inside the capture)."""
 
     def __init__(self, device, nbytes: int = 256 << 20):
         self.host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
         self.dev = torch.empty(nbytes, dtype=torch.uint8, device=device)
         self.off = 0
+        self.side = torch.cuda.Stream(device)
 
     def put(self, t: torch.Tensor) -> torch.Tensor:
         n = t.numel()
         start = (self.off + 255) & ~255
-        if start + n > self.host.numel():
+        if start + n > self.dev.numel():
             raise MemoryError("graph upload arena exhausted")
         self.host[start:start + n].copy_(t)
         d = self.dev[start:start + n]
-        d.copy_(self.host[start:start + n], non_blocking=True)
+        with torch.cuda.stream(self.side):
+            d.copy_(self.host[start:start + n], non_blocking=True)
+        self.side.synchronize()
         self.off = start + n
         return d
 
 
+class UploadCounter:
+    """Counts the arena bytes (256-B aligned) an eager pass uploads."""
+
+    def __init__(self):
+        self.nbytes = 0
+
+    def add(self, n: int):
+        self.nbytes += (n + 255) & ~255
+
+
 _ARENA: UploadArena | None = None
+_COUNTER: UploadCounter | None = None
 
 
 def set_upload_arena(arena: UploadArena | None):
@@ -54,11 +71,18 @@ def set_upload_arena(arena: UploadArena | None):
     _ARENA = arena
 
 
+def set_upload_counter(counter: UploadCounter | None):
+    global _COUNTER
+    _COUNTER = counter
+
+
 def _upload(arr: np.ndarray, device) -> torch.Tensor:
     """Host task table -> device bytes (async on the current stream)."""
     t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8))
     if t.numel() == 0:
         return torch.empty(0, dtype=torch.uint8, device=device)
+    if _COUNTER is not None:
+        _COUNTER.add(t.numel())
     if _ARENA is not None:
         return _ARENA.put(t)
     return t.pin_memory().to(device, non_blocking=True)
