@@ -9,6 +9,6 @@ python tools/roofline_probe.py > gpurun_out/roof.log 2>&1 && \
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ntt3 -s 3 -c 1 -o gpurun_out/full_roofline python tools/roofline_probe.py > gpurun_out/ncu_roof.log 2>&1
 timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_ntt3_fwd<hb::PolF64, .int.14, .int.1>" -s 4 -c 1 -o gpurun_out/full_lift python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_lift.log 2>&1
 timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:k_ntt3_inv -s 8 -c 1 -o gpurun_out/full_inv python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_inv.log 2>&1
-timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.4, .int.4, .int.4" -s 6 -c 1 -o gpurun_out/full_ksgemm python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_ksg.log 2>&1
-timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.4, .int.4, .int.2" -s 0 -c 1 -o gpurun_out/full_mac python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_mac.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.8, .int.4, .int.2" -s 6 -c 1 -o gpurun_out/full_ksgemm python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_ksg.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:"k_mac_pipe<.int.8, .int.4, .int.1" -s 0 -c 1 -o gpurun_out/full_mac python tools/step_profile.py 1d-w64 full 64 > gpurun_out/ncu_mac.log 2>&1
 ls gpurun_out
