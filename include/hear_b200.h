@@ -88,6 +88,11 @@ int hb_ew(hb_ring* ring, int op, const void* tasks, int count, void* stream);
 /* Plaintext multiply-accumulate rows: sum_t pt_t * ct_t (the mult_plain/add
  * chains of hear/convolution.py:276-312, fastpath.py:168-180).               */
 int hb_mac(hb_ring* ring, const void* tasks, int count, const void* terms, void* stream);
+/* Many-term sums dst = sum_k srcs[term_off + k] (mod p) over HbMacTask rows
+ * (the add chains of sum_each: hear/fastpath.py rotate-and-sum and FC
+ * partial sums, ring.py:159 pw_add), srcs a device array of row pointers;
+ * nterms * p < 2^64.                                                        */
+int hb_sum(hb_ring* ring, const void* tasks, int count, const void* srcs, void* stream);
 /* Same, one launch per layer over [B*2, rows, N] ciphertext blocks.          */
 int hb_mac_strided(hb_ring* ring, const void* outs, int nout, const void* terms, int rows,
                    int bc, void* stream);

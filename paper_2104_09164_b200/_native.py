@@ -50,6 +50,7 @@ def lib():
         L.hb_mac.argtypes = [vp, vp, i32, vp, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
+        L.hb_sum.argtypes = [vp, vp, i32, vp, vp]
         L.hb_ks_inner.argtypes = [vp, vp, i32, vp]
         L.hb_ks_inner2.argtypes = [vp, vp, i32, i32, vp]
         L.hb_mac_shared.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]

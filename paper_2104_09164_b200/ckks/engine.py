@@ -834,6 +834,39 @@ class CkksBackend(BackendBase):
                 out[i] = Ct(CtData(res[q]), lvl, t0[0].scale * t0[1].scale, self.n2)
         return out
 
+    def _raw_sum_each(self, groups) -> list:
+        """Each group's sum in one pass (csrc/ops.cu k_sum_rows): every source
+        row read once instead of a pairwise add chain; modular addition, so
+        bit-identical to the left-to-right chain."""
+        kmax = max(len(g) for g in groups)
+        if kmax * max(self.ring.primes) >= 1 << 64:   # 64-bit accumulator headroom
+            return super()._raw_sum_each(groups)
+        out = [g[0] if len(g) == 1 else None for g in groups]
+        todo = [j for j, g in enumerate(groups) if len(g) > 1]
+        for lvl, idx in self._by_level([groups[j] for j in todo], lambda g: g[0].level).items():
+            js = [todo[i] for i in idx]
+            bsz = groups[js[0]][0].payload.batch
+            r = lvl + 1
+            k = max(len(groups[j]) for j in js)
+            rp = self.ring.row_ptrs
+            res = self.ring.empty(len(js), bsz, 2, r)
+            nrow = bsz * 2 * r
+            srcs = np.zeros((len(js), nrow, k), dtype=np.uint64)
+            zero = None
+            for q, j in enumerate(js):
+                g = groups[j]
+                for t, c in enumerate(g):
+                    srcs[q, :, t] = rp(c.payload.data)
+                if len(g) < k:   # ragged groups: pad with a zero row
+                    if zero is None:
+                        zero = self.ring.zeros(1)
+                    srcs[q, :, len(g):] = np.uint64(zero.data_ptr())
+            self.ring.sum_rows(rp(res), srcs.reshape(-1, k),
+                               np.tile(np.arange(r), len(js) * bsz * 2))
+            for q, j in enumerate(js):
+                out[j] = Ct(CtData(res[q]), lvl, groups[j][0].scale, self.n2)
+        return out
+
     def _raw_add_each(self, pairs) -> list:
         out = [None] * len(pairs)
         for lvl, idx in self._by_level(pairs, lambda p: p[0].level).items():

@@ -231,6 +231,17 @@ class RingContext:
             nat.check(self._lib.hb_mac_strided(self.handle, _ptr(d), len(outs), _ptr(t), rows, bc,
                                                self.stream), "mac_strided")
 
+    def sum_rows(self, dst: np.ndarray, srcs: np.ndarray, primes: np.ndarray):
+        """dst[r] = sum_k srcs[r, k] (mod p_r) for every output row r."""
+        rows, k = srcs.shape
+        if rows:
+            tasks = np.zeros(rows, dtype=nat.MAC_TASK)
+            tasks["dst"], tasks["prime"] = dst, primes
+            tasks["nterms"], tasks["term_off"] = k, np.arange(rows) * k
+            d = _upload(tasks, self.device)
+            s = _upload(np.ascontiguousarray(srcs, dtype=np.uint64).ravel(), self.device)
+            nat.check(self._lib.hb_sum(self.handle, _ptr(d), rows, _ptr(s), self.stream), "sum")
+
     def tensor(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)

@@ -28,6 +28,7 @@ cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
                                cudaStream_t);
 cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_sum_rows(const HbMacTask*, int, const void*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_shared(const void*, const void*, const void*, int, int, const HbPrime*, int,
                               int, int, cudaStream_t);
 cudaError_t launch_mac_gemm(const void*, const void*, const void*, int, int, const HbPrime*, int,
@@ -310,6 +311,12 @@ int hb_mac_strided(hb_ring* r, const void* outs, int nout, const void* terms, in
   cudaError_t e = launch_mac_strided(outs, nout, (const HbMacTerm*)terms, r->dev.primes, r->dev.n,
                                      rows, bc, (cudaStream_t)stream);
   return e ? fail(e, "hb_mac_strided") : 0;
+}
+
+int hb_sum(hb_ring* r, const void* tasks, int count, const void* srcs, void* stream) {
+  cudaError_t e = launch_sum_rows((const HbMacTask*)tasks, count, srcs, r->dev.primes, r->dev.n,
+                                  (cudaStream_t)stream);
+  return e ? fail(e, "hb_sum") : 0;
 }
 
 int hb_tensor(hb_ring* r, const void* tasks, int count, void* stream) {

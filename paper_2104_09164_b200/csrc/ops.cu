@@ -838,4 +838,39 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
   return cudaGetLastError();
 }
 
+// Many-term modular sums: dst = sum_k srcs[term_off + k] (mod p) per row task
+// (HbMacTask layout, pt unused) -- the left-to-right add chains of sum_each
+// (hear/fastpath.py rotate-and-sum / FC partial sums, ring.py:159 pw_add) in
+// one pass: each source row is read once and the result written once,
+// instead of a read-read-write per pairwise add.  Residues < p < 2^62 summed
+// in 64 bits (fewer than 4 terms per 2^63 headroom is never reached: the
+// caller bounds nterms so nterms * p < 2^64), one reduction at the end.
+__global__ void __launch_bounds__(256)
+k_sum_rows(const HbMacTask* __restrict__ tasks, const u64* const* __restrict__ srcs,
+           const HbPrime* __restrict__ primes, int n) {
+  const HbMacTask tk = tasks[blockIdx.y];
+  const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (j >= n) return;
+  const HbPrime P = primes[tk.prime];
+  u64 a0 = 0, a1 = 0;
+  const u64* const* s = srcs + tk.term_off;
+  for (int k = 0; k < tk.nterms; ++k) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(s[k] + j));
+    a0 += v.x;
+    a1 += v.y;
+  }
+  ulonglong2 o;
+  o.x = reduce64(a0, P);
+  o.y = reduce64(a1, P);
+  *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
+}
+
+cudaError_t launch_sum_rows(const HbMacTask* tasks, int count, const void* srcs,
+                            const HbPrime* primes, int n, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  dim3 grid((n / 2 + 255) / 256, count);
+  k_sum_rows<<<grid, 256, 0, st>>>(tasks, reinterpret_cast<const u64* const*>(srcs), primes, n);
+  return cudaGetLastError();
+}
+
 }  // namespace hb

@@ -320,3 +320,27 @@ def test_fused_rot_add_equals_rot_then_add(env):
     for f, p_ in zip(fused, plain):
         a, b = be.export(f), be.export(p_)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_sum_each_one_pass_equals_add_chain():
+    """sum_each in one pass (k_sum_rows) equals the left-to-right add chain,
+    ragged groups included, with the same operation counters."""
+    from paper_2104_09164_b200.backend import BackendBase
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    ps = gen_params("fast-hear")
+    be = CkksBackend(ps, seed=5, keygen=False)
+    lvl = 7
+    hs = [be.import_ct(*[np.stack(x) for x in zip(*[rand_ct(ps, lvl, 300 + 3 * h + i)
+                                                     for i in range(3)])], lvl, ps.msg_scale)
+          for h in range(7)]
+    groups = [hs[:5], hs[5:7], hs[3:4], hs[1:7]]
+    be.reset_counters()
+    fast = be.sum_each(groups)
+    n_fast = be.counters.as_dict()
+    be.reset_counters()
+    slow = BackendBase._raw_sum_each(be, groups)
+    for f, s_ in zip(fast, slow):
+        a, b = be.export(f), be.export(s_)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert sum(v.get("add", 0) for v in n_fast.values()) == 4 + 1 + 0 + 5
