@@ -481,12 +481,20 @@ class CkksBackend(BackendBase):
     def _raw_add_plain(self, a: Ct, p: Pt) -> Ct:
         x = a.payload.data
         bsz, lvl = x.shape[0], a.level
-        out = x.clone()
+        r = lvl + 1
+        out = torch.empty_like(x)
         rp = self.ring.row_ptrs
-        prow = rp(p.payload)[:lvl + 1]
-        c0 = rp(out).reshape(bsz, 2, lvl + 1)[:, 0].ravel()
-        self._ew(nat.EW_ADD, c0, c0, np.tile(prow, bsz), primes=self._row_primes(bsz, lvl + 1))
+        # one launch: c0 rows + plaintext, c1 rows + a zero row (a copy)
+        b = np.empty((bsz, 2, r), dtype=np.uint64)
+        b[:, 0] = rp(p.payload)[:r]
+        b[:, 1] = np.uint64(self._zero_row().data_ptr())
+        self._ew(nat.EW_ADD, rp(out), rp(x), b.ravel(), primes=self._row_primes(2 * bsz, r))
         return Ct(CtData(out), a.level, a.scale, self.n2)
+
+    def _zero_row(self) -> torch.Tensor:
+        if getattr(self, "_zrow", None) is None:
+            self._zrow = self.ring.zeros(1)
+        return self._zrow
 
     def _raw_mult_plain(self, a: Ct, p: Pt) -> Ct:
         x = a.payload.data
@@ -852,15 +860,12 @@ class CkksBackend(BackendBase):
             res = self.ring.empty(len(js), bsz, 2, r)
             nrow = bsz * 2 * r
             srcs = np.zeros((len(js), nrow, k), dtype=np.uint64)
-            zero = None
             for q, j in enumerate(js):
                 g = groups[j]
                 for t, c in enumerate(g):
                     srcs[q, :, t] = rp(c.payload.data)
                 if len(g) < k:   # ragged groups: pad with a zero row
-                    if zero is None:
-                        zero = self.ring.zeros(1)
-                    srcs[q, :, len(g):] = np.uint64(zero.data_ptr())
+                    srcs[q, :, len(g):] = np.uint64(self._zero_row().data_ptr())
             self.ring.sum_rows(rp(res), srcs.reshape(-1, k),
                                np.tile(np.arange(r), len(js) * bsz * 2))
             for q, j in enumerate(js):
