@@ -335,9 +335,14 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
   const char* old = getenv("HEAR_B200_MAC_SHARED");
   const char* pipe = getenv("HEAR_B200_MAC_PIPE");   // "0": register-prefetch kernels
   cudaError_t e = cudaErrorNotSupported;
-  // the cp.async pipeline pays off once a layer has several clips per launch;
-  // one or two clip-components run the register-prefetch kernel (lower latency)
-  if (r->dev.use_f64 && bc >= 8 && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
+  // the cp.async-pipelined GEMM at every batch size (measured: also the lower
+  // latency at one clip); HEAR_B200_MAC_PIPE_MIN raises the threshold
+  static int pipe_min = -1;
+  if (pipe_min < 0) {
+    const char* v = getenv("HEAR_B200_MAC_PIPE_MIN");
+    pipe_min = v ? atoi(v) : 1;
+  }
+  if (r->dev.use_f64 && bc >= pipe_min && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
     e = launch_mac_pipe(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) (void)cudaGetLastError();   // term table too large
   }
