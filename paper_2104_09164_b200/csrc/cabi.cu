@@ -26,7 +26,7 @@ cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream
 cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
-                               cudaStream_t);
+                               bool, cudaStream_t);
 cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_sum_rows(const HbMacTask*, int, const void*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_shared(const void*, const void*, const void*, int, int, const HbPrime*, int,
@@ -309,7 +309,7 @@ int hb_mac(hb_ring* r, const void* tasks, int count, const void* terms, void* st
 int hb_mac_strided(hb_ring* r, const void* outs, int nout, const void* terms, int rows, int bc,
                    void* stream) {
   cudaError_t e = launch_mac_strided(outs, nout, (const HbMacTerm*)terms, r->dev.primes, r->dev.n,
-                                     rows, bc, (cudaStream_t)stream);
+                                     rows, bc, r->dev.use_f64 != 0, (cudaStream_t)stream);
   return e ? fail(e, "hb_mac_strided") : 0;
 }
 

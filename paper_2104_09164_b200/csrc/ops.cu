@@ -402,13 +402,54 @@ k_mac_strided(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __re
   }
 }
 
+// fp64-pipe variant (rings with every prime < 2^42): products as fmod_mul
+// (5 fp64 ops + one rounding) summed as balanced doubles, one
+// canonicalisation -- instead of 64x64->128-bit integer products and
+// 128-bit folds on the integer pipe; same canonical residues.
+__global__ void __launch_bounds__(256)
+k_mac_strided_f64(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __restrict__ terms,
+                  const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  const long long total = (long long)nout * BC * R;
+  for (long long y = blockIdx.y; y < total; y += gridDim.y) {
+    const int o = (int)(y / ((long long)BC * R));
+    const int rem = (int)(y % ((long long)BC * R));
+    const int bc = rem / R, r = rem % R;
+    const HbMacOut ou = outs[o];
+    const HbPrime P = primes[r];
+    const double p = P.pd, pinv = P.pinv;
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    const size_t ct_off = ((size_t)bc * R + r) * n + j;
+    const size_t pt_off = (size_t)r * n + j;
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = 0; k < ou.nterms; ++k) {
+      const HbMacTerm tm = terms[ou.term_off + k];
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(tm.pt + pt_off));
+      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(tm.ct + ct_off));
+      const double a0 = u64_to_f(a.x), a1 = u64_to_f(a.y);
+      s0 += fmod_mul(u64_to_f(b.x), a0, a0 * pinv, p);
+      s1 += fmod_mul(u64_to_f(b.y), a1, a1 * pinv, p);
+      if ((k & 255) == 255) { s0 = fmod_reduce(s0, p, pinv); s1 = fmod_reduce(s1, p, pinv); }
+    }
+    ulonglong2 v;
+    v.x = fmod_canon(s0, p, pinv);
+    v.y = fmod_canon(s1, p, pinv);
+    *reinterpret_cast<ulonglong2*>(ou.dst + ct_off) = v;
+  }
+}
+
 cudaError_t launch_mac_strided(const void* outs, int nout, const HbMacTerm* terms,
-                               const HbPrime* primes, int n, int R, int BC, cudaStream_t st) {
+                               const HbPrime* primes, int n, int R, int BC, bool f64,
+                               cudaStream_t st) {
   if (nout <= 0) return cudaSuccess;
   const long long total = (long long)nout * BC * R;
   dim3 grid((n / 2 + EW_THREADS - 1) / EW_THREADS, total < 65535 ? (int)total : 65535);
-  k_mac_strided<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout, terms,
-                                             primes, n, R, BC);
+  if (f64)
+    k_mac_strided_f64<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout,
+                                                   terms, primes, n, R, BC);
+  else
+    k_mac_strided<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout,
+                                               terms, primes, n, R, BC);
   return cudaGetLastError();
 }
 
