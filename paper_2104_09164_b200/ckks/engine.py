@@ -778,7 +778,9 @@ class CkksBackend(BackendBase):
 
     # HBM budget for one batched launch group's temporaries (decomposed
     # digits of many ciphertexts); larger groups are split into chunks.
-    ks_budget_bytes = 6 << 30
+    # temporaries of one batched key switch (digits, inner products); B200 has
+    # 180 GB, and larger batches of jobs make the inner-product GEMM wider
+    ks_budget_bytes = int(float(os.environ.get("HEAR_B200_KS_BUDGET_GB", "24")) * (1 << 30))
 
     @staticmethod
     def _by_level(items, level_of):
