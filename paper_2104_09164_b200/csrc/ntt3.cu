@@ -23,7 +23,18 @@
 // the twiddles from L1).  The only cluster barrier makes the mbarrier
 // initialisation visible and is split around the first pass.  The lazy
 // intermediate never touches L2/HBM (the two-pass kernels write and re-read
-// it: 256 KB per row).  Shared memory per CTA: 64 KB + 8 B.
+// it: 256 KB per row).
+//
+// Also in shared memory: the column twiddles and the stride-8 block-stage
+// twiddles of the CTA's tile (staged once, LDS at immediate offsets); the
+// last three forward / first three inverse stages read a plane-major
+// (w, w/p) table with lanes on consecutive entries.  ModDown modes: the x_r
+// tile is TMA-bulk-copied (cp.async.bulk + second mbarrier) into the
+// consumed column buffer while the block pass runs, and the epilogue
+// (x_r - y) * P^-1 (+ c0) (+ post-addend) runs on the fp64 pipe on 16-byte
+// lane-contiguous chunks.  Inverse: a second destination can receive the
+// input row verbatim (the ModUp identity digit).  Shared memory per CTA:
+// 64 KB + 9.7 KB twiddles + 16 B (3 CTAs per SM at 80 registers).
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
