@@ -80,6 +80,12 @@ int hb_ntt_kernels(hb_ring* ring, int count);
 /* 1 when the ring's modular arithmetic runs on the fp64 pipe (every prime
  * < 2^42 and HEAR_B200_INT_NTT unset), else 0.                              */
 int hb_ring_uses_f64(const hb_ring* ring);
+/* Launch every library kernel with programmatic dependent launch (PDL:
+ * the next kernel's CTAs are scheduled while the previous grid drains; each
+ * kernel waits on griddepcontrol before touching its inputs) while `on`.
+ * For CUDA-graph capture, where task tables are static device data.  Returns
+ * the previous setting.                                                     */
+int hb_set_pdl(int on);
 /* Element-wise op `op` over HbEwTask rows: 0 add (ring.py:159), 1 sub
  * (ring.py:167), 2 mul (ring.py:127), 3 scalar mul (ring.py:175), 4 a*b+c
  * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,

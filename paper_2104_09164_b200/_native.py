@@ -44,6 +44,7 @@ def lib():
         L.hb_ntt_inv.argtypes = [vp, vp, i32, vp]
         L.hb_ntt_kernels.argtypes = [vp, i32]
         L.hb_ring_uses_f64.argtypes = [vp]
+        L.hb_set_pdl.argtypes = [i32]
         L.hb_ks_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_longlong,
                                  ctypes.c_longlong, i32, i32, vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]

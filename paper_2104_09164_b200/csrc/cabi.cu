@@ -18,6 +18,10 @@
 
 #include "ring.cuh"
 
+// programmatic dependent launch switch (ring.cuh); set only while a CUDA graph
+// of the evaluation is captured (hb_set_pdl)
+int g_hb_pdl = 0;
+
 namespace hb {
 cudaError_t launch_ntt_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
 cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
@@ -291,6 +295,12 @@ int hb_ntt_inv(hb_ring* r, const void* tasks, int count, void* stream) {
 }
 
 int hb_ntt_kernels(hb_ring* r, int count) { return ntt_kernels(r->dev, count); }
+
+int hb_set_pdl(int on) {
+  const int old = g_hb_pdl;
+  g_hb_pdl = on ? 1 : 0;
+  return old;
+}
 
 int hb_ring_uses_f64(const hb_ring* r) { return r && r->dev.use_f64 ? 1 : 0; }
 

@@ -40,6 +40,7 @@ template <int TO, int TB, int WO, int WB>
 __global__ void __launch_bounds__(256)
 k_mac_gemm_c3(HbMacGroupC g, const HbPrime* __restrict__ primes, const double* __restrict__ cconst,
               int w, int fold, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   extern __shared__ const u64* ptrs[];
   const int T = g.nterms, O = g.nout;
   for (int i = threadIdx.x + threadIdx.y * 32; i < T + O * T + O; i += 256) {
@@ -143,7 +144,7 @@ static cudaError_t mac_c3_t(const HbMacGroupC& g, const HbPrime* primes, const d
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
-  k_mac_gemm_c3<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, cc, w, fold, n, R, BC);
+  (void)hb_launch(k_mac_gemm_c3<TO, TB, WO, WB>, dim3(grid), dim3(block), smem, st, g, primes, cc, w, fold, n, R, BC);
   return cudaGetLastError();
 }
 
@@ -168,6 +169,7 @@ cudaError_t launch_mac_gemm_c3(const void* cts, const void* pts, const void* dst
 __global__ void __launch_bounds__(256)
 k_ks_inner_c3(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes,
               const double* __restrict__ cconst, int w, int fold, int n, int nb) {
+  HB_PDL_ENTRY();
   const HbKsTask2 tk = tasks[blockIdx.y];
   const int b = blockIdx.x * blockDim.y + threadIdx.y;    // grid order as ops.cu k_ks_inner2
   const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
@@ -230,7 +232,7 @@ cudaError_t launch_ks_inner_c3(const void* tasks, int ntasks, int nb, const HbRi
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
   dim3 grid((nb + by - 1) / by, ntasks, (R.n / 2 + 31) / 32);
-  k_ks_inner_c3<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), R.primes,
+  (void)hb_launch(k_ks_inner_c3, dim3(grid), dim3(block), 0, st, reinterpret_cast<const HbKsTask2*>(tasks), R.primes,
                                         R.chunk_consts, R.chunk_w, R.chunk_fold, R.n, nb);
   return cudaGetLastError();
 }

@@ -49,6 +49,7 @@ __device__ void fft_smem(double2* a, const HbFftTables& T, int sign) {
 // Sets *overflow when any |coefficient| >= 2^52 (encoder.py:50-55).
 __global__ void k_encode(const double* __restrict__ slots, long long* __restrict__ coeffs,
                          double scale, HbFftTables T, int* overflow) {
+  HB_PDL_ENTRY();
   extern __shared__ double2 a[];
   const int n2 = T.n2;
   const double* v = slots + (size_t)blockIdx.x * n2;
@@ -75,6 +76,7 @@ __global__ void k_encode(const double* __restrict__ slots, long long* __restrict
 // Decode: double coefficients (N per poly) -> real slot values / scale.
 __global__ void k_decode(const double* __restrict__ coeffs, double* __restrict__ slots,
                          double scale, HbFftTables T) {
+  HB_PDL_ENTRY();
   extern __shared__ double2 a[];
   const int n2 = T.n2;
   const double* c = coeffs + (size_t)blockIdx.x * 2 * n2;
@@ -95,7 +97,7 @@ cudaError_t launch_encode(const double* slots, long long* coeffs, int npoly, dou
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_encode, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
-  k_encode<<<npoly, 512, smem, st>>>(slots, coeffs, scale, T, overflow);
+  (void)hb_launch(k_encode, dim3(npoly), dim3(512), smem, st, slots, coeffs, scale, T, overflow);
   return cudaGetLastError();
 }
 
@@ -106,7 +108,7 @@ cudaError_t launch_decode(const double* coeffs, double* slots, int npoly, double
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_decode, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
-  k_decode<<<npoly, 512, smem, st>>>(coeffs, slots, scale, T);
+  (void)hb_launch(k_decode, dim3(npoly), dim3(512), smem, st, coeffs, slots, scale, T);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,7 @@ HB_DEV u64 recombine3(double s0, double s1, double s2, const double* cc, double 
 template <int TO, int TB, int WO, int WB, bool C3, int S>
 __global__ void __launch_bounds__(256)
 k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
+  HB_PDL_ENTRY();
   constexpr int OB = TO * WO, CB = TB * WB, ROWS = OB + CB;
   constexpr int STAGE = ROWS * 32;            // u64 per stage
   constexpr int CHUNKS = ROWS * 16;           // 16-byte copies per stage
@@ -208,7 +209,7 @@ cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cu
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32));
-  k_mac_pipe<TO, TB, WO, WB, C3, S><<<grid, block, smem, st>>>(g, RG, R, BC);
+  (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, C3, S>, dim3(grid), dim3(block), smem, st, g, RG, R, BC);
   return cudaGetLastError();
 }
 

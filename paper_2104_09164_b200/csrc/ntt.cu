@@ -122,6 +122,7 @@ HB_DEV void ntt_fwd_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P)
 template <int LOGN, int MODE, bool F64>
 __global__ void __launch_bounds__((1 << LOGN) / 16)
 k_ntt_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
+  HB_PDL_ENTRY();
   const HbNttTask tk = tasks[blockIdx.x];
   const HbPrime P = R.primes[tk.dst_prime];
   if (F64)
@@ -215,6 +216,7 @@ HB_DEV void ntt_inv_body(const HbNttTask& tk, const HbRing& R, const HbPrime& P)
 template <int LOGN, bool F64>
 __global__ void __launch_bounds__((1 << LOGN) / 16)
 k_ntt_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
+  HB_PDL_ENTRY();
   const HbNttTask tk = tasks[blockIdx.x];
   const HbPrime P = R.primes[tk.dst_prime];
   if (F64)
@@ -233,7 +235,7 @@ static cudaError_t fwd_one(const HbNttTask* tasks, int count, const HbRing& R, c
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt_fwd<LOGN, MODE, F64>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
-  k_ntt_fwd<LOGN, MODE, F64><<<count, T, smem, st>>>(tasks, R);
+  (void)hb_launch(k_ntt_fwd<LOGN, MODE, F64>, dim3(count), dim3(T), smem, st, tasks, R);
   return cudaGetLastError();
 }
 
@@ -263,7 +265,7 @@ static cudaError_t inv_one(const HbNttTask* tasks, int count, const HbRing& R, c
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt_inv<LOGN, F64>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
-  k_ntt_inv<LOGN, F64><<<count, T, smem, st>>>(tasks, R);
+  (void)hb_launch(k_ntt_inv<LOGN, F64>, dim3(count), dim3(T), smem, st, tasks, R);
   return cudaGetLastError();
 }
 

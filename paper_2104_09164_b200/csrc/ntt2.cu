@@ -77,6 +77,7 @@ HB_DEV u64 as_bits(typename Pol::T v) {
 template <class Pol, int LOGN, int MODE, bool FWD>
 __global__ void __launch_bounds__(THREADS2, HB_NTT2_MINB)
 k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
+  HB_PDL_ENTRY();
   constexpr int S1 = LOGN - 7, M = 1 << S1, CW = TILE / M, NCH = 128 / CW;
   constexpr int GQ = M / 16;  // 16-element groups per column
   typedef typename Pol::T V;
@@ -163,6 +164,7 @@ k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
 template <class Pol, int LOGN, int MODE, bool FWD>
 __global__ void __launch_bounds__(THREADS2, HB_NTT2_MINB)
 k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
+  HB_PDL_ENTRY();
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, NT = N / TILE;
   typedef typename Pol::T V;
   __shared__ __align__(16) V sm[TILE];
@@ -356,8 +358,8 @@ static cudaError_t fwd2_t(const HbNttTask* tasks, int count, const HbRing& R, cu
   const int CH = ntt_chunk();
   for (int c0 = 0; c0 < count; c0 += CH) {   // chunks keep the intermediate in L2
     const int c = count - c0 < CH ? count - c0 : CH;
-    k_ntt2_cols<Pol, LOGN, MODE, true><<<c * NCH, THREADS2, 0, st>>>(tasks + c0, R);
-    k_ntt2_blocks<Pol, LOGN, MODE, true><<<c * ((1 << LOGN) / TILE), THREADS2, dyn, st>>>(tasks + c0, R);
+    (void)hb_launch(k_ntt2_cols<Pol, LOGN, MODE, true>, dim3(c * NCH), dim3(THREADS2), 0, st, tasks + c0, R);
+    (void)hb_launch(k_ntt2_blocks<Pol, LOGN, MODE, true>, dim3(c * ((1 << LOGN) / TILE)), dim3(THREADS2), dyn, st, tasks + c0, R);
   }
   return cudaGetLastError();
 }
@@ -373,9 +375,9 @@ static cudaError_t inv2_t(const HbNttTask* tasks, int count, const HbRing& R, cu
   const int CH = ntt_chunk();
   for (int c0 = 0; c0 < count; c0 += CH) {
     const int c = count - c0 < CH ? count - c0 : CH;
-    k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false><<<c * ((1 << LOGN) / TILE), THREADS2, dyn, st>>>(tasks + c0, R);
+    (void)hb_launch(k_ntt2_blocks<Pol, LOGN, FWD_PLAIN, false>, dim3(c * ((1 << LOGN) / TILE)), dim3(THREADS2), dyn, st, tasks + c0, R);
     // the column pass reads the block pass's lazy output from dst
-    k_ntt2_cols<Pol, LOGN, FWD_PLAIN, false><<<c * NCH, THREADS2, 0, st>>>(tasks + c0, R);
+    (void)hb_launch(k_ntt2_cols<Pol, LOGN, FWD_PLAIN, false>, dim3(c * NCH), dim3(THREADS2), 0, st, tasks + c0, R);
   }
   return cudaGetLastError();
 }

@@ -224,6 +224,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
+  HB_PDL_ENTRY();   // static prologue above; the row data below may be the previous kernel's
   // ---- column pass over columns [rank*CW, rank*CW + CW)
   const int cg0 = rank * CW;
   {
@@ -401,6 +402,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   };
   const int t = threadIdx.x;
   const size_t base = (size_t)rank * TILE3;
+  HB_PDL_ENTRY();   // static prologue above; the row data below may be the previous kernel's
   // ---- block pass on tile `rank`: coalesced 16-byte loads into the
   // swizzled tile, stages 0..2 (contiguous 8), 3..6 (stride 8)
 #pragma unroll
@@ -501,13 +503,15 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.blockDim = dim3(THREADS3);
   cfg.dynamicSmemBytes = smem3<LOGN>();
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_hb_pdl ? 2 : 1;
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(smem3<LOGN>()), &smem_cur);
   if (e != cudaSuccess) return e;
@@ -522,13 +526,15 @@ cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.blockDim = dim3(THREADS3);
   cfg.dynamicSmemBytes = smem3<LOGN>();
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_hb_pdl ? 2 : 1;
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt3_inv<PolF64, LOGN>, (int)(smem3<LOGN>()), &smem_cur);
   if (e != cudaSuccess) return e;

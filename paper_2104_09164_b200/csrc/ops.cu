@@ -29,6 +29,7 @@ constexpr int EW_THREADS = 256;
 template <int OP>
 __global__ void __launch_bounds__(EW_THREADS)
 k_ew(const HbEwTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes, int n) {
+  HB_PDL_ENTRY();
   for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
     const HbEwTask tk = tasks[t];
     const HbPrime P = primes[tk.prime];
@@ -86,7 +87,7 @@ cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* 
   dim3 grid = ew_grid(ntasks, n);
   switch (op) {
 #define HB_EW_CASE(OPC) \
-  case OPC: k_ew<OPC><<<grid, EW_THREADS, 0, st>>>(tasks, ntasks, primes, n); break;
+  case OPC: (void)hb_launch(k_ew<OPC>, dim3(grid), dim3(EW_THREADS), 0, st, tasks, ntasks, primes, n); break;
     HB_EW_CASE(EW_ADD)
     HB_EW_CASE(EW_SUB)
     HB_EW_CASE(EW_MUL)
@@ -112,6 +113,7 @@ cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* 
 __global__ void __launch_bounds__(EW_THREADS)
 k_mac(const HbMacTask* __restrict__ tasks, int ntasks, const HbMacTerm* __restrict__ terms,
       const HbPrime* __restrict__ primes, int n) {
+  HB_PDL_ENTRY();
   for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
     const HbMacTask tk = tasks[t];
     const HbPrime P = primes[tk.prime];
@@ -136,7 +138,7 @@ k_mac(const HbMacTask* __restrict__ tasks, int ntasks, const HbMacTerm* __restri
 cudaError_t launch_mac(const HbMacTask* tasks, int ntasks, const HbMacTerm* terms,
                        const HbPrime* primes, int n, cudaStream_t st) {
   if (ntasks <= 0) return cudaSuccess;
-  k_mac<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(tasks, ntasks, terms, primes, n);
+  (void)hb_launch(k_mac, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, tasks, ntasks, terms, primes, n);
   return cudaGetLastError();
 }
 
@@ -153,6 +155,7 @@ struct HbTensorTask {
 __global__ void __launch_bounds__(EW_THREADS)
 k_tensor(const HbTensorTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes,
          int n) {
+  HB_PDL_ENTRY();
   for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
     const HbTensorTask tk = tasks[t];
     const HbPrime P = primes[tk.prime];
@@ -186,7 +189,7 @@ k_tensor(const HbTensorTask* __restrict__ tasks, int ntasks, const HbPrime* __re
 cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, int n,
                           cudaStream_t st) {
   if (ntasks <= 0) return cudaSuccess;
-  k_tensor<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(
+  (void)hb_launch(k_tensor, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, 
       reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
   return cudaGetLastError();
 }
@@ -198,6 +201,7 @@ cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, 
 __global__ void __launch_bounds__(EW_THREADS)
 k_ks_inner(const HbKsTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes,
            int n) {
+  HB_PDL_ENTRY();
   for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
     const HbKsTask tk = tasks[t];
     const HbPrime P = primes[tk.prime];
@@ -234,7 +238,7 @@ k_ks_inner(const HbKsTask* __restrict__ tasks, int ntasks, const HbPrime* __rest
 cudaError_t launch_ks_inner(const HbKsTask* tasks, int ntasks, const HbPrime* primes, int n,
                             cudaStream_t st) {
   if (ntasks <= 0) return cudaSuccess;
-  k_ks_inner<<<ew_grid(ntasks, n), EW_THREADS, 0, st>>>(tasks, ntasks, primes, n);
+  (void)hb_launch(k_ks_inner, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, tasks, ntasks, primes, n);
   return cudaGetLastError();
 }
 
@@ -278,6 +282,7 @@ HB_DEV double mw_to_double(const u64* m, int nl, bool neg) {
 __global__ void k_crt_double(const HbCrtTask* __restrict__ tasks, int ntasks, const u64* __restrict__ consts,
                              const HbPrime* __restrict__ primes, const int* __restrict__ prime_idx,
                              int keep, int nl, int n) {
+  HB_PDL_ENTRY();
   // consts layout: Q[nl], Qhalf[nl], qhat_inv[keep], qhat[keep][nl]
   const u64* Q = consts;
   const u64* Qh = consts + nl;
@@ -352,7 +357,7 @@ cudaError_t launch_crt_double(const HbCrtTask* tasks, int ntasks, const u64* con
   if (ntasks <= 0) return cudaSuccess;
   if (nl > CRT_MAXL) return cudaErrorInvalidValue;
   dim3 grid((n + 255) / 256, ntasks < 65535 ? ntasks : 65535);
-  k_crt_double<<<grid, 256, 0, st>>>(tasks, ntasks, consts, primes, prime_idx, keep, nl, n);
+  (void)hb_launch(k_crt_double, dim3(grid), dim3(256), 0, st, tasks, ntasks, consts, primes, prime_idx, keep, nl, n);
   return cudaGetLastError();
 }
 
@@ -375,6 +380,7 @@ struct HbMacOut {
 __global__ void __launch_bounds__(EW_THREADS)
 k_mac_strided(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __restrict__ terms,
               const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   const long long total = (long long)nout * BC * R;
   for (long long y = blockIdx.y; y < total; y += gridDim.y) {
     const int o = (int)(y / ((long long)BC * R));
@@ -409,6 +415,7 @@ k_mac_strided(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __re
 __global__ void __launch_bounds__(256)
 k_mac_strided_f64(const HbMacOut* __restrict__ outs, int nout, const HbMacTerm* __restrict__ terms,
                   const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   const long long total = (long long)nout * BC * R;
   for (long long y = blockIdx.y; y < total; y += gridDim.y) {
     const int o = (int)(y / ((long long)BC * R));
@@ -445,10 +452,10 @@ cudaError_t launch_mac_strided(const void* outs, int nout, const HbMacTerm* term
   const long long total = (long long)nout * BC * R;
   dim3 grid((n / 2 + EW_THREADS - 1) / EW_THREADS, total < 65535 ? (int)total : 65535);
   if (f64)
-    k_mac_strided_f64<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout,
+    (void)hb_launch(k_mac_strided_f64, dim3(grid), dim3(EW_THREADS), 0, st, reinterpret_cast<const HbMacOut*>(outs), nout,
                                                    terms, primes, n, R, BC);
   else
-    k_mac_strided<<<grid, EW_THREADS, 0, st>>>(reinterpret_cast<const HbMacOut*>(outs), nout,
+    (void)hb_launch(k_mac_strided, dim3(grid), dim3(EW_THREADS), 0, st, reinterpret_cast<const HbMacOut*>(outs), nout,
                                                terms, primes, n, R, BC);
   return cudaGetLastError();
 }
@@ -477,6 +484,7 @@ constexpr int MAC_OT = 8;
 
 __global__ void __launch_bounds__(256)
 k_mac_shared(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   const int jp = blockIdx.x * 32 + threadIdx.x;       // coefficient pair
   const int r = blockIdx.y % R;
   const int bc = (blockIdx.y / R) * blockDim.y + threadIdx.y;
@@ -528,7 +536,7 @@ cudaError_t launch_mac_shared(const void* cts, const void* pts, const void* dsts
   const int by = BC < 8 ? BC : 8;
   dim3 block(32, by);
   dim3 grid((n / 2 + 31) / 32, R * ((BC + by - 1) / by), (nout + MAC_OT - 1) / MAC_OT);
-  k_mac_shared<<<grid, block, 0, st>>>(g, primes, n, R, BC);
+  (void)hb_launch(k_mac_shared, dim3(grid), dim3(block), 0, st, g, primes, n, R, BC);
   return cudaGetLastError();
 }
 
@@ -541,6 +549,7 @@ cudaError_t launch_mac_shared(const void* cts, const void* pts, const void* dsts
 __global__ void __launch_bounds__(256)
 k_ks_inner2(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
             int nb) {
+  HB_PDL_ENTRY();
   const HbKsTask2 tk = tasks[blockIdx.y];
   // grid: x = clip group (fastest), y = task, z = coefficient chunk (slowest):
   // the clips of one key row run back to back, so the key is read from HBM once
@@ -582,7 +591,7 @@ cudaError_t launch_ks_inner2(const void* tasks, int ntasks, int nb, const HbPrim
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
   dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
-  k_ks_inner2<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
+  (void)hb_launch(k_ks_inner2, dim3(grid), dim3(block), 0, st, reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
   return cudaGetLastError();
 }
 
@@ -602,6 +611,7 @@ namespace hb {
 template <int TO, int TB, int WO, int WB>
 __global__ void __launch_bounds__(256, (TO * TB > 16 ? 1 : 2))
 k_mac_gemm(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   extern __shared__ const u64* ptrs[];   // cts[T] | pts[O*T] | dsts[O]
   const int T = g.nterms, O = g.nout;
   for (int i = threadIdx.x + threadIdx.y * 32; i < T + O * T + O; i += 256) {
@@ -673,7 +683,7 @@ static cudaError_t mac_gemm_t(const HbMacGroup& g, const HbPrime* primes, int n,
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
-  k_mac_gemm<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
+  (void)hb_launch(k_mac_gemm<TO, TB, WO, WB>, dim3(grid), dim3(block), smem, st, g, primes, n, R, BC);
   return cudaGetLastError();
 }
 
@@ -705,6 +715,7 @@ namespace hb {
 template <int TO, int TB, int WO, int WB>
 __global__ void __launch_bounds__(256)
 k_mac_gemm_f64(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
+  HB_PDL_ENTRY();
   extern __shared__ const u64* ptrs[];
   const int T = g.nterms, O = g.nout;
   for (int i = threadIdx.x + threadIdx.y * 32; i < T + O * T + O; i += 256) {
@@ -794,7 +805,7 @@ static cudaError_t mac_gemm_f64_t(const HbMacGroup& g, const HbPrime* primes, in
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + TB * WB - 1) / (TB * WB), (g.nout + TO * WO - 1) / (TO * WO), R * (n / 32));
-  k_mac_gemm_f64<TO, TB, WO, WB><<<grid, block, smem, st>>>(g, primes, n, R, BC);
+  (void)hb_launch(k_mac_gemm_f64<TO, TB, WO, WB>, dim3(grid), dim3(block), smem, st, g, primes, n, R, BC);
   return cudaGetLastError();
 }
 
@@ -821,6 +832,7 @@ cudaError_t launch_mac_gemm_f64(const void* cts, const void* pts, const void* ds
 __global__ void __launch_bounds__(256)
 k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
                 int nb) {
+  HB_PDL_ENTRY();
   const HbKsTask2 tk = tasks[blockIdx.y];
   // grid: x = clip group (fastest), y = task, z = coefficient chunk (slowest):
   // the clips of one key row run back to back, so the key is read from HBM once
@@ -875,7 +887,7 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
   const int by = nb < 8 ? nb : 8;
   dim3 block(32, by);
   dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
-  k_ks_inner2_f64<<<grid, block, 0, st>>>(reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
+  (void)hb_launch(k_ks_inner2_f64, dim3(grid), dim3(block), 0, st, reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
   return cudaGetLastError();
 }
 
@@ -889,6 +901,7 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
 __global__ void __launch_bounds__(256)
 k_sum_rows(const HbMacTask* __restrict__ tasks, const u64* const* __restrict__ srcs,
            const HbPrime* __restrict__ primes, int n) {
+  HB_PDL_ENTRY();
   const HbMacTask tk = tasks[blockIdx.y];
   const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (j >= n) return;
@@ -910,7 +923,7 @@ cudaError_t launch_sum_rows(const HbMacTask* tasks, int count, const void* srcs,
                             const HbPrime* primes, int n, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   dim3 grid((n / 2 + 255) / 256, count);
-  k_sum_rows<<<grid, 256, 0, st>>>(tasks, reinterpret_cast<const u64* const*>(srcs), primes, n);
+  (void)hb_launch(k_sum_rows, dim3(grid), dim3(256), 0, st, tasks, reinterpret_cast<const u64* const*>(srcs), primes, n);
   return cudaGetLastError();
 }
 

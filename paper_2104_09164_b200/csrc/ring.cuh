@@ -1,7 +1,40 @@
 // Device-side ring context and task descriptors shared by all kernels.
 #pragma once
 #include <cuda_runtime.h>
+#include <utility>
 #include "modarith.cuh"
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// When g_hb_pdl is set (CUDA-graph capture of the evaluation, where task
+// tables are static device data), every library kernel is launched with
+// programmatic stream serialisation: the next kernel's CTAs may be scheduled
+// while this one drains.  Every kernel starts with HB_PDL_ENTRY() -- wait for
+// the previous grid's completion and memory, then allow the next grid to
+// launch -- so results are unchanged; without the attribute both are no-ops.
+extern int g_hb_pdl;
+#define HB_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define HB_PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#define HB_PDL_ENTRY() \
+  do {                 \
+    HB_PDL_WAIT();     \
+    HB_PDL_LAUNCH();   \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t hb_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_hb_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Twiddle entry: power of the 2N-th root plus its Shoup companion, stored
 // together so one 16-byte load fetches both.

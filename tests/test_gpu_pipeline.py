@@ -114,3 +114,34 @@ def test_cuda_graph_replay_bit_exact():
         replay = g(ct).payload.data
         torch.cuda.synchronize()
         assert torch.equal(eager, replay)
+
+
+def test_graph_with_pdl_bit_identical():
+    """CUDA-graph replay with programmatic dependent launch (HEAR_B200_PDL=1)
+    is bit-identical to eager evaluation."""
+    import os
+    import torch
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import (GraphedPipeline, compile_pipeline, encrypt_input,
+                                                run_pipeline)
+    from paper_2104_09164_b200.model import (collapse_layers, make_random_input, make_random_model,
+                                             net_by_name)
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    shape = net_by_name("1d-w64")
+    cpar = collapse_layers(make_random_model(shape, 1), shape)
+    be = CkksBackend(gen_params("fast-hear"), seed=3)
+    cp = compile_pipeline(shape, "fast", "full", be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    enc = ModelEncoder(cp, cpar, be).prepare()
+    ct = encrypt_input(np.stack([make_random_input(shape, 50 + i) for i in range(8)]), cp, be)
+    want = run_pipeline(enc, ct, be).payload.data.clone()
+    os.environ["HEAR_B200_PDL"] = "1"
+    try:
+        g = GraphedPipeline(enc, be, batch=8)
+    finally:
+        del os.environ["HEAR_B200_PDL"]
+    for _ in range(2):
+        got = g(ct).payload.data
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
