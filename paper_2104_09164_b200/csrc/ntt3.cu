@@ -212,7 +212,6 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
   const Pol pol(P);
-  stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, tk.dst_prime), rank);
   auto fetch_col = [&](int s, int idx) { return tws[(1 << s) + idx - 1]; };
   auto fetch_blk = [&](int s, int idx) {
     const int e = s - S1;
@@ -224,22 +223,38 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
-  HB_PDL_ENTRY();   // static prologue above; the row data below may be the previous kernel's
+  HB_PDL_ENTRY();   // the row data below may be the previous kernel's output
   // ---- column pass over columns [rank*CW, rank*CW + CW)
   const int cg0 = rank * CW;
   {
     const int c = t % CW, gq = t / CW;
     V x[16];
-#pragma unroll
-    for (int rd = 0; rd < CP::NR; ++rd) {
+    {   // round-0 operands: raw loads in flight while the twiddles are staged
+      u64 raw[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        if (!CP::owns(rd, q)) break;
-        const int m = CP::m_of(rd, gq, q);
-        x[q] = rd == 0 ? ld_src<Pol, MODE>(tk, pol, ps, ps_half, (size_t)m * 128 + cg0 + c)
-                       : sm[csw<CW>(m, c)];
+        if (!CP::owns(0, q)) break;
+        raw[q] = __ldg(tk.src + (size_t)CP::m_of(0, gq, q) * 128 + cg0 + c);
       }
-      if (rd == 0) __syncthreads();   // staged twiddles visible (src loads already issued)
+      stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, tk.dst_prime), rank);
+      __syncthreads();   // staged twiddles visible
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (!CP::owns(0, q)) break;
+        if (MODE == FWD_PLAIN) x[q] = pol.from_canon(raw[q]);
+        else if (MODE == FWD_I64) x[q] = pol.from_signed((i64)raw[q]);
+        else x[q] = pol.from_lift(raw[q], ps, ps_half);
+      }
+    }
+#pragma unroll
+    for (int rd = 0; rd < CP::NR; ++rd) {
+      if (rd > 0) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (!CP::owns(rd, q)) break;
+          x[q] = sm[csw<CW>(CP::m_of(rd, gq, q), c)];
+        }
+      }
       col_butterflies<Pol, S1, true>(x, rd, gq, fetch_col, pol);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
@@ -394,7 +409,6 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
   const Pol pol(P);
-  stage_twiddles<LOGN, false>(tws, Pol::inv_table(R, tk.dst_prime), rank);
   auto fetch_col = [&](int r, int idx) { return tws[(N >> (r + 1)) + idx - 1]; };
   auto fetch_blk = [&](int r, int idx) {
     const int off = r == 3 ? 0 : r == 4 ? 256 : r == 5 ? 384 : 448;
@@ -402,18 +416,24 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   };
   const int t = threadIdx.x;
   const size_t base = (size_t)rank * TILE3;
-  HB_PDL_ENTRY();   // static prologue above; the row data below may be the previous kernel's
+  HB_PDL_ENTRY();   // the row data below may be the previous kernel's output
   // ---- block pass on tile `rank`: coalesced 16-byte loads into the
   // swizzled tile, stages 0..2 (contiguous 8), 3..6 (stride 8)
+  {   // input chunks in flight while the twiddles are staged
+    ulonglong2 in[TILE3 / 2 / THREADS3];
 #pragma unroll
-  for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-    const int k = t + i * THREADS3;
-    const ulonglong2 in = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base) + k);
-    if (tk.add2)   // inverse: verbatim copy of the input row (ModUp identity digit)
-      reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base)[k] = in;
-    const int pc = swz3_chunk(k);
-    sm[2 * pc] = pol.from_canon(in.x);
-    sm[2 * pc + 1] = pol.from_canon(in.y);
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i)
+      in[i] = __ldg(reinterpret_cast<const ulonglong2*>(tk.src + base) + t + i * THREADS3);
+    stage_twiddles<LOGN, false>(tws, Pol::inv_table(R, tk.dst_prime), rank);
+#pragma unroll
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+      const int k = t + i * THREADS3;
+      if (tk.add2)   // inverse: verbatim copy of the input row (ModUp identity digit)
+        reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base)[k] = in[i];
+      const int pc = swz3_chunk(k);
+      sm[2 * pc] = pol.from_canon(in[i].x);
+      sm[2 * pc + 1] = pol.from_canon(in[i].y);
+    }
   }
   __syncthreads();
   constexpr int N8 = N / 8;
