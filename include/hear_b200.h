@@ -80,6 +80,11 @@ int hb_ntt_kernels(hb_ring* ring, int count);
 /* 1 when the ring's modular arithmetic runs on the fp64 pipe (every prime
  * < 2^42 and HEAR_B200_INT_NTT unset), else 0.                              */
 int hb_ring_uses_f64(const hb_ring* ring);
+/* 1 when hb_ntt_fwd accepts mode 5 on this ring (the cluster-fused NTT):
+ * FWD_LIFT fused with the key-switch inner product, dst += NTT(lift(src)) *
+ * aux and add2 += NTT(lift(src)) * add with 64-bit atomic adds of canonical
+ * products (the caller reduces the sums afterwards).                         */
+int hb_ntt_fused_ks(const hb_ring* ring);
 /* Launch every library kernel with programmatic dependent launch (PDL:
  * the next kernel's CTAs are scheduled while the previous grid drains; each
  * kernel waits on griddepcontrol before touching its inputs) while `on`.

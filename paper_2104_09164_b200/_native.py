@@ -44,6 +44,7 @@ def lib():
         L.hb_ntt_inv.argtypes = [vp, vp, i32, vp]
         L.hb_ntt_kernels.argtypes = [vp, i32]
         L.hb_ring_uses_f64.argtypes = [vp]
+        L.hb_ntt_fused_ks.argtypes = [vp]
         L.hb_set_pdl.argtypes = [i32]
         L.hb_ks_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_longlong,
                                  ctypes.c_longlong, i32, i32, vp]
@@ -112,7 +113,7 @@ TENSOR_TASK = np.dtype([("a0", "<u8"), ("a1", "<u8"), ("b0", "<u8"), ("b1", "<u8
 CRT_TASK = np.dtype([("rows", "<u8"), ("out", "<u8")])
 
 # NTT fused modes (csrc/ntt.cu FwdMode)
-FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER = 0, 1, 2, 3, 4
+FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER, FWD_LIFT_KS = 0, 1, 2, 3, 4, 5
 # element-wise ops (csrc/ops.cu EwOp)
 EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PERM, \
     EW_SUB_SCALED, EW_PERM_ADD = range(10)

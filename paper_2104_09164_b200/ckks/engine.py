@@ -81,6 +81,16 @@ class _Ksk:
         self.ap = None
 
 
+class _Digits:
+    """Lazy ModUp: the INTT'd digit rows (coefficient form) and the input
+    rows, for the fused ModUp + inner product (ntt3 mode FWD_LIFT_KS) that
+    never materialises the [B, l+1, l+2, N] digit expansion."""
+
+    def __init__(self, coef: torch.Tensor, ptrs: np.ndarray):
+        self.coef, self.ptrs = coef, ptrs
+        self.shape = (coef.shape[0],)
+
+
 class KeyMaterial:
     def __init__(self):
         self.s_coeffs = None
@@ -134,6 +144,12 @@ class CkksBackend(BackendBase):
         # product (ks_gemm); smaller ones the per-job kernel (ks_inner2), which
         # has the lower latency at one or two clips
         self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "8"))
+        # opt-in (HEAR_B200_KS_FUSED=1): single-job key switches (relinearisation,
+        # rot_each) with the ModUp fused into the inner product in the cluster
+        # NTT (64-bit atomic accumulation, no digit expansion through HBM);
+        # bit-exact, measured 7 % slower on the bench step than ModUp + GEMM
+        self.ks_fused = (os.environ.get("HEAR_B200_KS_FUSED", "0") == "1"
+                         and bool(nat.lib().hb_ntt_fused_ks(self.ring.handle)))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -520,7 +536,7 @@ class CkksBackend(BackendBase):
                    d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
                    prime=self._row_primes(bsz, r))
         self.ring.tensor(t)
-        de = self._decompose(dr[:, 2], lvl)
+        de = self._decompose(dr[:, 2], lvl, lazy=bsz >= self.ks_gemm_min)
         out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
@@ -544,7 +560,7 @@ class CkksBackend(BackendBase):
 
     # ------------------------------------------------------------------ key switching
 
-    def _decompose(self, d, lvl: int) -> torch.Tensor:
+    def _decompose(self, d, lvl: int, lazy: bool = False):
         """Digits of d extended to chain rows 0..lvl plus the special prime:
         de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303).
 
@@ -565,6 +581,18 @@ class CkksBackend(BackendBase):
         rp = self.ring.row_ptrs
         coef = self.ring.empty(bsz, ndig)
         prim = self._row_primes(bsz, ndig)
+        if lazy:   # the caller's key switch runs the fused ModUp + inner product
+            self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                     dst_prime=prim, src_prime=prim))
+            return _Digits(coef, ptrs)
+        return self._lift_digits(coef, ptrs, lvl, inverse_done=False)
+
+    def _lift_digits(self, coef, ptrs, lvl: int, inverse_done: bool = True) -> torch.Tensor:
+        """The [B, l+1, l+2, N] digit expansion from INTT'd digits (ModUp)."""
+        bsz = ptrs.shape[0]
+        ndig, rows = lvl + 1, lvl + 2
+        rp = self.ring.row_ptrs
+        prim = self._row_primes(bsz, ndig)
         de = self.ring.empty(bsz, ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         src = np.repeat(rp(coef), rows)
@@ -573,10 +601,13 @@ class CkksBackend(BackendBase):
         dp = np.tile(gidx, bsz * ndig)
         ident = sp == np.tile(np.tile(np.arange(rows), ndig), bsz)
         lift = ~ident
-        # the inverse transform also copies each input row to its identity
-        # digit position of de (add2), so no separate copy launch
-        self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                 dst_prime=prim, src_prime=prim, add2=dst[ident]))
+        if inverse_done:
+            self._ew(nat.EW_COPY, dst[ident], ptrs.ravel(), primes=prim)
+        else:
+            # the inverse transform also copies each input row to its identity
+            # digit position of de (add2), so no separate copy launch
+            self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                     dst_prime=prim, src_prime=prim, add2=dst[ident]))
         self.ring.ntt_fwd(_tasks(nat.NTT_TASK, int(lift.sum()), src=src[lift], dst=dst[lift],
                                  src_prime=sp[lift], dst_prime=dp[lift]), nat.FWD_LIFT)
         return de
@@ -593,9 +624,17 @@ class CkksBackend(BackendBase):
         ndig, rows = lvl + 1, lvl + 2
         nj = len(jobs)
         rp = self.ring.row_ptrs
+        fused = False
+        if isinstance(de, _Digits):
+            offs0 = [job[4] if len(job) > 4 else 0 for job in jobs]
+            fused = (self.ks_fused and len(set(offs0)) == nj
+                     and all(job[1] is None or (job[0].bp is not None and self.preperm)
+                             for job in jobs))
+            if not fused:   # shared digit sets or gathered digits: materialise
+                de = self._lift_digits(de.coef, de.ptrs, lvl)
         ip = self.ring.empty(nj * bsz * 2, rows)
         ipr = rp(ip).reshape(nj, bsz, 2, rows)
-        der = rp(de).reshape(de.shape[0], ndig, rows)
+        der = None if fused else rp(de).reshape(de.shape[0], ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         parts = []
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
@@ -612,7 +651,7 @@ class CkksBackend(BackendBase):
             kb_t, ka_t = (key.bp, key.ap) if prepermuted else (key.b, key.a)
             kbr = rp(kb_t).reshape(kb_t.shape[0], key.lmax + 2)[0, krow]
             kar = rp(ka_t).reshape(ka_t.shape[0], key.lmax + 2)[0, krow]
-            parts.append(_tasks(
+            parts.append(None if fused else _tasks(
                 nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
                 out_a=ipr[j, 0, 1],
                 perm=perm.data_ptr() if perm is not None and not prepermuted else 0,
@@ -628,7 +667,9 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        if natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
+        if fused:
+            self._ks_fused(de, lvl, jobs, [natural[j] for j in range(nj)], ip, ipr, bsz)
+        elif natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
             # every natural-order inner product in ONE GEMM launch: a hoisted
             # group shares its digit set, rot_each / relinearisation jobs bring
             # their own (one output pair per tile)
@@ -732,6 +773,54 @@ class CkksBackend(BackendBase):
                         self._ew(nat.EW_ADD, dst.ravel(), dst.ravel(), post[j].ravel(),
                                  primes=np.tile(np.arange(r), bsz * 2))
         return res
+
+    def _ks_fused(self, dg: _Digits, lvl: int, jobs, keys, ip, ipr, bsz: int):
+        """Inner products of single-job key switches with the ModUp fused in
+        (ntt3 FWD_LIFT_KS): every (digit i, target row t != i) transform is
+        multiplied by the job's two key rows in the NTT epilogue and added to
+        the inner product rows with 64-bit atomics; the identity digit rows
+        contribute x_t * k[t][t] directly; one reduction canonicalises.
+        Same canonical inner product as the GEMM over the materialised digits
+        (modular arithmetic), without the 13x digit expansion through HBM."""
+        ndig, rows, n8 = lvl + 1, lvl + 2, np.uint64(8 * self.n)
+        nj = len(jobs)
+        rp = self.ring.row_ptrs
+        ip.zero_()
+        coefr = rp(dg.coef).reshape(dg.coef.shape[0], ndig)
+        offs = np.array([job[4] if len(job) > 4 else 0 for job in jobs])
+        gidx = np.array(list(range(lvl + 1)) + [self.S])
+        # key row pointers: kp[j, c, i, t] for digit i, target row t (krow)
+        kp = np.zeros((nj, 2, ndig, rows), dtype=np.uint64)
+        for j, (kb, ka, lmax) in enumerate(keys):
+            krow = np.array(list(range(lvl + 1)) + [lmax + 1], dtype=np.uint64)
+            for c, t in enumerate((kb, ka)):
+                kp[j, c] = (np.uint64(t.data_ptr())
+                            + (np.arange(ndig, dtype=np.uint64)[:, None] * np.uint64(lmax + 2)
+                               + krow[None, :]) * n8)
+        # identity digits: ip_c[j, b, i] = x[off_j + b, i] * k_c[i][i]
+        xs = np.stack([dg.ptrs[o:o + bsz] for o in offs])             # [nj, bsz, ndig]
+        diag = kp[:, :, np.arange(ndig), np.arange(ndig)]             # [nj, 2, ndig]
+        dst = ipr[:, :, :, :ndig]                                     # [nj, bsz, 2, ndig]
+        a = np.broadcast_to(xs[:, :, None, :], dst.shape)
+        b = np.broadcast_to(diag[:, None, :, :], dst.shape)
+        self._ew(nat.EW_MUL, dst.ravel(), np.ascontiguousarray(a).ravel(),
+                 np.ascontiguousarray(b).ravel(), primes=np.tile(np.arange(ndig), nj * bsz * 2))
+        # fused ModUp x key rows: tasks (j, b, i, t != i), target rows fastest
+        # (consecutive clusters share the source digit row, not the accumulator)
+        jj, bb, ii, tt = np.meshgrid(np.arange(nj), np.arange(bsz), np.arange(ndig),
+                                     np.arange(rows), indexing="ij")
+        keep = (ii != tt).ravel()
+        jj, bb, tt, ii = jj.ravel()[keep], bb.ravel()[keep], tt.ravel()[keep], ii.ravel()[keep]
+        t = _tasks(nat.NTT_TASK, len(jj), src=coefr[offs[jj] + bb, ii], src_prime=ii,
+                   dst_prime=gidx[tt], dst=ipr[jj, bb, 0, tt], add2=ipr[jj, bb, 1, tt],
+                   aux=kp[jj, 0, ii, tt], add=kp[jj, 1, ii, tt])
+        self.ring.ntt_fwd(t, nat.FWD_LIFT_KS)
+        # canonicalise the accumulated sums (< ndig * p < 2^64): Shoup by 1
+        m = nj * bsz * 2
+        pr = np.tile(gidx, m)
+        one_sh = np.array([(1 << 64) // p for p in self.ring.primes], dtype=np.uint64)
+        self._ew(nat.EW_MUL_SCALAR, rp(ip), rp(ip), primes=pr,
+                 scal=np.ones(m * rows, dtype=np.uint64), scal_sh=one_sh[pr])
 
     def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
         """Natural-order key-switch inner products of several jobs as one
@@ -927,7 +1016,7 @@ class CkksBackend(BackendBase):
                 c1 = np.concatenate([
                     self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
                     for i in chunk])
-                de = self._decompose(c1, lvl)
+                de = self._decompose(c1, lvl, lazy=bsz >= self.ks_gemm_min)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -951,7 +1040,8 @@ class CkksBackend(BackendBase):
                 chunk = idx[c0:c0 + step]
                 rows = [self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)
                         for i in chunk]
-                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl)
+                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl,
+                                     lazy=bsz >= self.ks_gemm_min)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -981,7 +1071,8 @@ class CkksBackend(BackendBase):
                     b0=xr[:, :, 0].ravel(), b1=xr[:, :, 1].ravel(), d0=dr[:, :, 0].ravel(),
                     d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
                     prime=self._row_primes(k * bsz, r)))
-                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl)
+                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl,
+                                     lazy=bsz >= self.ks_gemm_min)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de

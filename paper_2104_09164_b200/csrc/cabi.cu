@@ -26,6 +26,7 @@ namespace hb {
 cudaError_t launch_ntt_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
 cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 int ntt_kernels(const HbRing&, int);
+bool ntt3_supported(const HbRing& R);
 cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
@@ -303,6 +304,8 @@ int hb_set_pdl(int on) {
 }
 
 int hb_ring_uses_f64(const hb_ring* r) { return r && r->dev.use_f64 ? 1 : 0; }
+
+int hb_ntt_fused_ks(const hb_ring* r) { return r && ntt3_supported(r->dev) ? 1 : 0; }
 
 int hb_ew(hb_ring* r, int op, const void* tasks, int count, void* stream) {
   cudaError_t e = launch_ew(op, (const HbEwTask*)tasks, count, r->dev.primes, r->dev.n,

@@ -248,11 +248,12 @@ def test_hoisted_rotations_fast_hear_vs_oracle(env):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("gemm_min", ["1", "1000"])
-def test_rot_each_and_relin_batched_vs_oracle(gemm_min):
+@pytest.mark.parametrize("gemm_min,fused", [("1", "0"), ("1000", "0"), ("1", "1")])
+def test_rot_each_and_relin_batched_vs_oracle(gemm_min, fused):
     """Batched key switches with a digit set per job (rot_each over several
     handles: one GEMM launch, one output pair per tile) and relinearisation,
-    GEMM and per-job inner products, against the CPU oracle at N = 2^14."""
+    GEMM, per-job and fused ModUp + inner products (ntt3 FWD_LIFT_KS),
+    against the CPU oracle at N = 2^14."""
     import os
     from oracle.cpu_engine import OracleCkks
     from paper_2104_09164_b200.backend import Ct
@@ -266,10 +267,13 @@ def test_rot_each_and_relin_batched_vs_oracle(gemm_min):
         _ORACLE["cpu"] = cpu
     cpu = _ORACLE["cpu"]
     os.environ["HEAR_B200_KS_GEMM_MIN"] = gemm_min
+    os.environ["HEAR_B200_KS_FUSED"] = fused
     try:
         gpu = CkksBackend(ps, seed=11)
     finally:
         del os.environ["HEAR_B200_KS_GEMM_MIN"]
+        del os.environ["HEAR_B200_KS_FUSED"]
+    assert gpu.ks_fused == (fused == "1")
     gpu.ensure_rotation_keys({a: 12 for a in amounts})
     lvl = 9
     cts = [[rand_ct(ps, lvl, 70 + 3 * h + i) for i in range(2)] for h in range(2)]
