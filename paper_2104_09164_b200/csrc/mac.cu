@@ -183,6 +183,19 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * prime + k);
   }
   const size_t rj = rj0 + lane;
+  auto value = [&](int o, int b) {
+    return C3 ? recombine3(acc[o][b][0], acc[o][b][1], acc[o][b][2], cc, p, pinv)
+              : fmod_canon(acc[o][b][0], p, pinv);
+  };
+  if (oc + OB <= O && bc + CB <= BC) {   // full tile (the common case): no bounds checks
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      u64* d = g.dsts[oc + os + o] + rj;
+#pragma unroll
+      for (int b = 0; b < TB; ++b) d[(size_t)(bc + bs + b) * g.dst_bstride] = value(o, b);
+    }
+    return;
+  }
 #pragma unroll
   for (int o = 0; o < TO; ++o) {
     const int oo = oc + os + o;
@@ -192,9 +205,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     for (int b = 0; b < TB; ++b) {
       const int bb = bc + bs + b;
       if (bb >= BC) continue;
-      d[(size_t)bb * g.dst_bstride + rj] =
-          C3 ? recombine3(acc[o][b][0], acc[o][b][1], acc[o][b][2], cc, p, pinv)
-             : fmod_canon(acc[o][b][0], p, pinv);
+      d[(size_t)bb * g.dst_bstride + rj] = value(o, b);
     }
   }
 }
