@@ -150,6 +150,10 @@ class CkksBackend(BackendBase):
         # bit-exact, measured 7 % slower on the bench step than ModUp + GEMM
         self.ks_fused = (os.environ.get("HEAR_B200_KS_FUSED", "0") == "1"
                          and bool(nat.lib().hb_ntt_fused_ks(self.ring.handle)))
+        # cluster NTT: inverse transforms whose rows feed ModUp / ModDown /
+        # rescale write centred lifts as doubles (task scal = 1) and the
+        # forward transforms read them with src_prime = -1: one lift per row
+        self.lift_once = bool(nat.lib().hb_ntt_fused_ks(self.ring.handle))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -583,7 +587,8 @@ class CkksBackend(BackendBase):
         prim = self._row_primes(bsz, ndig)
         if lazy:   # the caller's key switch runs the fused ModUp + inner product
             self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                     dst_prime=prim, src_prime=prim))
+                                     dst_prime=prim, src_prime=prim,
+                                     scal=int(self.lift_once)))
             return _Digits(coef, ptrs)
         return self._lift_digits(coef, ptrs, lvl, inverse_done=False)
 
@@ -607,9 +612,11 @@ class CkksBackend(BackendBase):
             # the inverse transform also copies each input row to its identity
             # digit position of de (add2), so no separate copy launch
             self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                     dst_prime=prim, src_prime=prim, add2=dst[ident]))
+                                     dst_prime=prim, src_prime=prim, add2=dst[ident],
+                                     scal=int(self.lift_once)))
         self.ring.ntt_fwd(_tasks(nat.NTT_TASK, int(lift.sum()), src=src[lift], dst=dst[lift],
-                                 src_prime=sp[lift], dst_prime=dp[lift]), nat.FWD_LIFT)
+                                 src_prime=-1 if self.lift_once else sp[lift],
+                                 dst_prime=dp[lift]), nat.FWD_LIFT)
         return de
 
     def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None) -> list:
@@ -703,7 +710,8 @@ class CkksBackend(BackendBase):
         spc = self.ring.empty(m)
         sprime = np.full(m, self.S)
         self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=iprows[:, lvl + 1], dst=rp(spc),
-                                 dst_prime=sprime, src_prime=sprime))
+                                 dst_prime=sprime, src_prime=sprime, scal=int(self.lift_once)))
+        src_p = -1 if self.lift_once else self.S
         out = self.ring.empty(m, r)
         if late and len(late) == nj and self.ring.two_pass:
             # pre-permuted rotations: ModDown of the natural-order inner product
@@ -718,7 +726,7 @@ class CkksBackend(BackendBase):
                     addn[j, :, 0] = c0
             t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out),
                        aux=iprows[:, :r].ravel(),
-                       src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
+                       src_prime=src_p, dst_prime=np.tile(np.arange(r), m),
                        scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
                        add=addn.ravel(), perm=inv.ravel(), add2=post.ravel())
             self.ring.ntt_fwd(t, nat.FWD_MODDOWN_SCATTER)
@@ -726,7 +734,7 @@ class CkksBackend(BackendBase):
             return [out[j] for j in range(nj)]
         t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(rp(spc), r), dst=rp(out),
                    aux=iprows[:, :r].ravel(),
-                   src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
+                   src_prime=src_p, dst_prime=np.tile(np.arange(r), m),
                    scal=np.tile(self._pinv[:r], m), scal_sh=np.tile(self._pinv_sh[:r], m),
                    add=add.ravel(), perm=perms.ravel(),
                    add2=(post.ravel() if has_post and not late else 0))
@@ -811,7 +819,8 @@ class CkksBackend(BackendBase):
                                      np.arange(rows), indexing="ij")
         keep = (ii != tt).ravel()
         jj, bb, tt, ii = jj.ravel()[keep], bb.ravel()[keep], tt.ravel()[keep], ii.ravel()[keep]
-        t = _tasks(nat.NTT_TASK, len(jj), src=coefr[offs[jj] + bb, ii], src_prime=ii,
+        t = _tasks(nat.NTT_TASK, len(jj), src=coefr[offs[jj] + bb, ii],
+                   src_prime=-1 if self.lift_once else ii,
                    dst_prime=gidx[tt], dst=ipr[jj, bb, 0, tt], add2=ipr[jj, bb, 1, tt],
                    aux=kp[jj, 0, ii, tt], add=kp[jj, 1, ii, tt])
         self.ring.ntt_fwd(t, nat.FWD_LIFT_KS)
@@ -987,12 +996,13 @@ class CkksBackend(BackendBase):
             rows = rows.reshape(k * bsz * 2, lvl + 1)
             topc = self.ring.empty(k * bsz * 2)
             self.ring.ntt_inv(_tasks(nat.NTT_TASK, k * bsz * 2, src=rows[:, lvl],
-                                     dst=rp(topc), dst_prime=lvl, src_prime=lvl))
+                                     dst=rp(topc), dst_prime=lvl, src_prime=lvl,
+                                     scal=int(self.lift_once)))
             res = self.ring.empty(k, bsz, 2, lvl)
             inv, inv_sh = self._resc[lvl]
             m = k * bsz * 2
             t = _tasks(nat.NTT_TASK, m * lvl, src=np.repeat(rp(topc), lvl), dst=rp(res),
-                       aux=rows[:, :lvl].ravel(), src_prime=lvl,
+                       aux=rows[:, :lvl].ravel(), src_prime=-1 if self.lift_once else lvl,
                        dst_prime=np.tile(np.arange(lvl), m), scal=np.tile(inv, m),
                        scal_sh=np.tile(inv_sh, m))
             self.ring.ntt_fwd(t, nat.FWD_MODDOWN)

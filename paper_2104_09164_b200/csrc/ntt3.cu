@@ -223,8 +223,12 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   };
   const int t = threadIdx.x;
   u64 ps = 0, ps_half = 0;
-  if (MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER ||
-      MODE == FWD_LIFT_KS) {
+  // src_prime < 0: the source row already holds centred lifts as doubles
+  // (written by the inverse transform, task scal = 1), lifted once for all
+  // target primes instead of once per target row
+  const bool lifted = tk.src_prime < 0;
+  if ((MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER ||
+       MODE == FWD_LIFT_KS) && !lifted) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
@@ -248,6 +252,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         if (!CP::owns(0, q)) break;
         if (MODE == FWD_PLAIN) x[q] = pol.from_canon(raw[q]);
         else if (MODE == FWD_I64) x[q] = pol.from_signed((i64)raw[q]);
+        else if (lifted) x[q] = fmod_reduce(__longlong_as_double((long long)raw[q]), pol.p, pol.pinv);
         else x[q] = pol.from_lift(raw[q], ps, ps_half);
       }
     }
@@ -435,6 +440,8 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   const HbNttTask tk = tasks[blockIdx.x / CL];
   const HbPrime P = R.primes[tk.dst_prime];
   const Pol pol(P);
+  const bool lifted_out = tk.scal == 1;
+  const u64 lift_half = P.p >> 1;
   auto fetch_col = [&](int r, int idx) { return tws[(N >> (r + 1)) + idx - 1]; };
   auto fetch_blk = [&](int r, int idx) {
     const int off = r == 3 ? 0 : r == 4 ? 256 : r == 5 ? 384 : 448;
@@ -534,7 +541,15 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
     for (int q = 0; q < 16; ++q) {
       if (!CP::owns(rd, q)) break;
       const int m = CP::m_of(rd, gq, q);
-      if (last) tk.dst[(size_t)m * 128 + cg0 + c] = pol.inv_final(x[q]);
+      if (last) {
+        const u64 v = pol.inv_final(x[q]);
+        // scal = 1: store the centred lift as a double (the next transform's
+        // source under other primes: ModUp digits, ModDown / rescale rows)
+        tk.dst[(size_t)m * 128 + cg0 + c] =
+            lifted_out ? (u64)__double_as_longlong(v > lift_half ? u64_to_f(v) - pol.p
+                                                                 : u64_to_f(v))
+                       : v;
+      }
       else sm[csw<CW>(m, c)] = pol.inv_round_end(x[q]);
     }
     if (!last) __syncthreads();
