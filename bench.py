@@ -186,6 +186,9 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     m, r = bsz * 2, lvl + 1
     g = torch.Generator(device=be.dev).manual_seed(1)
     src = be.ring.empty(m).random_(0, 1 << 30, generator=g)
+    lifted = getattr(be, "lift_once", False)
+    if lifted:   # the engine's source rows: centred lifts stored as doubles
+        src = (src - (1 << 29)).to(torch.float64).view(torch.int64)
     aux = be.ring.empty(m, r).random_(0, 1 << 30, generator=g)
     c0 = be.ring.empty(bsz, r).random_(0, 1 << 30, generator=g)
     out = be.ring.empty(m, r)
@@ -193,7 +196,8 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     add = np.zeros((bsz, 2, r), dtype=np.uint64)
     add[:, 0] = be.ring.row_ptrs(c0).reshape(bsz, r)
     t = _tasks(nat.NTT_TASK, m * r, src=np.repeat(be.ring.row_ptrs(src), r),
-               dst=be.ring.row_ptrs(out), aux=be.ring.row_ptrs(aux), src_prime=be.S,
+               dst=be.ring.row_ptrs(out), aux=be.ring.row_ptrs(aux),
+               src_prime=-1 if lifted else be.S,
                dst_prime=np.tile(np.arange(r), m), scal=np.tile(be._pinv[:r], m),
                scal_sh=np.tile(be._pinv_sh[:r], m), add=add.ravel(),
                perm=np.full(m * r, inv.data_ptr(), dtype=np.uint64))

@@ -540,7 +540,7 @@ class CkksBackend(BackendBase):
                    d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
                    prime=self._row_primes(bsz, r))
         self.ring.tensor(t)
-        de = self._decompose(dr[:, 2], lvl, lazy=bsz >= self.ks_gemm_min)
+        de = self._decompose(dr[:, 2], lvl, lazy=self.ks_fused and bsz >= self.ks_gemm_min)
         out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
@@ -1026,7 +1026,7 @@ class CkksBackend(BackendBase):
                 c1 = np.concatenate([
                     self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
                     for i in chunk])
-                de = self._decompose(c1, lvl, lazy=bsz >= self.ks_gemm_min)
+                de = self._decompose(c1, lvl, lazy=self.ks_fused and bsz >= self.ks_gemm_min)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1051,7 +1051,7 @@ class CkksBackend(BackendBase):
                 rows = [self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)
                         for i in chunk]
                 de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl,
-                                     lazy=bsz >= self.ks_gemm_min)
+                                     lazy=self.ks_fused and bsz >= self.ks_gemm_min)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1082,7 +1082,7 @@ class CkksBackend(BackendBase):
                     d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
                     prime=self._row_primes(k * bsz, r)))
                 de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl,
-                                     lazy=bsz >= self.ks_gemm_min)
+                                     lazy=self.ks_fused and bsz >= self.ks_gemm_min)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de
