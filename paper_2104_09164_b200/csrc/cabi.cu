@@ -29,7 +29,7 @@ int ntt_kernels(const HbRing&, int);
 bool ntt3_supported(const HbRing& R);
 cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
-cudaError_t launch_tensor(const void*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_tensor(const void*, int, const HbPrime*, int, bool, cudaStream_t);
 cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
                                bool, cudaStream_t);
 cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
@@ -333,7 +333,8 @@ int hb_sum(hb_ring* r, const void* tasks, int count, const void* srcs, void* str
 }
 
 int hb_tensor(hb_ring* r, const void* tasks, int count, void* stream) {
-  cudaError_t e = launch_tensor(tasks, count, r->dev.primes, r->dev.n, (cudaStream_t)stream);
+  cudaError_t e = launch_tensor(tasks, count, r->dev.primes, r->dev.n, r->dev.use_f64 != 0,
+                                (cudaStream_t)stream);
   return e ? fail(e, "hb_tensor") : 0;
 }
 

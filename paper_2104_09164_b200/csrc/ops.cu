@@ -186,11 +186,50 @@ k_tensor(const HbTensorTask* __restrict__ tasks, int ntasks, const HbPrime* __re
   }
 }
 
-cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, int n,
+// fp64-pipe tensor product (rings with every prime < 2^42): the four
+// products as fmod_mul, one canonicalisation each -- same residues as the
+// 128-bit integer products above.
+__global__ void __launch_bounds__(EW_THREADS)
+k_tensor_f64(const HbTensorTask* __restrict__ tasks, int ntasks,
+             const HbPrime* __restrict__ primes, int n) {
+  HB_PDL_ENTRY();
+  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
+    const HbTensorTask tk = tasks[t];
+    const HbPrime P = primes[tk.prime];
+    const double p = P.pd, pinv = P.pinv;
+    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
+    if (j >= n) continue;
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(tk.a0 + j);
+    const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(tk.a1 + j);
+    const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(tk.b0 + j);
+    const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(tk.b1 + j);
+    const double x0[2] = {u64_to_f(a0.x), u64_to_f(a0.y)};
+    const double x1[2] = {u64_to_f(a1.x), u64_to_f(a1.y)};
+    const double y0[2] = {u64_to_f(b0.x), u64_to_f(b0.y)};
+    const double y1[2] = {u64_to_f(b1.x), u64_to_f(b1.y)};
+    u64 r0[2], r1[2], r2[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double q0 = y0[e] * pinv, q1 = y1[e] * pinv;
+      r0[e] = fmod_canon(fmod_mul(x0[e], y0[e], q0, p), p, pinv);
+      r1[e] = fmod_canon(fmod_mul(x0[e], y1[e], q1, p) + fmod_mul(x1[e], y0[e], q0, p), p, pinv);
+      r2[e] = fmod_canon(fmod_mul(x1[e], y1[e], q1, p), p, pinv);
+    }
+    *reinterpret_cast<ulonglong2*>(tk.d0 + j) = make_ulonglong2(r0[0], r0[1]);
+    *reinterpret_cast<ulonglong2*>(tk.d1 + j) = make_ulonglong2(r1[0], r1[1]);
+    *reinterpret_cast<ulonglong2*>(tk.d2 + j) = make_ulonglong2(r2[0], r2[1]);
+  }
+}
+
+cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, int n, bool f64,
                           cudaStream_t st) {
   if (ntasks <= 0) return cudaSuccess;
-  (void)hb_launch(k_tensor, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, 
-      reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
+  if (f64)
+    (void)hb_launch(k_tensor_f64, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st,
+                    reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
+  else
+    (void)hb_launch(k_tensor, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st,
+                    reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
   return cudaGetLastError();
 }
 
