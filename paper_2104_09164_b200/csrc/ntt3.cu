@@ -192,10 +192,16 @@ HB_DEV void stage_twiddles(HbTwD* tws, const HbTwD* tab, int rank) {
         idx = (N >> (r + 1)) + rank * (4096 >> (r + 1)) + (kb - off);
       }
     }
-    const double2 w = __ldg(reinterpret_cast<const double2*>(tab + idx));
-    tws[k] = HbTwD{w.x, w.y};
+    // asynchronous 16-byte copy (LDGSTS): no register round trip, no STS
+    // stall on the load; completed by tws_wait() before the first use
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(tws + k)),
+                 "l"(tab + idx)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
+
+HB_DEV void tws_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // Forward.
@@ -246,6 +252,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         raw[q] = __ldg(tk.src + (size_t)CP::m_of(0, gq, q) * 128 + cg0 + c);
       }
       stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, tk.dst_prime), rank);
+      tws_wait();
       __syncthreads();   // staged twiddles visible
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
@@ -468,6 +475,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
       sm[2 * pc + 1] = pol.from_canon(in[i].y);
     }
   }
+  tws_wait();
   __syncthreads();
   constexpr int N8 = N / 8;
   const HbTwD* t3 = R.tw3_inv + (size_t)tk.dst_prime * N;
