@@ -459,7 +459,21 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   HB_PDL_ENTRY();   // the row data below may be the previous kernel's output
   // ---- block pass on tile `rank`: coalesced 16-byte loads into the
   // swizzled tile, stages 0..2 (contiguous 8), 3..6 (stride 8)
-  {   // input chunks in flight while the twiddles are staged
+  // input tile: raw residues straight into the swizzled smem tile with
+  // cp.async (converted when read), unless the row is also copied out (ModUp
+  // identity digit: through registers)
+  const bool raw_tile = tk.add2 == nullptr;
+  if (raw_tile) {
+    const uint32_t sm0 = smem_addr(sm);
+#pragma unroll
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+      const int k = t + i * THREADS3;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm0 + 16u * swz3_chunk(k)),
+                   "l"(tk.src + base + 2 * k)
+                   : "memory");
+    }
+    stage_twiddles<LOGN, false>(tws, Pol::inv_table(R, tk.dst_prime), rank);
+  } else {   // input chunks in flight while the twiddles are staged
     ulonglong2 in[TILE3 / 2 / THREADS3];
 #pragma unroll
     for (int i = 0; i < TILE3 / 2 / THREADS3; ++i)
@@ -468,8 +482,8 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
     for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
       const int k = t + i * THREADS3;
-      if (tk.add2)   // inverse: verbatim copy of the input row (ModUp identity digit)
-        reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base)[k] = in[i];
+      // inverse: verbatim copy of the input row (ModUp identity digit)
+      reinterpret_cast<ulonglong2*>(const_cast<u64*>(tk.add2) + base)[k] = in[i];
       const int pc = swz3_chunk(k);
       sm[2 * pc] = pol.from_canon(in[i].x);
       sm[2 * pc + 1] = pol.from_canon(in[i].y);
@@ -497,6 +511,10 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
       const int pc = swz3_chunk((e0 >> 1) + v);
       x[2 * v] = sm[2 * pc];
       x[2 * v + 1] = sm[2 * pc + 1];
+      if (raw_tile) {   // canonical residues landed raw: convert here
+        x[2 * v] = pol.from_canon((u64)__double_as_longlong(x[2 * v]));
+        x[2 * v + 1] = pol.from_canon((u64)__double_as_longlong(x[2 * v + 1]));
+      }
     }
     inv_group_f<Pol, 3>(x, 0, (rank * 32 + b2) * 16 + G8, fetch_fine, pol);
 #pragma unroll
