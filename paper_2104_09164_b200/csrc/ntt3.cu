@@ -244,23 +244,30 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   {
     const int c = t % CW, gq = t / CW;
     V x[16];
-    {   // round-0 operands: raw loads in flight while the twiddles are staged
-      u64 raw[16];
+    {   // the column slice lands raw in the swizzled smem tile by cp.async
+        // (16-byte column pairs; csw keeps pairs adjacent) while the twiddles
+        // are staged; round 0 converts on read
+      const uint32_t sm0 = smem_addr(sm);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if (!CP::owns(0, q)) break;
-        raw[q] = __ldg(tk.src + (size_t)CP::m_of(0, gq, q) * 128 + cg0 + c);
+      for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+        const int k = t + i * THREADS3;
+        const int m = k / (CW / 2), cp2 = 2 * (k % (CW / 2));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         sm0 + 8u * csw<CW>(m, cp2)),
+                     "l"(tk.src + (size_t)m * 128 + cg0 + cp2)
+                     : "memory");
       }
       stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, tk.dst_prime), rank);
       tws_wait();
-      __syncthreads();   // staged twiddles visible
+      __syncthreads();   // column slice and staged twiddles visible
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         if (!CP::owns(0, q)) break;
-        if (MODE == FWD_PLAIN) x[q] = pol.from_canon(raw[q]);
-        else if (MODE == FWD_I64) x[q] = pol.from_signed((i64)raw[q]);
-        else if (lifted) x[q] = fmod_reduce(__longlong_as_double((long long)raw[q]), pol.p, pol.pinv);
-        else x[q] = pol.from_lift(raw[q], ps, ps_half);
+        const u64 raw = (u64)__double_as_longlong(sm[csw<CW>(CP::m_of(0, gq, q), c)]);
+        if (MODE == FWD_PLAIN) x[q] = pol.from_canon(raw);
+        else if (MODE == FWD_I64) x[q] = pol.from_signed((i64)raw);
+        else if (lifted) x[q] = fmod_reduce(__longlong_as_double((long long)raw), pol.p, pol.pinv);
+        else x[q] = pol.from_lift(raw, ps, ps_half);
       }
     }
 #pragma unroll
