@@ -48,7 +48,18 @@ constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
 // local buffer, receive buffer, staged twiddles (TW3 x 16 B), 2 mbarriers
 template <int LOGN>
-constexpr int smem3() { return 2 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
+__host__ __device__ constexpr int smem3() { return 2 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
+#ifndef HB_NTT3_C0BUF
+#define HB_NTT3_C0BUF 0
+#endif
+// -DHB_NTT3_C0BUF=1: rotation ModDown (scatter) gets one more 32 KB tile so
+// the c0 addend is TMA-prefetched with x_r instead of loaded in the epilogue
+// (the epilogue's top stall); measured 12 % slower: 106 KB of smem leaves
+// two CTAs per SM instead of three
+template <int LOGN, int MODE>
+__host__ __device__ constexpr int smem3f() {
+  return smem3<LOGN>() + ((HB_NTT3_C0BUF && MODE == 4) ? TILE3 * 8 + 16 : 0);
+}
 #ifndef HB_NTT3_MINB
 #define HB_NTT3_MINB 3
 #endif
@@ -111,6 +122,20 @@ HB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar)
 // fire-and-forget 64-bit add to global memory (no return value: RED)
 HB_DEV void red_add_u64(const u64* p, u64 v) {
   asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// a second bulk copy on a barrier already armed for its bytes
+HB_DEV void bulk_g2s_more(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t d = smem_addr(dst), b = smem_addr(mbar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+HB_DEV void mbar_expect(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)),
+               "r"(bytes)
+               : "memory");
 }
 HB_DEV void mbar_wait0(uint64_t* mbar) {
   const uint32_t a = smem_addr(mbar);
@@ -217,6 +242,9 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
+  constexpr bool C0BUF = HB_NTT3_C0BUF && MODE == FWD_MODDOWN_SCATTER;
+  u64* c0buf = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(smraw3) +
+                                      ((smem3<LOGN>() + 15) & ~15));
   xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
@@ -307,7 +335,15 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     // the column slice is consumed: prefetch the epilogue's x_r tile into it
     // (TMA bulk copy) while the block pass runs
     __syncthreads();
-    if (t == 0) bulk_g2s(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
+    if (t == 0) {
+      if (C0BUF && tk.add) {   // x_r and the c0 addend on one barrier
+        mbar_expect(mbar + 1, 2 * TILE3 * 8);
+        bulk_g2s_more(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
+        bulk_g2s_more(c0buf, tk.add + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
+      } else {
+        bulk_g2s(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
+      }
+    }
   }
   mbar_wait0(mbar);
   // ---- block pass over blocks [rank*32, rank*32 + 32)
@@ -401,7 +437,8 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
           a0 = __ldg(tk.add + pp.x);
           a1 = __ldg(tk.add + pp.y);
         } else {
-          const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
+          const ulonglong2 a2 = C0BUF ? *reinterpret_cast<const ulonglong2*>(c0buf + 2 * k)
+                                      : __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
           a0 = a2.x;
           a1 = a2.y;
         }
@@ -592,10 +629,11 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
 template <int LOGN, int MODE>
 cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int CL = (1 << LOGN) / TILE3;
+  constexpr int FWDSMEM = smem3f<LOGN, MODE>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * CL);
   cfg.blockDim = dim3(THREADS3);
-  cfg.dynamicSmemBytes = smem3<LOGN>();
+  cfg.dynamicSmemBytes = FWDSMEM;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -607,7 +645,7 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.attrs = at;
   cfg.numAttrs = g_hb_pdl ? 2 : 1;
   static int smem_cur = 0;
-  cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(smem3<LOGN>()), &smem_cur);
+  cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(FWDSMEM), &smem_cur);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_fwd<PolF64, LOGN, MODE>, tasks, R);
 }
