@@ -120,11 +120,14 @@ int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* d
  * with K = keys[..] + r*N for r < rows-1 and K = keys_last[..] (the key's
  * special row) and the special prime prime_last for r = rows-1.  de is
  * [ndig] row-block base pointers shared by every job, or [nout/2][ndig]
- * (each job its own digits) when de_per_job.  Pointer tables live in device
- * memory.  fp64 rings only.                                                 */
+ * (each job its own digits) when de_per_job.  last_term_bstride != 0: the
+ * last term has its own clip stride (a rotation's c0 against rows of P mod
+ * q_r, folding the ModDown addend into the inner product).  Pointer tables
+ * live in device memory.  fp64 rings only.                                  */
 int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* keys_last,
                const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
-               long long dst_bstride, int prime_last, int de_per_job, void* stream);
+               long long dst_bstride, int prime_last, int de_per_job,
+               long long last_term_bstride, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);

@@ -47,7 +47,7 @@ def lib():
         L.hb_ntt_fused_ks.argtypes = [vp]
         L.hb_set_pdl.argtypes = [i32]
         L.hb_ks_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_longlong,
-                                 ctypes.c_longlong, i32, i32, vp]
+                                 ctypes.c_longlong, i32, i32, ctypes.c_longlong, vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_mac.argtypes = [vp, vp, i32, vp, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]

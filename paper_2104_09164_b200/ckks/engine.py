@@ -144,6 +144,10 @@ class CkksBackend(BackendBase):
         # product (ks_gemm); smaller ones the per-job kernel (ks_inner2), which
         # has the lower latency at one or two clips
         self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "8"))
+        # opt-in (HEAR_B200_FOLD_C0=1): rotations through the GEMM fold their c0
+        # into the inner product (P c0 as one more term) instead of the ModDown
+        # epilogue's addend load; bit-exact, measured 0.4 % slower
+        self.fold_c0 = os.environ.get("HEAR_B200_FOLD_C0", "0") == "1"
         # opt-in (HEAR_B200_KS_FUSED=1): single-job key switches (relinearisation,
         # rot_each) with the ModUp fused into the inner product in the cluster
         # NTT (64-bit atomic accumulation, no digit expansion through HBM);
@@ -692,7 +696,13 @@ class CkksBackend(BackendBase):
                 # contiguous, so it is one (b, a) GEMM over all their clips
                 self._ks_gemm(der, lvl, keys[:1], ipr[js[:1]], bsz * len(js), offs[:1])
             else:
-                self._ks_gemm(der, lvl, keys, ipr[js], bsz, offs)
+                # rotations on pre-permuted keys: fold c0 into the inner
+                # product as one more GEMM term (P c0 on the b rows), so the
+                # ModDown epilogue loads no addend
+                c0s = self._foldable_c0(late, js, bsz) if self.fold_c0 else None
+                self._ks_gemm(der, lvl, keys, ipr[js], bsz, offs, c0s)
+                if c0s is not None:
+                    late = [(j, perm, None) for j, perm, _ in late]
             rest = [parts[j] for j in range(nj) if j not in natural]
             if rest:
                 self.ring.ks_inner2(np.concatenate(rest), bsz)
@@ -831,7 +841,38 @@ class CkksBackend(BackendBase):
         self._ew(nat.EW_MUL_SCALAR, rp(ip), rp(ip), primes=pr,
                  scal=np.ones(m * rows, dtype=np.uint64), scal_sh=one_sh[pr])
 
-    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
+    def _foldable_c0(self, late, js, bsz: int):
+        """Per GEMM job, (row-0 pointer, clip stride in elements) of the c0 to
+        fold into its inner product, or None when some job cannot fold (not a
+        pre-permuted rotation, no c0, or clips not uniformly strided)."""
+        c0 = {j: c for j, _, c in late}
+        out = []
+        for j in js:
+            c = c0.get(j)
+            if c is None:
+                return None
+            c = np.asarray(c, dtype=np.uint64).reshape(bsz, -1)
+            if bsz > 1:
+                d = np.diff(c[:, 0].astype(np.int64))
+                if not np.all(d == d[0]) or d[0] % 8:
+                    return None
+                stride = int(d[0]) // 8
+            else:
+                stride = 0
+            out.append((int(c[0, 0]), stride))
+        strides = {st for _, st in out}
+        return out if len(strides) == 1 else None
+
+    def _fold_rows(self):
+        """[L+2, N] rows of P mod q_r (special row 0) and an all-zero block."""
+        if getattr(self, "_pmod_rows", None) is None:
+            rows = np.zeros((self.L + 2, self.n), dtype=np.uint64)
+            rows[:self.L + 1] = self._pmod[:, None]
+            self._pmod_rows = self._dev(rows)
+            self._zero_rows = self.ring.zeros(self.L + 2)
+        return self._pmod_rows, self._zero_rows
+
+    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs, c0s=None):
         """Natural-order key-switch inner products of several jobs as one
         per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): terms = digits,
         outputs = (job, component), the special row (its own prime and key
@@ -849,12 +890,27 @@ class CkksBackend(BackendBase):
                 kps.append(base + np.uint64(lmax + 1) * n8)
             dp.extend([ipr[j, 0, 0, 0], ipr[j, 0, 1, 0]])
         kp, kps, dp = np.stack(kp), np.stack(kps), np.array(dp, dtype=np.uint64)
-        if len(set(offs)) == 1:
+        shared = len(set(offs)) == 1
+        if shared:
             dep = der[offs[0], :, 0]                    # [ndig] row 0 of each digit
         else:
             dep = np.stack([der[o, :, 0] for o in offs])   # [njobs, ndig]
+        last_bs = 0
+        if c0s is not None and (not shared or len({c for c, _ in c0s}) == 1):
+            # extra term: c0 x (P mod q_r) on b outputs, x 0 on a outputs
+            pm, zr = self._fold_rows()
+            pmp, zrp = np.uint64(pm.data_ptr()), np.uint64(zr.data_ptr())
+            kcol = np.array([pmp, zrp] * len(keys), dtype=np.uint64)[:, None]
+            kp = np.concatenate([kp, kcol], axis=1)
+            kps = np.concatenate([kps, np.full((len(kp), 1), zrp, dtype=np.uint64)], axis=1)
+            c0p = np.array([c for c, _ in c0s], dtype=np.uint64)
+            dep = (np.concatenate([dep, c0p[:1]]) if shared
+                   else np.concatenate([dep, c0p[:, None]], axis=1))
+            last_bs = c0s[0][1] if bsz > 1 else 1
+        elif c0s is not None:
+            raise ValueError("shared digit set with different c0 rows")
         self.ring.ks_gemm(dep, kp, kps, dp, rows, bsz, ndig * rows * self.n,
-                          2 * rows * self.n, self.S)
+                          2 * rows * self.n, self.S, last_bs)
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)

@@ -265,7 +265,8 @@ class RingContext:
         return bool(self._lib.hb_ring_uses_f64(self.handle))
 
     def ks_gemm(self, de: np.ndarray, keys: np.ndarray, keys_last: np.ndarray, dsts: np.ndarray,
-                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int):
+                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int,
+                last_term_bstride: int = 0):
         """Natural-order key-switch inner products as one per-coefficient GEMM
         (csrc/mac.cu launch_ks_gemm): de [ndig] shared or [njobs, ndig] per job,
         keys / keys_last [nout, ndig], dsts [nout]."""
@@ -280,7 +281,7 @@ class RingContext:
             o3 = o2 + 8 * keys.size
             nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
                                            de_bstride, dst_bstride, prime_last, per_job,
-                                           self.stream), "ks_gemm")
+                                           last_term_bstride, self.stream), "ks_gemm")
 
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):

@@ -44,7 +44,8 @@ cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cud
 cudaError_t launch_mac_pipe(const void*, const void*, const void*, int, int, const HbRing&, int,
                             int, cudaStream_t);
 cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, int, int,
-                           const HbRing&, int, int, long long, long long, int, int, cudaStream_t);
+                           const HbRing&, int, int, long long, long long, int, int, long long,
+                           cudaStream_t);
 cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, const HbRing&, int,
                                int, cudaStream_t);
 cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
@@ -376,10 +377,11 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
 
 int hb_ks_gemm(hb_ring* r, const void* de, const void* keys, const void* keys_last,
                const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
-               long long dst_bstride, int prime_last, int de_per_job, void* stream) {
+               long long dst_bstride, int prime_last, int de_per_job,
+               long long last_term_bstride, void* stream) {
   cudaError_t e = launch_ks_gemm(de, keys, keys_last, dsts, ndig, nout, r->dev, rows, bc,
                                  de_bstride, dst_bstride, prime_last, de_per_job,
-                                 (cudaStream_t)stream);
+                                 last_term_bstride, (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_gemm") : 0;
 }
 

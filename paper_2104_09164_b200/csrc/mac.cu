@@ -35,6 +35,8 @@ struct HbMacGroupP {
   const u64* const* pts_last;   // ... except the last row when set: its pt rows
   int prime_last;               //     (pointers to the row itself) and prime
   int cts_per_tile;       // cts is [output tile][T] (each tile has its own terms)
+  long long ct_last_bstride;  // != 0: the last term's clip stride (a folded-in
+                              // c0 term of the key switch, see launch_ks_gemm)
 };
 
 namespace {
@@ -98,7 +100,9 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
         const u64* src;
         if (row < CB) {
           const int b = bc + row < BC ? bc + row : BC - 1;
-          src = ptab[t] + (size_t)b * g.ct_bstride + rj0 + part * 2;
+          const long long bs = (g.ct_last_bstride && t == T - 1) ? g.ct_last_bstride
+                                                                 : g.ct_bstride;
+          src = ptab[t] + (size_t)b * bs + rj0 + part * 2;
         } else {
           src = ptab[T + (row - CB) * T + t] + prow + part * 2;
         }
@@ -271,6 +275,7 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
   g.pts_last = nullptr;
   g.prime_last = 0;
   g.cts_per_tile = 0;
+  g.ct_last_bstride = 0;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
@@ -281,10 +286,14 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
 // primes 0..rows-2 and the last row in prime_last with its own key rows
 // (keys_last).  de_per_job: de is [job][ndig] (each job its own digits,
 // one output pair per tile) instead of [ndig] shared by every job.
+// last_term_bstride != 0: the last of the ndig terms is not a digit but the
+// rotation's c0 (its own clip stride) against P mod q_r (b outputs) or zero
+// rows (a outputs): ModDown(x + P c0) = ModDown(x) + c0 exactly, so the
+// ModDown epilogue needs no addend load.
 cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_last,
                            const void* dsts, int ndig, int nout, const HbRing& RG, int rows,
                            int BC, long long de_bstride, long long dst_bstride, int prime_last,
-                           int de_per_job, cudaStream_t st) {
+                           int de_per_job, long long last_term_bstride, cudaStream_t st) {
   if (nout <= 0 || ndig <= 0) return cudaSuccess;
   if (!RG.use_f64) return cudaErrorNotSupported;
   HbMacGroupP g;
@@ -299,6 +308,7 @@ cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_la
   g.pts_last = reinterpret_cast<const u64* const*>(keys_last);
   g.prime_last = prime_last;
   g.cts_per_tile = de_per_job;
+  g.ct_last_bstride = last_term_bstride;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 

@@ -205,6 +205,7 @@ _ORACLE = {}
 
 
 @pytest.mark.parametrize("env", [{"HEAR_B200_KS_GEMM_MIN": "1"}, {"HEAR_B200_KS_GEMM_MIN": "1000"},
+                                 {"HEAR_B200_KS_GEMM_MIN": "1", "HEAR_B200_FOLD_C0": "1"},
                                  {"HEAR_B200_PREPERM": "0"},
                                  {"HEAR_B200_NTT3": "0", "HEAR_B200_KS_GEMM_MIN": "1"}])
 def test_hoisted_rotations_fast_hear_vs_oracle(env):
