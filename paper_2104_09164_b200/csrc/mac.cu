@@ -21,6 +21,10 @@
 #include <cstdlib>
 #include "ring.cuh"
 
+#ifndef HB_MAC_STAGES
+#define HB_MAC_STAGES 3   // cp.async pipeline depth of the GEMM (3 measured best: 2 % over 4)
+#endif
+
 namespace hb {
 
 struct HbMacGroupP {
@@ -236,27 +240,27 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
     if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
     return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
   }
-  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, false, 4>(g, RG, rows, BC, st);
+  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   // one (b, a) output pair per tile when every job brings its own digits
-  if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
+  if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   // output tile sized to the layer so no warp idles on absent outputs
-  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
-  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
+  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   static int tile = -1;   // HEAR_B200_GEMM_TILE: experiment knob for the wide tiles
   if (tile < 0) {
     const char* v = getenv("HEAR_B200_GEMM_TILE");
     tile = v ? atoi(v) : 0;
   }
   if (g.nout <= 8) {
-    if (tile == 44) return mac_pipe_t<4, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
-    return mac_pipe_t<8, 4, 1, 8, false, 4>(g, RG, rows, BC, st);
+    if (tile == 44) return mac_pipe_t<4, 4, 2, 4, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+    return mac_pipe_t<8, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   }
-  if (tile == 48) return mac_pipe_t<4, 8, 4, 2, false, 4>(g, RG, rows, BC, st);
-  if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, 4>(g, RG, rows, BC, st);
+  if (tile == 48) return mac_pipe_t<4, 8, 4, 2, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
   // operand feeds twice the products of the 4x4 tile; measured +1.6 % on
   // the bench step (hoisted key-switch GEMM and conv MAC)
-  return mac_pipe_t<8, 4, 2, 4, false, 4>(g, RG, rows, BC, st);
+  return mac_pipe_t<8, 4, 2, 4, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
 }
 
 // fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
