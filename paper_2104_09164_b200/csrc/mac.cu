@@ -24,6 +24,9 @@
 #ifndef HB_MAC_STAGES
 #define HB_MAC_STAGES 3   // cp.async pipeline depth of the GEMM (3 measured best: 2 % over 4)
 #endif
+#ifndef HB_MAC_STAGES_LONG
+#define HB_MAC_STAGES_LONG 3   // ... for term lists longer than 32 (conv layer MACs)
+#endif
 
 namespace hb {
 
@@ -259,7 +262,9 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
   // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
   // operand feeds twice the products of the 4x4 tile; measured +1.6 % on
-  // the bench step (hoisted key-switch GEMM and conv MAC)
+  // the bench step (hoisted key-switch GEMM and conv MAC).  Long term lists
+  // (conv layers) keep a deeper pipeline (HB_MAC_STAGES_LONG)
+  if (g.nterms > 32) return mac_pipe_t<8, 4, 2, 4, false, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
   return mac_pipe_t<8, 4, 2, 4, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
 }
 
