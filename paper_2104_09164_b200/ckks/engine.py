@@ -148,6 +148,10 @@ class CkksBackend(BackendBase):
         # into the inner product (P c0 as one more term) instead of the ModDown
         # epilogue's addend load; bit-exact, measured 0.4 % slower
         self.fold_c0 = os.environ.get("HEAR_B200_FOLD_C0", "0") == "1"
+        # opt-in (HEAR_B200_BATCH_HOIST=1): hoisted rotations of several handles
+        # share one ModUp / ModDown launch; fewer launches (eager global layer
+        # -17 %) but measured 0.5 % slower inside the CUDA graph
+        self.batch_hoist = os.environ.get("HEAR_B200_BATCH_HOIST", "0") == "1"
         # opt-in (HEAR_B200_KS_FUSED=1): single-job key switches (relinearisation,
         # rot_each) with the ModUp fused into the inner product in the cluster
         # NTT (64-bit atomic accumulation, no digit expansion through HBM);
@@ -690,7 +694,14 @@ class CkksBackend(BackendBase):
             same_key = all(k[0].data_ptr() == keys[0][0].data_ptr() for k in keys)
             stacked = (js == list(range(js[0], js[0] + len(js)))
                        and offs == [offs[0] + q * bsz for q in range(len(js))])
-            if len(js) > 1 and same_key and stacked:
+            groups: dict = {}
+            for j, o in zip(js, offs):
+                groups.setdefault(o, []).append(j)
+            if len(groups) > 1 and all(len(g) >= 2 for g in groups.values()):
+                # hoisted groups of several handles: one shared-digit GEMM each
+                for o, g in groups.items():
+                    self._ks_gemm(der, lvl, [natural[j] for j in g], ipr[g], bsz, [o] * len(g))
+            elif len(js) > 1 and same_key and stacked:
                 # one key over consecutive handles (rotate-and-sum by one amount,
                 # relinearisation of a layer): their digits and outputs are
                 # contiguous, so it is one (b, a) GEMM over all their clips
@@ -1145,6 +1156,40 @@ class CkksBackend(BackendBase):
                 for q, i in enumerate(chunk):
                     c = cts[i]
                     out[i] = Ct(CtData(res[q]), lvl, c.scale * c.scale, self.n2)
+        return out
+
+    def _raw_rot_many_each(self, cts, ks) -> list:
+        """Hoisted rotations of several handles by the same amounts: one ModUp
+        over all their clips, one inner-product GEMM per handle (its digit
+        set shared by its rotations), one ModDown over every rotation."""
+        out = [None] * len(cts)
+        for lvl, idx in self._by_level(cts, lambda c: c.level).items():
+            bsz = cts[idx[0]].payload.batch
+            per = bsz * (lvl + 1) * (lvl + 2) * self.n * 8
+            if (len(idx) < 2 or per * len(idx) > self.ks_budget_bytes or not self.batch_hoist
+                    or any(cts[i].payload.batch != bsz for i in idx)):
+                for i in idx:
+                    out[i] = self._raw_rot_many(cts[i], ks)
+                continue
+            rp = self.ring.row_ptrs
+            c1 = np.concatenate([rp(cts[i].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
+                                 for i in idx])
+            de = self._decompose(c1, lvl)
+            jobs, keys_of = [], []
+            for h, i in enumerate(idx):
+                for k in ks:
+                    key, perm, add, g = self._rot_job(cts[i], k)
+                    jobs.append((key, perm, add, g, h * bsz))
+                    keys_of.append((i, k))
+            res = {i: {} for i in idx}
+            step = max(1, self._ks_chunk(bsz, lvl) * 4)
+            for c0 in range(0, len(jobs), step):
+                sub = self._ks_apply_many(de, lvl, jobs[c0:c0 + step], bsz)
+                for (i, k), o in zip(keys_of[c0:c0 + step], sub):
+                    res[i][k] = Ct(CtData(o), lvl, cts[i].scale, self.n2)
+            del de
+            for i in idx:
+                out[i] = res[i]
         return out
 
     def _raw_rot_many(self, a: Ct, ks) -> dict:

@@ -219,7 +219,7 @@ def hconv(cts: list, weights: ConvWeights, plan: ConvPlan, backend: BackendBase,
         raise ValueError(f"expected {plan.m} input ciphertexts, got {len(cts)}")
     n2 = backend.n2
     taps, blocks = plan.tap_amounts, plan.block_amounts
-    pre = [backend.rot_many(ct, plan.pre_amounts()) for ct in cts]
+    pre = backend.rot_many_each(cts, plan.pre_amounts())
     if j_chunk is None:
         j_chunk = plan.n_o
     outs = []

@@ -349,3 +349,38 @@ def test_sum_each_one_pass_equals_add_chain():
         a, b = be.export(f), be.export(s_)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert sum(v.get("add", 0) for v in n_fast.values()) == 4 + 1 + 0 + 5
+
+
+@pytest.mark.parametrize("gemm_min", ["1", "1000"])
+def test_rot_many_each_equals_rot_many(gemm_min):
+    """Hoisted rotations of several handles in one batch (one ModUp, one
+    GEMM per handle, one ModDown) equal per-handle rot_many, with the same
+    operation counters."""
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    ps = gen_params("fast-hear")
+    os.environ["HEAR_B200_KS_GEMM_MIN"] = gemm_min
+    os.environ["HEAR_B200_BATCH_HOIST"] = "1"
+    try:
+        be = CkksBackend(ps, seed=9)
+    finally:
+        del os.environ["HEAR_B200_KS_GEMM_MIN"]
+        del os.environ["HEAR_B200_BATCH_HOIST"]
+    assert be.batch_hoist
+    amts = [3, 17, 200]
+    be.ensure_rotation_keys({a: 12 for a in amts})
+    lvl = 5
+    hs = [be.import_ct(*[np.stack(x) for x in zip(*[rand_ct(ps, lvl, 500 + 3 * h + i)
+                                                     for i in range(2)])], lvl, ps.msg_scale)
+          for h in range(3)]
+    be.reset_counters()
+    many = be.rot_many_each(hs, amts + [0])
+    c_many = be.counters.as_dict()
+    be.reset_counters()
+    single = [be.rot_many(h, amts + [0]) for h in hs]
+    assert be.counters.as_dict() == c_many
+    for m, s_ in zip(many, single):
+        for a in amts + [0]:
+            x, y = be.export(m[a]), be.export(s_[a])
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
