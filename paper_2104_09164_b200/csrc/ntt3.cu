@@ -137,6 +137,12 @@ HB_DEV void mbar_expect(uint64_t* mbar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+HB_DEV void st_async8(uint32_t raddr, uint32_t rmbar, double a) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "l"(__double_as_longlong(a)), "r"(rmbar)
+               : "memory");
+}
 HB_DEV void mbar_wait0(uint64_t* mbar) {
   const uint32_t a = smem_addr(mbar);
   asm volatile(
@@ -308,25 +314,25 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         }
       }
       col_butterflies<Pol, S1, true>(x, rd, gq, fetch_col, pol);
+      if (rd < CP::NR - 1) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if (!CP::owns(rd, q)) break;
-        sm[csw<CW>(CP::m_of(rd, gq, q), c)] = x[q];
+        for (int q = 0; q < 16; ++q) {
+          if (!CP::owns(rd, q)) break;
+          sm[csw<CW>(CP::m_of(rd, gq, q), c)] = x[q];
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
-  }
-  // ---- push (block m, columns 2k, 2k+1) to the owner of block m's tile
-  cluster_wait();   // peers' mbarriers are initialised
-  {
+    // ---- push the last round's values straight from registers: element
+    // (m, column) to the owner of block m's tile (8-byte st.async)
+    cluster_wait();   // peers' mbarriers are initialised
     const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(mbar);
 #pragma unroll
-    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-      const int k = t + i * THREADS3;
-      const int m = k / (CW / 2), c = 2 * (k % (CW / 2));
-      const double2 v = *reinterpret_cast<const double2*>(sm + csw<CW>(m, c));
+    for (int q = 0; q < 16; ++q) {
+      if (!CP::owns(CP::NR - 1, q)) break;
+      const int m = CP::m_of(CP::NR - 1, gq, q);
       const uint32_t dst = m >> 5;
-      st_async16(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), v.x, v.y);
+      st_async8(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), x[q]);
     }
   }
   constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
