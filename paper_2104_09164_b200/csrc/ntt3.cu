@@ -581,22 +581,17 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[bsw(blk * 128 + u * 8 + cc)];
     inv_group_f<Pol, 4>(x, 3, rank * 32 + blk, fetch_blk, pol);
-#pragma unroll
-    for (int u = 0; u < 16; ++u) sm[bsw(blk * 128 + u * 8 + cc)] = pol.inv_round_end(x[u]);
-  }
-  __syncthreads();
-  // ---- push (block m, columns 2k, 2k+1) to the owner of those columns
-  cluster_wait();
-  {
+    // ---- push straight from registers: element (block m, column u*8+cc) to
+    // the owner of that column (8-byte st.async)
+    cluster_wait();
     const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(mbar);
+    const int m = rank * 32 + blk;
 #pragma unroll
-    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-      const int k = t + i * THREADS3;
-      const int ml = k >> 6, col = 2 * (k & 63);
-      const double2 v = *reinterpret_cast<const double2*>(sm + bsw(ml * 128 + col));
+    for (int u = 0; u < 16; ++u) {
+      const int col = u * 8 + cc;
       const uint32_t dst = col / CW;
-      st_async16(mapa(rb0 + 8u * csw<CW>(rank * 32 + ml, col % CW), dst), mapa(mb0, dst), v.x,
-                 v.y);
+      st_async8(mapa(rb0 + 8u * csw<CW>(m, col % CW), dst), mapa(mb0, dst),
+                pol.inv_round_end(x[u]));
     }
   }
   mbar_wait0(mbar);
