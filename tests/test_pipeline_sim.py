@@ -86,3 +86,32 @@ def test_ladders():
     cp = compile_pipeline(net_by_name("2d-w128"), "fast", "giant", gen_params("fast-hear"))
     assert cp.ladder_levels()[0] == 12 and cp.ladder_levels()[-1] == 0
     assert cp.expected("merge2").level == 8 and cp.expected("merge3").level == 4
+
+
+def test_batched_contract_forms_on_simulator():
+    """rot_many_each / rot_add_each / sum_each are the plain op sequences:
+    same slot values and the same operation counters (slot simulator)."""
+    rng = np.random.default_rng(3)
+    be = SimBackend(gen_params("fast-hear"))
+    cts = [be.enc(rng.uniform(-1, 1, be.n2), level=6) for _ in range(3)]
+    be.reset_counters()
+    many = be.rot_many_each(cts, [1, 5, 0])
+    c_many = be.counters.as_dict()
+    be.reset_counters()
+    single = [be.rot_many(c, [1, 5, 0]) for c in cts]
+    assert be.counters.as_dict() == c_many
+    for m, s_ in zip(many, single):
+        for k in (1, 5, 0):
+            assert np.array_equal(be.dec(m[k]), be.dec(s_[k]))
+    be.reset_counters()
+    fused = be.rot_add_each([(c, 7) for c in cts])
+    c_fused = be.counters.as_dict()
+    be.reset_counters()
+    plain = be.add_each(list(zip(cts, be.rot_each([(c, 7) for c in cts]))))
+    assert be.counters.as_dict() == c_fused
+    for f, p_ in zip(fused, plain):
+        assert np.array_equal(be.dec(f), be.dec(p_))
+    be.reset_counters()
+    sums = be.sum_each([cts, cts[:2], cts[2:]])
+    assert sum(v.get("add", 0) for v in be.counters.as_dict().values()) == 3
+    assert np.allclose(be.dec(sums[0]), sum(be.dec(c) for c in cts))
