@@ -17,24 +17,25 @@
 //            owners, column pass, N^-1 fused in the store.
 //
 // The exchange is producer/consumer through mbarrier transaction counts:
-// no cluster-wide barrier with release/acquire fences in the data path (the
-// cooperative-groups cluster.sync version profiled 16 % of its stall samples
-// on MEMBAR.ALL.GPU / ERRBAR / the barrier wait, and its CCTL.IVALL dropped
-// the twiddles from L1).  The only cluster barrier makes the mbarrier
-// initialisation visible and is split around the first pass.  The lazy
-// intermediate never touches L2/HBM (the two-pass kernels write and re-read
-// it: 256 KB per row).
+// no cluster-wide barrier in the data path (the cooperative-groups
+// cluster.sync version profiled 16 % of its stall samples on MEMBAR.ALL.GPU
+// / ERRBAR / the barrier wait).  One CTA buffer serves both passes: the
+// single cluster barrier (release-arrive after the CTA's last read of its
+// first-pass buffer, wait just before the pushes) both publishes the
+// mbarrier initialisation and frees the buffer for the peers' pushes.  The
+// lazy intermediate never touches L2/HBM (the two-pass kernels write and
+// re-read it: 256 KB per row).
 //
 // Also in shared memory: the column twiddles and the stride-8 block-stage
 // twiddles of the CTA's tile (staged once, LDS at immediate offsets); the
 // last three forward / first three inverse stages read a plane-major
 // (w, w/p) table with lanes on consecutive entries.  ModDown modes: the x_r
-// tile is TMA-bulk-copied (cp.async.bulk + second mbarrier) into the
-// consumed column buffer while the block pass runs, and the epilogue
-// (x_r - y) * P^-1 (+ c0) (+ post-addend) runs on the fp64 pipe on 16-byte
-// lane-contiguous chunks.  Inverse: a second destination can receive the
-// input row verbatim (the ModUp identity digit).  Shared memory per CTA:
-// 64 KB + 9.7 KB twiddles + 16 B (3 CTAs per SM at 80 registers).
+// tile is prefetched into L2 (cp.async.bulk.prefetch) while the block pass
+// runs, and the epilogue (x_r - y) * P^-1 (+ c0) (+ post-addend) runs on the
+// fp64 pipe on 16-byte lane-contiguous chunks.  Inverse: a second
+// destination can receive the input row verbatim (the ModUp identity digit).
+// Shared memory per CTA: 32 KB + 9.7 KB twiddles + 16 B; 64 registers: four
+// CTAs (32 warps) per SM.
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -47,8 +48,21 @@ namespace {
 constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
 // local buffer, receive buffer, staged twiddles (TW3 x 16 B), 2 mbarriers
+#ifndef HB_NTT3_SB
+#define HB_NTT3_SB 1
+#endif
+// HB_NTT3_SB = 1 (default): ONE 32 KB tile buffer per CTA -- the exchange
+// lands in the buffer the first pass worked in, after a cluster barrier
+// (arrive.release once the last local read is done, wait just before the
+// pushes).  42.5 KB of shared memory and <= 64 registers: four CTAs (32
+// warps) per SM instead of three.  The ModDown x_r tile is then prefetched
+// into L2 (cp.async.bulk.prefetch) instead of into shared memory.
+constexpr int NBUF3 = HB_NTT3_SB ? 1 : 2;
+#ifndef HB_NTT3_L2PF
+#define HB_NTT3_L2PF 1
+#endif
 template <int LOGN>
-__host__ __device__ constexpr int smem3() { return 2 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
+__host__ __device__ constexpr int smem3() { return NBUF3 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
 #ifndef HB_NTT3_C0BUF
 #define HB_NTT3_C0BUF 0
 #endif
@@ -56,12 +70,13 @@ __host__ __device__ constexpr int smem3() { return 2 * TILE3 * 8 + ((1 << (LOGN 
 // the c0 addend is TMA-prefetched with x_r instead of loaded in the epilogue
 // (the epilogue's top stall); measured 12 % slower: 106 KB of smem leaves
 // two CTAs per SM instead of three
+static_assert(!(HB_NTT3_SB && HB_NTT3_C0BUF), "the c0 tile needs the two-buffer layout");
 template <int LOGN, int MODE>
 __host__ __device__ constexpr int smem3f() {
   return smem3<LOGN>() + ((HB_NTT3_C0BUF && MODE == 4) ? TILE3 * 8 + 16 : 0);
 }
 #ifndef HB_NTT3_MINB
-#define HB_NTT3_MINB 3
+#define HB_NTT3_MINB (HB_NTT3_SB ? 4 : 3)
 #endif
 
 HB_DEV int swz3_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
@@ -96,7 +111,19 @@ HB_DEV void xchg_init(uint64_t* mbar, uint32_t bytes) {
                  : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  if (!HB_NTT3_SB) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+// single-buffer exchange: every local read of the buffer is performed before
+// any peer's push into it -- a release arrive (MEMBAR.ALL.GPU per thread).
+// Measured: a CTA barrier + relaxed arrive is NOT enough (peers' pushes
+// overwrote data still being read: nondeterministic rows under load,
+// tools/ntt3_check.py NTT3_DIFF=1); a CTA-scope fence + relaxed arrive was
+// deterministic and 3 % faster on ModUp but is outside the memory model.
+HB_DEV void cluster_arrive_sb() {
+  if (HB_NTT3_SB) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+HB_DEV void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 HB_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 // 16-byte push into a peer's shared memory, counted on the peer's mbarrier
@@ -244,7 +271,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   typedef typename Pol::T V;
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
-  V* rb = sm + TILE3;                     // received block tile
+  V* rb = sm + (NBUF3 - 1) * TILE3;       // received block tile
   constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
@@ -313,6 +340,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
           x[q] = sm[csw<CW>(CP::m_of(rd, gq, q), c)];
         }
       }
+      if (rd == CP::NR - 1) cluster_arrive_sb();   // last local read done
       col_butterflies<Pol, S1, true>(x, rd, gq, fetch_col, pol);
       if (rd < CP::NR - 1) {
 #pragma unroll
@@ -337,7 +365,12 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   }
   constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
   constexpr bool KS = MODE == FWD_LIFT_KS;   // aux = key row b, add = key row a
-  if (MD || KS) {
+  if ((MD || KS) && HB_NTT3_SB) {
+    if (t == 0 && HB_NTT3_L2PF) {   // the epilogue's x_r / addend tiles into L2 meanwhile
+      l2_prefetch(tk.aux + (size_t)rank * TILE3, TILE3 * 8);
+      if (tk.add && !(MODE == FWD_MODDOWN && tk.perm)) l2_prefetch(tk.add + (size_t)rank * TILE3, TILE3 * 8);
+    }
+  } else if (MD || KS) {
     // the column slice is consumed: prefetch the epilogue's x_r tile into it
     // (TMA bulk copy) while the block pass runs
     __syncthreads();
@@ -404,7 +437,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   // chain cost ~30 integer instructions per element)
   const double pd = P.pd, pinv = P.pinv;
   const double sd = u64_to_f(tk.scal), sq = sd * pinv;
-  if (MD || KS) mbar_wait0(mbar + 1);
+  if ((MD || KS) && !HB_NTT3_SB) mbar_wait0(mbar + 1);
   if (KS) {
     // fused key-switch inner product: this digit's transformed row times the
     // two key rows, accumulated with 64-bit atomic adds of canonical products
@@ -414,7 +447,8 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       const int k = t + i * THREADS3;
       const size_t j = base + 2 * k;
       const int pc = swz3_chunk(k);
-      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
+      const ulonglong2 kb = HB_NTT3_SB ? __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j))
+                                       : *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
       const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
       const double y0 = rb[2 * pc], y1 = rb[2 * pc + 1];
       const double y0q = y0 * pinv, y1q = y1 * pinv;
@@ -433,7 +467,8 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     ulonglong2 o;
     int2 sc = make_int2(0, 0);
     if (MD) {
-      const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
+      const ulonglong2 ax = HB_NTT3_SB ? __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j))
+                                       : *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
       double r0 = fmod_mul(u64_to_f(ax.x) - rb[2 * pc], sd, sq, pd);
       double r1 = fmod_mul(u64_to_f(ax.y) - rb[2 * pc + 1], sd, sq, pd);
       if (tk.add) {
@@ -488,7 +523,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   typedef typename Pol::T V;
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
-  V* rb = sm + TILE3;                     // received column slice
+  V* rb = sm + (NBUF3 - 1) * TILE3;       // received column slice
   constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
@@ -580,6 +615,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
     V x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[bsw(blk * 128 + u * 8 + cc)];
+    cluster_arrive_sb();   // last local read done
     inv_group_f<Pol, 4>(x, 3, rank * 32 + blk, fetch_blk, pol);
     // ---- push straight from registers: element (block m, column u*8+cc) to
     // the owner of that column (8-byte st.async)
