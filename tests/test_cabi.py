@@ -32,3 +32,31 @@ def test_layouts_and_version():
 def test_oracle_builds_and_loads():
     from oracle.cpu_engine import lib
     assert lib().or_num_threads() >= 1
+
+
+def test_no_cpu_fallback():
+    """The product path fails loudly: a missing kernel library raises on load,
+    and the engine refuses to build a ring without a CUDA device."""
+    import subprocess
+    import sys
+    code = ("import os, sys\n"
+            "sys.path.insert(0, %r)\n"
+            "from paper_2104_09164_b200 import _native as nat\n"
+            "try:\n"
+            "    nat.lib()\n"
+            "except nat.NativeError as e:\n"
+            "    assert 'no CPU fallback' in str(e), e\n"
+            "    print('missing-lib raised')\n") % ROOT
+    env = dict(os.environ, HEAR_B200_LIB="/nonexistent/libhear_b200.so")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "missing-lib raised" in out.stdout, out.stderr
+
+    import pytest
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present: the no-device branch is not reachable")
+    from paper_2104_09164_b200 import _native as nat
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    with pytest.raises(nat.NativeError, match="CUDA device"):
+        CkksBackend(gen_params("toy-fast"), seed=1)
