@@ -148,10 +148,13 @@ class CkksBackend(BackendBase):
         # into the inner product (P c0 as one more term) instead of the ModDown
         # epilogue's addend load; bit-exact, measured 0.4 % slower
         self.fold_c0 = os.environ.get("HEAR_B200_FOLD_C0", "0") == "1"
-        # opt-in (HEAR_B200_BATCH_HOIST=1): hoisted rotations of several handles
-        # share one ModUp / ModDown launch; fewer launches (eager global layer
-        # -17 %) but measured 0.5 % slower inside the CUDA graph
-        self.batch_hoist = os.environ.get("HEAR_B200_BATCH_HOIST", "0") == "1"
+        # hoisted rotations of several handles share one ModUp / ModDown launch
+        # when each handle carries at most `batch_hoist_max` clips: at one clip
+        # per handle the merged launches fill the GPU (B=1 latency 4.77 -> 4.15
+        # ms); at 128 clips they are throughput-neutral inside the CUDA graph.
+        # HEAR_B200_BATCH_HOIST=1 / 0 forces it on / off for every batch size.
+        self.batch_hoist_max = {"1": 1 << 30, "0": 0}.get(
+            os.environ.get("HEAR_B200_BATCH_HOIST", ""), 16)
         # opt-in (HEAR_B200_KS_FUSED=1): single-job key switches (relinearisation,
         # rot_each) with the ModUp fused into the inner product in the cluster
         # NTT (64-bit atomic accumulation, no digit expansion through HBM);
@@ -1166,7 +1169,7 @@ class CkksBackend(BackendBase):
         for lvl, idx in self._by_level(cts, lambda c: c.level).items():
             bsz = cts[idx[0]].payload.batch
             per = bsz * (lvl + 1) * (lvl + 2) * self.n * 8
-            if (len(idx) < 2 or per * len(idx) > self.ks_budget_bytes or not self.batch_hoist
+            if (len(idx) < 2 or per * len(idx) > self.ks_budget_bytes or bsz > self.batch_hoist_max
                     or any(cts[i].payload.batch != bsz for i in idx)):
                 for i in idx:
                     out[i] = self._raw_rot_many(cts[i], ks)

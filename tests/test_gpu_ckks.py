@@ -351,8 +351,8 @@ def test_sum_each_one_pass_equals_add_chain():
     assert sum(v.get("add", 0) for v in n_fast.values()) == 4 + 1 + 0 + 5
 
 
-@pytest.mark.parametrize("gemm_min", ["1", "1000"])
-def test_rot_many_each_equals_rot_many(gemm_min):
+@pytest.mark.parametrize("gemm_min,hoist", [("1", "1"), ("1000", "1"), ("1", "")])
+def test_rot_many_each_equals_rot_many(gemm_min, hoist):
     """Hoisted rotations of several handles in one batch (one ModUp, one
     GEMM per handle, one ModDown) equal per-handle rot_many, with the same
     operation counters."""
@@ -361,13 +361,13 @@ def test_rot_many_each_equals_rot_many(gemm_min):
     from paper_2104_09164_b200.ckks.params import gen_params
     ps = gen_params("fast-hear")
     os.environ["HEAR_B200_KS_GEMM_MIN"] = gemm_min
-    os.environ["HEAR_B200_BATCH_HOIST"] = "1"
+    os.environ["HEAR_B200_BATCH_HOIST"] = hoist   # "1": forced; "": default (small batches)
     try:
         be = CkksBackend(ps, seed=9)
     finally:
         del os.environ["HEAR_B200_KS_GEMM_MIN"]
         del os.environ["HEAR_B200_BATCH_HOIST"]
-    assert be.batch_hoist
+    assert be.batch_hoist_max >= 2
     amts = [3, 17, 200]
     be.ensure_rotation_keys({a: 12 for a in amts})
     lvl = 5
