@@ -65,6 +65,18 @@ HB_DEV u64 recombine3(double s0, double s1, double s2, const double* cc, double 
   return fmod_canon(r0 + r1 + r2, p, pinv);
 }
 
+// Operand conversion of the GEMM: the magic-number path (LOP + DADD on the
+// fp64 pipe) by default; -DHB_MAC_I2F moves it to the conversion pipe
+// (I2F.F64.U64), which is otherwise idle here: bit-identical, measured 0.4 %
+// slower on the bench step (profiles/r01_knob_ab.txt), so off.
+HB_DEV double mac_to_f(u64 x) {
+#ifdef HB_MAC_I2F
+  return __ull2double_rn(x);
+#else
+  return u64_to_f(x);
+#endif
+}
+
 template <int TO, int TB, int WO, int WB, bool C3, int S>
 __global__ void __launch_bounds__(256)
 k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
@@ -146,7 +158,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     const u64* st = stages + (t % S) * STAGE;
     double a[TO];
 #pragma unroll
-    for (int o = 0; o < TO; ++o) a[o] = u64_to_f(st[(CB + os + o) * 32 + lane]);
+    for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
     if constexpr (C3) {
 #pragma unroll
       for (int b = 0; b < TB; ++b) {
@@ -172,7 +184,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     } else {
       double c[TB];
 #pragma unroll
-      for (int b = 0; b < TB; ++b) c[b] = u64_to_f(st[(bs + b) * 32 + lane]);
+      for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
 #pragma unroll
       for (int o = 0; o < TO; ++o) {
         const double aq = a[o] * pinv;
