@@ -1,0 +1,7 @@
+#!/bin/bash
+# End-of-session check on the GPU box: GPU suite, smoke, bench line, reference arm.
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/res_default.json 2> gpurun_out/res_default.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/res_ref.json 2> gpurun_out/res_ref.err
+true
