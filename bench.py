@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--strategy", default="full", choices=["full", "giant", "baby"])
     ap.add_argument("--batch", type=int, default=128, help="clips per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--roofline-only", action="store_true")
+    ap.add_argument("--check-launch", action="store_true",
+                    help="multi-rank plumbing only: spawn, key replication, max-over-ranks")
     return ap.parse_args()
 
 
@@ -219,10 +220,14 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     e1.record(st)
     torch.cuda.synchronize()
     sec = e0.elapsed_time(e1) / 1e3 / reps
-    algo = (m * r * 20 + bsz * r * 8 + m * 8) * n
+    # x_r read + output written per row, c0 read per component-0 row, one
+    # special-prime source row per (clip, component); the inverse-Galois
+    # table is one shared 4N-byte array (L2-resident), counted once
+    algo = (m * r * 16 + bsz * r * 8 + m * 8) * n + 4 * n
     gbs = algo / sec / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     bfly = m * r * (n // 2) * (n.bit_length() - 1)
+    fp64_frac = bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12)
     kname = "k_ntt3_fwd<FWD_MODDOWN_SCATTER>"
     traffic = None
     try:
@@ -232,13 +237,58 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
             traffic = tr["dram_bytes"]
     except (OSError, ValueError, KeyError):
         pass
+    # the roof this kernel is nearer to: HBM bytes or the fp64 pipe (its
+    # modular butterflies run as fp64 instructions; no tensor-core work)
+    hbm_frac = gbs / peak
+    bound = "hbm" if hbm_frac >= fp64_frac else "fp64"
     return {"kernel": kname + " (rotation ModDown: cluster NTT + fused epilogue)",
-            "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(gbs / peak, 4), "traffic": traffic, "launch_us": round(sec * 1e6, 2),
+            "bound": bound, "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(hbm_frac, 4), "traffic": traffic, "launch_us": round(sec * 1e6, 2),
             "rows_per_launch": m * r, "algorithmic_bytes_per_launch": algo,
             "butterflies_per_s": round(bfly / sec / 1e12, 3),
-            "fp64_frac_of_measured": round(bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12), 3),
+            "fp64_frac_of_measured": round(fp64_frac, 3),
+            "fp64_peak_ops_per_s": FP64_MEASURED_TFLOPS * 1e12,
             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
+
+
+def step_roofline(enc, ct, be, run_pipeline, ms_graph: float, peaks: dict) -> dict:
+    """Step-level roofline: one eager pass of the step with every launch
+    accounted (ring.StepStats: algorithmic bytes = distinct source rows once
+    + every output row, nominal fp64 instructions of the modular arithmetic)
+    and timed with CUDA events around each launch on the launching stream.
+    Whole step: the summed algorithmic bytes / fp64 ops over the graph's
+    ms_per_step.  Per kernel family: its share of the eager step's device
+    time, achieved GB/s and fp64 fraction over its own launches."""
+    import torch
+    from paper_2104_09164_b200.ckks import ring as R
+    peak = peaks.get("hbm_gbs", 6650.0)
+    fp64_peak = FP64_MEASURED_TFLOPS * 1e12
+    st = R.StepStats(timed=True)
+    R.set_step_stats(st)
+    try:
+        torch.cuda.synchronize()
+        run_pipeline(enc, ct, be)
+        fam = st.finish()
+    finally:
+        R.set_step_stats(None)
+    tot_b = sum(f["bytes"] for f in fam.values())
+    tot_f = sum(f["fp64_ops"] for f in fam.values())
+    tot_ms = sum(f["ms"] for f in fam.values())
+    fams = {}
+    for name, f in sorted(fam.items(), key=lambda kv: -kv[1]["ms"]):
+        sec = max(f["ms"], 1e-9) / 1e3
+        fams[name] = {"launches": f["launches"], "share": round(f["ms"] / tot_ms, 4),
+                      "ms": round(f["ms"], 3), "algorithmic_bytes": f["bytes"],
+                      "achieved_gbs": round(f["bytes"] / sec / 1e9, 1),
+                      "hbm_frac": round(f["bytes"] / sec / 1e9 / peak, 4),
+                      "fp64_frac": round(f["fp64_ops"] / sec / fp64_peak, 4)}
+    sec = ms_graph / 1e3
+    return {"algorithmic_bytes_per_step": tot_b, "fp64_ops_per_step": tot_f,
+            "hbm_frac": round(tot_b / sec / 1e9 / peak, 4),
+            "fp64_frac": round(tot_f / sec / fp64_peak, 4),
+            "eager_step_device_ms": round(tot_ms, 3), "graph_ms_per_step": round(ms_graph, 3),
+            "fp64_ops_note": "8 per NTT butterfly, 6 per modular product (fmod_mul + accumulate)",
+            "families": fams}
 
 
 def keyswitch_rate(be, lvl: int, bsz: int) -> dict:
@@ -290,6 +340,9 @@ def gpu_arm(args):
     from paper_2104_09164_b200.fastpath import GraphedPipeline
 
     rank, ws, local = par.world()
+    if ws != args.gpus:
+        raise SystemExit(f"world size {ws} != --gpus {args.gpus}: launch with torchrun "
+                         "or let bench.py spawn the ranks")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     par.init("nccl")
@@ -304,7 +357,9 @@ def gpu_arm(args):
     shape = net_by_name(args.net)
     cpar = collapse_layers(make_random_model(shape, 1), shape)
     cp = compile_pipeline(shape, args.mode, args.strategy, params)
-    be = CkksBackend(params, seed=0, device=dev, keygen=(rank == 0))
+    # receivers encrypt from their own stream (never the sender's keygen stream)
+    be = CkksBackend(params, seed=0, device=dev, keygen=(rank == 0),
+                     enc_seed=np.random.SeedSequence(0, spawn_key=(rank,)))
     if rank == 0:
         be.ensure_rotation_keys(cp.rotations)
     par.replicate_keys(be, src=0)
@@ -417,7 +472,9 @@ def gpu_arm(args):
                "samples": len(lat), "batch": 1}
     del g1, graph
 
-    roof = ks = None
+    roof = ks = steproof = None
+    if rank == 0:
+        steproof = step_roofline(enc, ct, be, run_pipeline, ms, peaks)
     if rank == 0:   # per-GPU kernel figures; the other ranks hold no secret key
         # one rotation ModDown over 64 clips (the shape of the committed ncu capture)
         roof = dominant_kernel_roofline(be, lvl=params.max_level, bsz=64, peaks=peaks)
@@ -459,6 +516,7 @@ def gpu_arm(args):
             "per_clip_latency": latency,
             "keyswitch": ks,
             "roofline": roof,
+            "step_roofline": steproof,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -466,9 +524,58 @@ def gpu_arm(args):
     par.barrier()
 
 
+def launch_check(args):
+    """The multi-rank path without the encrypted network: world size, the
+    setup-time key broadcast over tensors of the real key layout (toy-fast
+    parameters, the toy network's rotation manifest), max over ranks.  Runs
+    on CPU (gloo) as well as on GPUs (NCCL)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_09164_b200 import parallel as par
+    from paper_2104_09164_b200.ckks.engine import key_layout
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline
+    from paper_2104_09164_b200.model import NetworkShape
+    rank, ws, local = par.world()
+    cuda = torch.cuda.is_available()
+    dev = torch.device("cuda", local) if cuda else torch.device("cpu")
+    if cuda:
+        torch.cuda.set_device(local)
+    par.init("nccl" if cuda else "gloo")
+    if ws != args.gpus:
+        raise SystemExit(f"world size {ws} != --gpus {args.gpus}")
+    ps = gen_params("toy-fast")
+    cp = compile_pipeline(NetworkShape(1, 32, 15, (4, 8, 16), 4), "fast", "giant", ps)
+    manifest = par.broadcast_object(sorted(cp.rotations.items()) if rank == 0 else None)
+    layout = key_layout(ps, manifest)
+    g = torch.Generator().manual_seed(7)
+    keys = [torch.randint(0, 1 << 40, shape, generator=g).to(dev) if rank == 0 else
+            torch.empty(shape, dtype=torch.int64, device=dev) for _, shape in layout]
+    par.broadcast_tensors(keys)
+    sums = torch.tensor([float(sum(int(k.sum()) for k in keys) % (1 << 50))], dtype=torch.float64,
+                        device=dev)
+    allsum = [torch.zeros_like(sums) for _ in range(ws)] if ws > 1 else [sums]
+    if ws > 1:
+        dist.all_gather(allsum, sums)
+    mx = par.max_over_ranks(float(rank + 1), dev)
+    if rank == 0:
+        print(json.dumps({"check": "launch", "n_ranks": ws, "backend": "nccl" if cuda else "gloo",
+                          "key_tensors": len(keys),
+                          "key_bytes": int(sum(k.numel() * 8 for k in keys)),
+                          "keys_identical": len({float(t.item()) for t in allsum}) == 1,
+                          "max_over_ranks": mx}), flush=True)
+    par.barrier()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` started as one process: become N ranks
+        from paper_2104_09164_b200.parallel import relaunch
+        sys.exit(relaunch(args.gpus, os.path.abspath(__file__), sys.argv[1:]))
+    if args.check_launch:
+        launch_check(args)
+    elif args.impl == "reference":
         reference_arm(args)
     else:
         gpu_arm(args)

@@ -101,6 +101,20 @@ class KeyMaterial:
         self.rot: dict = {}
 
 
+def key_layout(params: ParameterSet, manifest) -> list:
+    """[(name, shape)] of the public evaluation material in key_tensors order
+    (the reference's KeyMaterial, engine.py:27-36): public key rows, the
+    relinearisation key and one key per rotation amount of the manifest
+    [(amount, lmax)], digit-major [ndig, rows, N] with the special row last.
+    Pure function of the parameters: receivers allocate from it."""
+    n, L = params.n, params.max_level
+    out = [("pk_b", (L + 2, n)), ("pk_a", (L + 2, n)),
+           ("relin_b", (L + 1, L + 2, n)), ("relin_a", (L + 1, L + 2, n))]
+    for amt, lmax in sorted(manifest):
+        out += [(f"rot{amt}_b", (lmax + 1, lmax + 2, n)), (f"rot{amt}_a", (lmax + 1, lmax + 2, n))]
+    return out
+
+
 def _tasks(dtype, n, **fields) -> np.ndarray:
     t = np.zeros(n, dtype=dtype)
     for k, v in fields.items():
@@ -113,12 +127,22 @@ class CkksBackend(BackendBase):
 
     exact = False
 
-    def __init__(self, params: ParameterSet, seed: int = 0, device=None, keygen: bool = True):
+    def __init__(self, params: ParameterSet, seed: int = 0, device=None, keygen: bool = True,
+                 enc_seed=None):
         super().__init__(params)
         self.ring = RingContext(params, device)
         self.dev = self.ring.device
         self.emb = Embedding(params.n, self.dev)
-        self.rng = np.random.default_rng(seed)
+        # keygen=True: one generator for keys then encryptions, in the
+        # reference's draw order (bit-exact keys and ciphertexts).  A receiver
+        # (keygen=False, keys replicated from another rank) must NOT replay
+        # that stream -- its first ternary draw would be the sender's secret
+        # key -- so it encrypts from its own stream: `enc_seed` (e.g. a
+        # SeedSequence spawned per rank) or fresh OS entropy.
+        if keygen:
+            self.rng = np.random.default_rng(seed)
+        else:
+            self.rng = np.random.default_rng(enc_seed)
         self.n = params.n
         self.L = params.max_level
         self.S = self.ring.special_idx
@@ -186,14 +210,15 @@ class CkksBackend(BackendBase):
         return [(a, self.keys.rot[a].lmax) for a in sorted(self.keys.rot)]
 
     def alloc_keys(self, manifest):
-        """Allocate empty evaluation keys of the given layout (receiver side)."""
+        """Allocate empty evaluation keys of the given layout (receiver side),
+        in the order and shapes of key_layout / key_tensors."""
         k = self.keys
-        full = self.L + 2
-        k.pk_b, k.pk_a = self.ring.empty(full), self.ring.empty(full)
-        k.relin = _Ksk(self.ring.empty(self.L + 1, full), self.ring.empty(self.L + 1, full), self.L)
+        t = {name: torch.empty(shape, dtype=torch.int64, device=self.dev)
+             for name, shape in key_layout(self.params, manifest)}
+        k.pk_b, k.pk_a = t["pk_b"], t["pk_a"]
+        k.relin = _Ksk(t["relin_b"], t["relin_a"], self.L)
         for amt, lmax in manifest:
-            k.rot[amt] = _Ksk(self.ring.empty(lmax + 1, lmax + 2),
-                              self.ring.empty(lmax + 1, lmax + 2), lmax)
+            k.rot[amt] = _Ksk(t[f"rot{amt}_b"], t[f"rot{amt}_a"], lmax)
 
     # ------------------------------------------------------------------ sampling
 

@@ -92,6 +92,64 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+class StepStats:
+    """Algorithmic accounting of every launch helper below, for the step-level
+    roofline in bench.py: per kernel family, the launches, the ALGORITHMIC
+    HBM bytes (each distinct source row counted once per launch, every
+    destination row once; shared tables such as Galois permutations and
+    twiddles once per launch) and the modular products; with `timed`, also
+    the device time of each launch (CUDA events around it on the launching
+    stream, resolved by `finish`).  Enabled with `set_step_stats`; the
+    launch helpers do no accounting otherwise."""
+
+    FP64_PER_BUTTERFLY = 8   # fmod_mul (5) + add + sub + conditional correction
+    FP64_PER_MODMUL = 6      # fmod_mul (5) + accumulate
+
+    def __init__(self, timed: bool = False):
+        self.timed = timed
+        self.fam: dict = {}
+        self._ev: list = []
+
+    def add(self, fam: str, nbytes: int, fp64: int, kernels: int = 1):
+        r = self.fam.setdefault(fam, {"launches": 0, "bytes": 0, "fp64_ops": 0, "ms": 0.0})
+        r["launches"] += kernels
+        r["bytes"] += int(nbytes)
+        r["fp64_ops"] += int(fp64)
+
+    def begin(self):
+        if not self.timed:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def end(self, fam: str, e0):
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self._ev.append((fam, e0, e1))
+
+    def finish(self):
+        torch.cuda.synchronize()
+        for fam, e0, e1 in self._ev:
+            self.fam[fam]["ms"] += e0.elapsed_time(e1)
+        self._ev = []
+        return self.fam
+
+
+_STATS: StepStats | None = None
+
+
+def set_step_stats(stats: StepStats | None):
+    global _STATS
+    _STATS = stats
+
+
+def _uniq(col) -> int:
+    col = np.asarray(col, dtype=np.uint64).ravel()
+    return int(np.count_nonzero(np.unique(col)))
+
+
 class RingContext:
     """Per-parameter-set tables (host) and the kernel library handle (device).
 
@@ -202,22 +260,68 @@ class RingContext:
         """Kernels one NTT call enqueues (csrc/ntt.cu ntt_kernels)."""
         return int(self._lib.hb_ntt_kernels(self.handle, count))
 
+    _FWD_NAMES = {nat.FWD_PLAIN: "ntt_fwd", nat.FWD_LIFT: "ntt_fwd_modup_lift",
+                  nat.FWD_MODDOWN: "ntt_fwd_moddown", nat.FWD_I64: "ntt_fwd_i64",
+                  nat.FWD_MODDOWN_SCATTER: "ntt_fwd_moddown_scatter",
+                  nat.FWD_LIFT_KS: "ntt_fwd_lift_ks"}
+
+    def _ntt_account(self, fam: str, tasks: np.ndarray, kernels: int):
+        row = 8 * self.n
+        m = len(tasks)
+        nbytes = (_uniq(tasks["src"]) + m) * row             # sources once, every output
+        nbytes += (_uniq(tasks["aux"]) + _uniq(tasks["add"]) + _uniq(tasks["add2"])) * row
+        nbytes += _uniq(tasks["perm"]) * 4 * self.n + m * 16 * self.n // 8   # perms; twiddles
+        fp64 = m * (self.n // 2) * self.logn * StepStats.FP64_PER_BUTTERFLY
+        if fam.startswith("ntt_fwd_moddown"):
+            fp64 += m * self.n * StepStats.FP64_PER_MODMUL
+        _STATS.add(fam, nbytes, fp64, kernels)
+
     def ntt_fwd(self, tasks: np.ndarray, mode: int = nat.FWD_PLAIN):
         if len(tasks):
             d = _upload(tasks, self.device)
+            k = self._ntt_kernels(len(tasks))
+            fam = self._FWD_NAMES.get(mode, "ntt_fwd")
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_ntt_fwd(self.handle, _ptr(d), len(tasks), mode, self.stream),
-                      "ntt_fwd", self._ntt_kernels(len(tasks)))
+                      "ntt_fwd", k)
+            if _STATS:
+                _STATS.end(fam, e0)
+                self._ntt_account(fam, tasks, k)
 
     def ntt_inv(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)
+            k = self._ntt_kernels(len(tasks))
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_ntt_inv(self.handle, _ptr(d), len(tasks), self.stream),
-                      "ntt_inv", self._ntt_kernels(len(tasks)))
+                      "ntt_inv", k)
+            if _STATS:
+                _STATS.end("ntt_inv", e0)
+                self._ntt_account("ntt_inv", tasks, k)
+
+    _EW_READS = {nat.EW_ADD: ("a", "b"), nat.EW_SUB: ("a", "b"), nat.EW_MUL: ("a", "b"),
+                 nat.EW_MUL_SCALAR: ("a",), nat.EW_MULADD: ("a", "b", "c"),
+                 nat.EW_ADD_SCALED: ("a", "b"), nat.EW_COPY: ("a",), nat.EW_PERM: ("a",),
+                 nat.EW_SUB_SCALED: ("a", "b"), nat.EW_PERM_ADD: ("a", "b")}
+    _EW_MULS = {nat.EW_MUL: 1, nat.EW_MUL_SCALAR: 1, nat.EW_MULADD: 1, nat.EW_ADD_SCALED: 1,
+                nat.EW_SUB_SCALED: 1}
 
     def ew(self, op: int, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_ew(self.handle, op, _ptr(d), len(tasks), self.stream), "ew")
+            if _STATS:
+                _STATS.end("elementwise", e0)
+                rd = self._EW_READS.get(op, ())
+                rows = (_uniq(np.concatenate([tasks[f] for f in rd])) if rd else 0) + len(tasks)
+                nbytes = rows * 8 * self.n
+                if op == nat.EW_PERM:
+                    nbytes += _uniq(tasks["b"]) * 4 * self.n
+                if op == nat.EW_PERM_ADD:
+                    nbytes += _uniq(tasks["c"]) * 4 * self.n
+                _STATS.add("elementwise", nbytes,
+                           len(tasks) * self.n * self._EW_MULS.get(op, 0) * StepStats.FP64_PER_MODMUL)
 
     def mac(self, tasks: np.ndarray, terms: np.ndarray):
         if len(tasks):
@@ -228,8 +332,16 @@ class RingContext:
     def mac_strided(self, outs: np.ndarray, terms: np.ndarray, rows: int, bc: int):
         if len(outs):
             d, t = _upload(outs, self.device), _upload(terms, self.device)
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_mac_strided(self.handle, _ptr(d), len(outs), _ptr(t), rows, bc,
                                                self.stream), "mac_strided")
+            if _STATS:
+                _STATS.end("mac_strided", e0)
+                row = 8 * self.n
+                nbytes = (_uniq(terms["pt"]) * rows + _uniq(terms["ct"]) * rows * bc
+                          + len(outs) * rows * bc) * row
+                _STATS.add("mac_strided", nbytes,
+                           len(terms) * rows * bc * self.n * StepStats.FP64_PER_MODMUL)
 
     def sum_rows(self, dst: np.ndarray, srcs: np.ndarray, primes: np.ndarray):
         """dst[r] = sum_k srcs[r, k] (mod p_r) for every output row r."""
@@ -240,13 +352,23 @@ class RingContext:
             tasks["nterms"], tasks["term_off"] = k, np.arange(rows) * k
             d = _upload(tasks, self.device)
             s = _upload(np.ascontiguousarray(srcs, dtype=np.uint64).ravel(), self.device)
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_sum(self.handle, _ptr(d), rows, _ptr(s), self.stream), "sum")
+            if _STATS:
+                _STATS.end("sum_rows", e0)
+                _STATS.add("sum_rows", (_uniq(srcs) + rows) * 8 * self.n, 0)
 
     def tensor(self, tasks: np.ndarray):
         if len(tasks):
             d = _upload(tasks, self.device)
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_tensor(self.handle, _ptr(d), len(tasks), self.stream),
                       "tensor")
+            if _STATS:
+                _STATS.end("tensor", e0)
+                rd = _uniq(np.concatenate([tasks[f] for f in ("a0", "a1", "b0", "b1")]))
+                _STATS.add("tensor", (rd + 3 * len(tasks)) * 8 * self.n,
+                           4 * len(tasks) * self.n * StepStats.FP64_PER_MODMUL)
 
     def mac_shared(self, cts: np.ndarray, pts: np.ndarray, dsts: np.ndarray, rows: int, bc: int):
         """Shared-term MAC: dsts[o] = sum_t pts[o, t] * cts[t] over [bc, rows, N] blocks."""
@@ -255,9 +377,15 @@ class RingContext:
             buf = _upload(np.concatenate([cts.ravel(), pts.ravel(), dsts.ravel()])
                           .astype(np.uint64), self.device)
             base = _ptr(buf)
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_mac_shared(self.handle, base, base + 8 * nterms,
                                               base + 8 * (nterms + nout * nterms), nterms, nout,
                                               rows, bc, self.stream), "mac_shared")
+            if _STATS:   # ct terms [bc, rows, N] once, pt rows once, outputs
+                _STATS.end("layer_mac_gemm", e0)
+                nbytes = (_uniq(cts) * bc + _uniq(pts) + nout * bc) * rows * 8 * self.n
+                _STATS.add("layer_mac_gemm", nbytes, nout * nterms * bc * rows * self.n
+                           * StepStats.FP64_PER_MODMUL)
 
     @property
     def use_f64(self) -> bool:
@@ -279,9 +407,16 @@ class RingContext:
             o1 = base + 8 * de.size
             o2 = o1 + 8 * keys.size
             o3 = o2 + 8 * keys.size
+            e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
                                            de_bstride, dst_bstride, prime_last, per_job,
                                            last_term_bstride, self.stream), "ks_gemm")
+            if _STATS:   # digit sets [bc, ndig, rows] once, key rows once, outputs
+                _STATS.end("keyswitch_gemm", e0)
+                nbytes = (_uniq(de) * bc * rows + _uniq(keys) * (rows - 1) + _uniq(keys_last)
+                          + nout * bc * rows) * 8 * self.n
+                _STATS.add("keyswitch_gemm", nbytes, nout * ndig * bc * rows * self.n
+                           * StepStats.FP64_PER_MODMUL)
 
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):

@@ -53,9 +53,10 @@ cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStr
 struct HbCrtTask;
 cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
                               int, int, cudaStream_t);
-cudaError_t launch_encode(const double*, long long*, int, double, const HbFftTables&, int*,
+cudaError_t launch_encode(const double*, long long*, int, double, const HbFftTables&, int*, double2*, int,
                           cudaStream_t);
-cudaError_t launch_decode(const double*, double*, int, double, const HbFftTables&, cudaStream_t);
+cudaError_t launch_decode(const double*, double*, int, double, const HbFftTables&, double2*, int,
+                          cudaStream_t);
 }  // namespace hb
 
 using namespace hb;
@@ -82,6 +83,8 @@ struct hb_fft {
   double2* root_dev;
   double2* twist_dev;
   int* pos_dev;
+  double2* work_dev = nullptr;   // four-step FFT intermediate, work_polys polynomials
+  int work_polys = 0;
 };
 
 static thread_local char g_err[512];
@@ -401,26 +404,44 @@ int hb_crt_double(hb_ring* r, const void* tasks, int count, const unsigned long 
   return e ? fail(e, "hb_crt_double") : 0;
 }
 
+void hb_fft_destroy(hb_fft* f);
+
 hb_fft* hb_fft_create(int logn2, const double* root_re_im, const double* twist_re_im,
                       const int* slot_pos) {
   const int n2 = 1 << logn2;
+  if (logn2 < 8 || logn2 > 16) {
+    fail(cudaErrorInvalidValue, "hb_fft_create: ring degree outside 2^9..2^17");
+    return nullptr;
+  }
+  // the kernels index by DFT bin: invert slot j -> bin m_j (a permutation)
+  std::vector<int> slot_of(n2, -1);
+  for (int j = 0; j < n2; ++j) {
+    if (slot_pos[j] < 0 || slot_pos[j] >= n2 || slot_of[slot_pos[j]] >= 0) {
+      fail(cudaErrorInvalidValue, "hb_fft_create: slot_pos is not a permutation");
+      return nullptr;
+    }
+    slot_of[slot_pos[j]] = j;
+  }
   hb_fft* f = new hb_fft();
   f->t.logn2 = logn2;
   f->t.n2 = n2;
+  // 64 MB of intermediate: 512 polynomials per launch pair at N = 2^14, 128 at 2^16
+  f->work_polys = (int)((64ull << 20) / (sizeof(double2) * (size_t)n2));
   cudaError_t e;
   if ((e = cudaMalloc(&f->root_dev, sizeof(double2) * (n2 / 2))) ||
       (e = cudaMalloc(&f->twist_dev, sizeof(double2) * n2)) ||
       (e = cudaMalloc(&f->pos_dev, sizeof(int) * n2)) ||
+      (e = cudaMalloc(&f->work_dev, sizeof(double2) * (size_t)n2 * f->work_polys)) ||
       (e = cudaMemcpy(f->root_dev, root_re_im, sizeof(double2) * (n2 / 2), cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(f->twist_dev, twist_re_im, sizeof(double2) * n2, cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(f->pos_dev, slot_pos, sizeof(int) * n2, cudaMemcpyHostToDevice))) {
+      (e = cudaMemcpy(f->pos_dev, slot_of.data(), sizeof(int) * n2, cudaMemcpyHostToDevice))) {
     fail(e, "hb_fft_create");
-    delete f;
+    hb_fft_destroy(f);
     return nullptr;
   }
   f->t.root = f->root_dev;
   f->t.twist = f->twist_dev;
-  f->t.slot_pos = f->pos_dev;
+  f->t.slot_of = f->pos_dev;
   return f;
 }
 
@@ -429,18 +450,21 @@ void hb_fft_destroy(hb_fft* f) {
   cudaFree(f->root_dev);
   cudaFree(f->twist_dev);
   cudaFree(f->pos_dev);
+  cudaFree(f->work_dev);
   delete f;
 }
 
 int hb_encode(hb_fft* f, const double* slots, long long* coeffs, int npoly, double scale,
               int* overflow, void* stream) {
-  cudaError_t e = launch_encode(slots, coeffs, npoly, scale, f->t, overflow, (cudaStream_t)stream);
+  cudaError_t e = launch_encode(slots, coeffs, npoly, scale, f->t, overflow, f->work_dev,
+                                f->work_polys, (cudaStream_t)stream);
   return e ? fail(e, "hb_encode") : 0;
 }
 
 int hb_decode(hb_fft* f, const double* coeffs, double* slots, int npoly, double scale,
               void* stream) {
-  cudaError_t e = launch_decode(coeffs, slots, npoly, scale, f->t, (cudaStream_t)stream);
+  cudaError_t e = launch_decode(coeffs, slots, npoly, scale, f->t, f->work_dev, f->work_polys,
+                                (cudaStream_t)stream);
   return e ? fail(e, "hb_decode") : 0;
 }
 

@@ -152,7 +152,7 @@ struct HbFftTables {
   int n2;
   const double2* root;  // [n2/2]: e^{+2 pi i k / n2}
   const double2* twist; // [n2]:   zeta^k = e^{i pi k / N}
-  const int* slot_pos;  // [n2]:   m_j, slot j -> DFT bin
+  const int* slot_of;   // [n2]:   DFT bin m -> slot j with m_j = m (inverse of m_j)
 };
 
 // Clip-blocked key-switch inner product task (ops.cu k_ks_inner2).

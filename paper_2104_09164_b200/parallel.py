@@ -31,6 +31,28 @@ def init(backend: str) -> bool:
     return dist.is_initialized()
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(nproc: int, script: str, argv) -> int:
+    """Run `script argv` as `nproc` ranks of one node under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code.
+    Used when a multi-rank command is started as a plain process
+    (`python bench.py --gpus 8`)."""
+    import subprocess
+    import sys
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", script, *argv]
+    return subprocess.call(cmd)
+
+
 def shard(total: int, rank: int, world_size: int) -> range:
     """Contiguous, balanced slice of `total` clips owned by `rank`."""
     base, extra = divmod(total, world_size)

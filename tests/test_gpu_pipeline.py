@@ -145,3 +145,66 @@ def test_graph_with_pdl_bit_identical():
         got = g(ct).payload.data
         torch.cuda.synchronize()
         assert torch.equal(got, want)
+
+
+@pytest.fixture(scope="module")
+def pgold2():
+    with open(os.path.join(HERE, "golden", "pipeline_golden_r2.json")) as f:
+        return json.load(f)
+
+
+R2_KEYS = ["1d-w64/fast/full/fast-hear", "2d-w64/fast/giant/fast-hear", "2d-w64/hear/full/hear",
+           "2d-w128/fast/full/fast-hear"]
+
+
+@pytest.mark.parametrize("key", R2_KEYS)
+def test_r2_networks_match_reference(pgold2, key):
+    """The bench headline configuration and the 2D networks against the
+    reference CKKS engine's decrypted logits (tests/golden/make_golden_r2.py)."""
+    from paper_2104_09164_b200.model import net_by_name
+    if key not in pgold2:
+        pytest.skip(f"{key}: golden not generated")
+    net, mode, strat, prof = key.split("/")
+    g = pgold2[key]
+    lg, cnt, *_ = _run(net_by_name(net), g["model_seed"], g["input_seed"], prof, mode, strat,
+                       g["backend_seed"])
+    _check(lg, g)
+    assert cnt.as_dict() == g["counters"]
+    tol = 2.0 ** -9 if mode == "hear" else 2.0 ** -5
+    assert np.abs(lg - np.array(g["clear"])).max() <= tol
+
+
+def test_headline_graph_b128_matches_eager_and_reference(pgold2):
+    """The bench's timed object: 1d-w64 fast/full at fast-hear, 128 clips per
+    handle, replayed as the DEFAULT CUDA graph (no PDL).  The replay is
+    bit-identical to eager evaluation, and clip 0 (the golden's seeds)
+    decrypts to the reference CKKS engine's logits."""
+    import torch
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import (GraphedPipeline, compile_pipeline, dec_logits,
+                                                encrypt_input, run_pipeline)
+    from paper_2104_09164_b200.model import (collapse_layers, make_random_input, make_random_model,
+                                             net_by_name)
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    g = pgold2["1d-w64/fast/full/fast-hear"]
+    shape = net_by_name("1d-w64")
+    cpar = collapse_layers(make_random_model(shape, g["model_seed"]), shape)
+    be = CkksBackend(gen_params("fast-hear"), seed=g["backend_seed"])
+    cp = compile_pipeline(shape, "fast", "full", be.params)
+    be.ensure_rotation_keys(cp.rotations)
+    enc = ModelEncoder(cp, cpar, be).prepare()
+    x = np.stack([make_random_input(shape, g["input_seed"] + i) for i in range(128)])
+    ct = encrypt_input(x, cp, be)
+    be.reset_counters()
+    eager = run_pipeline(enc, ct, be)
+    assert be.counters.as_dict() == g["counters"]
+    want = eager.payload.data.clone()
+    assert os.environ.get("HEAR_B200_PDL", "0") == "0"
+    graph = GraphedPipeline(enc, be, batch=128)
+    for _ in range(2):
+        got = graph(ct)
+        torch.cuda.synchronize()
+        assert torch.equal(got.payload.data, want)
+    lg = dec_logits(got, cp, be)
+    _check(lg[0], g)

@@ -79,3 +79,62 @@ def test_gloo_key_replication_world2():
     assert res[0][0] == res[1][0]           # identical keys on both ranks
     assert res[0][1] == res[1][1] == 2.0    # max over ranks
     assert res[0][2] + res[1][2] == list(range(10))
+
+
+def _worker_layout(rank, port, q):
+    """Key replication over tensors of the REAL key layout (toy-fast params,
+    the toy network's rotation manifest), as the engine's receivers allocate."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE="2", LOCAL_RANK=str(rank))
+    from paper_2104_09164_b200 import parallel as par
+    from paper_2104_09164_b200.ckks.engine import key_layout
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline
+    from paper_2104_09164_b200.model import NetworkShape
+    par.init("gloo")
+    ps = gen_params("toy-fast")
+    cp = compile_pipeline(NetworkShape(1, 32, 15, (4, 8, 16), 4), "fast", "giant", ps)
+    man = par.broadcast_object(sorted(cp.rotations.items()) if rank == 0 else None)
+    g = torch.Generator().manual_seed(3)
+    keys = [torch.randint(0, 1 << 40, s, generator=g) if rank == 0 else
+            torch.empty(s, dtype=torch.int64) for _, s in key_layout(ps, man)]
+    par.broadcast_tensors(keys)
+    q.put((rank, [int(k.sum()) for k in keys], [tuple(k.shape) for k in keys]))
+    par.barrier()
+    torch.distributed.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_gloo_real_key_layout_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_layout, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict((r, (s, sh)) for r, s, sh in (q.get(timeout=150) for _ in ps))
+    for p in ps:
+        p.join(30)
+    assert res[0] == res[1]
+    from paper_2104_09164_b200.ckks.params import gen_params
+    n = gen_params("toy-fast").n
+    assert all(sh[-1] == n for sh in res[0][1])
+    assert len(res[0][1]) >= 6   # pk (2) + relin (2) + at least one rotation key pair
+
+
+@pytest.mark.timeout(300)
+def test_bench_spawns_ranks():
+    """`python bench.py --gpus 2` started as ONE process relaunches itself as
+    two ranks (torch.distributed.run) -- the path the driver's 8-GPU run
+    uses when it does not wrap bench.py in torchrun itself."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--check-launch"], capture_output=True, text=True, env=env, timeout=280)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_ranks"] == 2 and line["keys_identical"] and line["max_over_ranks"] == 2.0
