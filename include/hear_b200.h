@@ -59,6 +59,27 @@ int hear_pw_add(hb_ring* ring, unsigned long long* out, const unsigned long long
 int hear_pw_sub(hb_ring* ring, unsigned long long* out, const unsigned long long* a,
                 const unsigned long long* b, int nrows, const long long* gidx);
 
+/* ring.py:136 pw_mul_accum_perm(outb, outa, de, kb, ka, krow, perm, gidx, p, mu, sh):
+ * outb/outa[r] += sum_i de[i][r][perm[n]] * kb/ka[i][krow[r]][n] (mod p_gidx[r]);
+ * de [ndig][nrows][N], kb/ka [ndig][krows][N], perm [N] (intp), in place      */
+int hear_pw_mul_accum_perm(hb_ring* ring, unsigned long long* outb, unsigned long long* outa,
+                           const unsigned long long* de, const unsigned long long* kb,
+                           const unsigned long long* ka, const long long* krow,
+                           const long long* perm, const long long* gidx, int ndig, int nrows,
+                           int krows);
+/* ring.py:175 scalar_mul(a, c, gidx, p, mu, sh): a[r] *= c[r], in place       */
+int hear_scalar_mul(hb_ring* ring, unsigned long long* a, const unsigned long long* c, int nrows,
+                    const long long* gidx);
+/* ring.py:186 lift_center(x, p, out): residues -> centred int64 (one row)     */
+int hear_lift_center(const unsigned long long* x, unsigned long long p, long long* out, int n);
+/* ring.py:198 reduce_rows(c, gidx, p, out): centred int64 [N] -> [nrows][N]   */
+int hear_reduce_rows(hb_ring* ring, const long long* c, const long long* gidx, int nrows,
+                     unsigned long long* out);
+/* ring.py:210 sub_scaled_inv(rows, corr, pinv, gidx, p, mu, sh):
+ * rows[r] = (rows[r] - corr[r]) * pinv[r], in place                         */
+int hear_sub_scaled_inv(hb_ring* ring, unsigned long long* rows, const unsigned long long* corr,
+                        const unsigned long long* pinv, int nrows, const long long* gidx);
+
 /* ---- device task-table kernels --------------------------------------------- */
 /* Forward NTT over `count` row tasks (HbNttTask, csrc/ring.cuh).  mode 0:
  * plain (ring.py:113); 1: fused centred lift + reduce of a digit row, the

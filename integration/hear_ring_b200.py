@@ -1,57 +1,3 @@
-# INTEGRATION — using the B200 kernels from the reference package
-
-## 1. Drop-in at the engine level (recommended)
-
-The package exposes the reference API with the same names and argument
-meaning; switching is an import change:
-
-```python
-# before
-from hear.ckks.params import gen_params
-from hear.ckks.engine import CkksBackend
-from hear.fastpath import compile_pipeline, infer
-from hear.modelenc import ModelEncoder
-# after
-from paper_2104_09164_b200.ckks.params import gen_params
-from paper_2104_09164_b200.ckks.engine import CkksBackend
-from paper_2104_09164_b200.fastpath import compile_pipeline, infer
-from paper_2104_09164_b200.modelenc import ModelEncoder
-
-be = CkksBackend(gen_params("fast-hear"), seed=0)      # same keys as the reference
-cp = compile_pipeline(shape, "fast", "giant", be.params)
-be.ensure_rotation_keys(cp.rotations)
-logits, counters, enc = infer(collapsed, x, "fast", "giant", be,
-                              encoder=ModelEncoder(cp, collapsed, be))
-```
-
-`x` may also be a batch `(B, 32, 15, 2)`; the engine then evaluates B clips
-per kernel launch and returns `(B, classes)` logits.  Ciphertexts exchange
-with reference-format payloads via `be.export(ct) -> (c0, c1)` and
-`be.import_ct(c0, c1, level, scale)`.
-
-## 2. Kernel-level binding (ctypes stub a maintainer would add to hear/ckks/)
-
-The `hear_*` symbols of `include/hear_b200.h` take the reference's host arrays
-directly, one per numba kernel of `hear/ckks/ring.py`:
-
-| `hear_*` entry point | replaces (reference) |
-|---|---|
-| `hear_ntt_fwd` / `hear_ntt_inv` | `ring.py:113` `ntt_fwd`, `ring.py:120` `ntt_inv` (`RingContext.fwd/inv`, :296-300) |
-| `hear_pw_mul` / `hear_pw_add` / `hear_pw_sub` | `ring.py:127` `pw_mul`, `:159` `pw_add`, `:167` `pw_sub` |
-| `hear_pw_mul_accum_perm` | `ring.py:136` `pw_mul_accum_perm` (key-switch inner product with Galois gather) |
-| `hear_scalar_mul` | `ring.py:175` `scalar_mul` |
-| `hear_lift_center` | `ring.py:186` `lift_center` |
-| `hear_reduce_rows` | `ring.py:198` `reduce_rows` |
-| `hear_sub_scaled_inv` | `ring.py:210` `sub_scaled_inv` (rescale / ModDown core) |
-
-The complete binding is `integration/hear_ring_b200.py` (reproduced below);
-a maintainer copies it to `hear/ckks/ring_b200.py` and routes `RingContext`'s
-wrappers through `B200Ring`.  `tests/test_gpu_boundary.py` runs this file as
-written: every `hear_*` call against the reference's golden digests
-(`ckks_golden.json`) and the C oracle, and a guard test that the stub calls
-every `hear_*` symbol the header declares.
-
-```python
 """Kernel-level binding stub a maintainer adds to the reference package
 (as hear/ckks/ring_b200.py) to run its ring kernels on the B200 library.
 
@@ -177,32 +123,3 @@ class B200Ring:
         pinv, g = np.ascontiguousarray(pinv, dtype=np.uint64), _g(gidx)
         _ok(_L.hear_sub_scaled_inv(self.h, _u64(rows), _u64(corr), pinv.ctypes.data,
                                    rows.shape[0], g.ctypes.data), "sub_scaled_inv")
-```
-
-Each `hear_*` call copies its rows to the GPU, runs, and copies back, so at
-this granularity the PCIe round trip dominates; the engine-level drop-in (§1)
-keeps everything resident in HBM and is the intended integration.
-
-## 3. Device entry points (what the engine binds)
-
-`CkksBackend` drives the `hb_*` task-table entry points of
-`include/hear_b200.h` with device-resident rows: `hb_ntt_fwd` / `hb_ntt_inv`
-(cluster-fused or two-pass transforms with the ModUp / ModDown / rescale /
-rotate-and-add epilogues), `hb_ks_gemm` (every natural-order key-switch inner
-product as one per-coefficient GEMM), `hb_ks_inner2` (per-job inner product
-with the Galois gather), `hb_mac_shared` (a layer's plaintext MAC as a
-per-coefficient GEMM), `hb_mac_strided` (per-output term lists), `hb_sum`
-(many-term sums), `hb_ew`, `hb_tensor`, `hb_encode` / `hb_decode`,
-`hb_crt_double`.  Task layouts are `csrc/ring.cuh`; `_native.py` checks the
-numpy mirrors against `hb_sizeof_task` at load time.  `hb_ntt_kernels` and
-`hb_ring_uses_f64` report the launch count and arithmetic policy the library
-chose; `hb_set_pdl` switches programmatic dependent launch on for a CUDA-graph
-capture.
-
-## 4. Build
-
-```
-python -m paper_2104_09164_b200.build          # nvcc, sm_100a, in-tree .so
-python oracle/build.py                         # CPU oracle (tests only)
-python -c "import __graft_entry__ as g; g.build()"
-```

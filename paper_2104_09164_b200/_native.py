@@ -66,6 +66,11 @@ def lib():
             getattr(L, name).argtypes = [vp, vp, i32, vp]
         for name in ("hear_pw_mul", "hear_pw_add", "hear_pw_sub"):
             getattr(L, name).argtypes = [vp, vp, vp, vp, i32, vp]
+        L.hear_pw_mul_accum_perm.argtypes = [vp] * 9 + [i32] * 3
+        L.hear_scalar_mul.argtypes = [vp, vp, vp, i32, vp]
+        L.hear_lift_center.argtypes = [vp, ctypes.c_uint64, vp, i32]
+        L.hear_reduce_rows.argtypes = [vp, vp, vp, i32, vp]
+        L.hear_sub_scaled_inv.argtypes = [vp, vp, vp, vp, i32, vp]
         _lib = L
         _check_layouts()
     return _lib

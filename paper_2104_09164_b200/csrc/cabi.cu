@@ -50,6 +50,9 @@ cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, 
                                int, cudaStream_t);
 cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_lift_center(const u64*, u64, long long*, int, cudaStream_t);
+cudaError_t launch_reduce_rows(const long long*, const int*, int, const HbPrime*, u64*, int,
+                               cudaStream_t);
 struct HbCrtTask;
 cudaError_t launch_crt_double(const HbCrtTask*, int, const u64*, const HbPrime*, const int*, int,
                               int, int, cudaStream_t);
@@ -542,6 +545,183 @@ int hear_pw_add(hb_ring* r, unsigned long long* out, const unsigned long long* a
 int hear_pw_sub(hb_ring* r, unsigned long long* out, const unsigned long long* a,
                 const unsigned long long* b, int nrows, const long long* gidx) {
   return host_rows_op(r, nrows, gidx, 2 + 1, const_cast<unsigned long long*>(a), b, out);
+}
+
+}  // extern "C"
+
+// Device scratch of the remaining hear_* entry points: freed on every exit.
+namespace {
+struct DevBufs {
+  std::vector<void*> p;
+  ~DevBufs() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <typename T>
+  cudaError_t get(T** out, size_t bytes, const void* host = nullptr) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes ? bytes : 1);
+    if (e) return e;
+    p.push_back(q);
+    *out = (T*)q;
+    return host ? cudaMemcpy(q, host, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+  }
+};
+
+// EW launch over nrows host rows with per-row constants (scalar_mul /
+// sub_scaled_inv): dst = op(a[, b]) with scal = c[r] mod p_{gidx[r]}.
+int host_scaled_op(hb_ring* r, int op, unsigned long long* rows, const unsigned long long* corr,
+                   const unsigned long long* c, int nrows, const long long* gidx,
+                   const char* what) {
+  if (nrows <= 0) return 0;
+  const int n = r->dev.n;
+  const size_t bytes = (size_t)nrows * n * sizeof(u64);
+  DevBufs d;
+  u64 *da = nullptr, *db = nullptr;
+  HbEwTask* dt = nullptr;
+  std::vector<HbEwTask> t(nrows);
+  cudaError_t e;
+  if ((e = d.get(&da, bytes, rows))) return fail(e, what);
+  if (corr && (e = d.get(&db, bytes, corr))) return fail(e, what);
+  for (int i = 0; i < nrows; ++i) {
+    const int g = (int)gidx[i];
+    if (g < 0 || g >= r->dev.nprimes) return fail(cudaErrorInvalidValue, what);
+    const u64 p = r->primes_host[g].p;
+    memset(&t[i], 0, sizeof(HbEwTask));
+    t[i].dst = da + (size_t)i * n;
+    t[i].a = da + (size_t)i * n;
+    t[i].b = db ? db + (size_t)i * n : nullptr;
+    t[i].scal = c[i] % p;
+    t[i].scal_sh = shoup(t[i].scal, p);
+    t[i].prime = g;
+  }
+  if ((e = d.get(&dt, sizeof(HbEwTask) * nrows, t.data()))) return fail(e, what);
+  if ((e = launch_ew(op, dt, nrows, r->dev.primes, n, 0)) || (e = cudaDeviceSynchronize()) ||
+      (e = cudaMemcpy(rows, da, bytes, cudaMemcpyDeviceToHost)))
+    return fail(e, what);
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+// ring.py:175 scalar_mul(a, c, gidx, ...): a[r] *= c[r] in place.
+int hear_scalar_mul(hb_ring* r, unsigned long long* a, const unsigned long long* c, int nrows,
+                    const long long* gidx) {
+  return host_scaled_op(r, EW_MUL_SCALAR, a, nullptr, c, nrows, gidx, "hear_scalar_mul");
+}
+
+// ring.py:210 sub_scaled_inv(rows, corr, pinv, gidx, ...):
+// rows[r] = (rows[r] - corr[r]) * pinv[r] in place.
+int hear_sub_scaled_inv(hb_ring* r, unsigned long long* rows, const unsigned long long* corr,
+                        const unsigned long long* pinv, int nrows, const long long* gidx) {
+  return host_scaled_op(r, EW_SUB_SCALED, rows, corr, pinv, nrows, gidx, "hear_sub_scaled_inv");
+}
+
+// ring.py:136 pw_mul_accum_perm(outb, outa, de, kb, ka, krow, perm, gidx, ...):
+// outb/outa[r] += sum_i de[i][r][perm[n]] * kb/ka[i][krow[r]][n]  (mod p_{gidx[r]}).
+// de: [ndig][nrows][N]; kb, ka: [ndig][krows][N]; perm: [N] (the reference's
+// intp array); the inner product runs as the engine's per-job key-switch
+// kernel (Galois gather on the digits), then one modular add into out.
+int hear_pw_mul_accum_perm(hb_ring* r, unsigned long long* outb, unsigned long long* outa,
+                           const unsigned long long* de, const unsigned long long* kb,
+                           const unsigned long long* ka, const long long* krow,
+                           const long long* perm, const long long* gidx, int ndig, int nrows,
+                           int krows) {
+  const char* what = "hear_pw_mul_accum_perm";
+  if (nrows <= 0) return 0;
+  const int n = r->dev.n;
+  const size_t row = (size_t)n * sizeof(u64);
+  DevBufs d;
+  u64 *dde, *dkb, *dka, *dob, *doa, *dib, *dia;
+  int* dperm;
+  cudaError_t e;
+  std::vector<int> p32(n);
+  for (int j = 0; j < n; ++j) {
+    if (perm[j] < 0 || perm[j] >= n) return fail(cudaErrorInvalidValue, what);
+    p32[j] = (int)perm[j];
+  }
+  if ((e = d.get(&dde, row * ndig * nrows, de)) || (e = d.get(&dkb, row * ndig * krows, kb)) ||
+      (e = d.get(&dka, row * ndig * krows, ka)) || (e = d.get(&dob, row * nrows, outb)) ||
+      (e = d.get(&doa, row * nrows, outa)) || (e = d.get(&dib, row * nrows)) ||
+      (e = d.get(&dia, row * nrows)) || (e = d.get(&dperm, sizeof(int) * n, p32.data())))
+    return fail(e, what);
+  std::vector<HbKsTask2> kt(nrows);
+  std::vector<HbEwTask> at(2 * nrows);
+  for (int i = 0; i < nrows; ++i) {
+    if (krow[i] < 0 || krow[i] >= krows || gidx[i] < 0 || gidx[i] >= r->dev.nprimes)
+      return fail(cudaErrorInvalidValue, what);
+    memset(&kt[i], 0, sizeof(HbKsTask2));
+    kt[i].de = dde + (size_t)i * n;
+    kt[i].kb = dkb + (size_t)krow[i] * n;
+    kt[i].ka = dka + (size_t)krow[i] * n;
+    kt[i].out_b = dib + (size_t)i * n;
+    kt[i].out_a = dia + (size_t)i * n;
+    kt[i].perm = dperm;
+    kt[i].de_dstride = (long long)nrows * n;
+    kt[i].key_stride = (long long)krows * n;
+    kt[i].ndig = ndig;
+    kt[i].prime = (int)gidx[i];
+    for (int c = 0; c < 2; ++c) {
+      HbEwTask& t = at[2 * i + c];
+      memset(&t, 0, sizeof(HbEwTask));
+      t.dst = (c ? doa : dob) + (size_t)i * n;
+      t.a = t.dst;
+      t.b = (c ? dia : dib) + (size_t)i * n;
+      t.prime = (int)gidx[i];
+    }
+  }
+  HbKsTask2* dkt;
+  HbEwTask* dat;
+  if ((e = d.get(&dkt, sizeof(HbKsTask2) * nrows, kt.data())) ||
+      (e = d.get(&dat, sizeof(HbEwTask) * 2 * nrows, at.data())))
+    return fail(e, what);
+  if (hb_ks_inner2(r, dkt, nrows, 1, nullptr)) return (int)cudaErrorLaunchFailure;
+  if ((e = launch_ew(EW_ADD, dat, 2 * nrows, r->dev.primes, n, 0)) ||
+      (e = cudaDeviceSynchronize()) ||
+      (e = cudaMemcpy(outb, dob, row * nrows, cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(outa, doa, row * nrows, cudaMemcpyDeviceToHost)))
+    return fail(e, what);
+  return 0;
+}
+
+// ring.py:186 lift_center(x, p, out): one row of residues mod p -> centred int64.
+int hear_lift_center(const unsigned long long* x, unsigned long long p, long long* out, int n) {
+  if (n <= 0) return 0;
+  DevBufs d;
+  u64* dx;
+  long long* dout;
+  cudaError_t e;
+  if ((e = d.get(&dx, sizeof(u64) * n, x)) || (e = d.get(&dout, sizeof(long long) * n)) ||
+      (e = launch_lift_center(dx, p, dout, n, 0)) || (e = cudaDeviceSynchronize()) ||
+      (e = cudaMemcpy(out, dout, sizeof(long long) * n, cudaMemcpyDeviceToHost)))
+    return fail(e, "hear_lift_center");
+  return 0;
+}
+
+// ring.py:198 reduce_rows(c, gidx, p, out): centred int64 coefficients [N] ->
+// residues out[r] under prime gidx[r], out [nrows][N].
+int hear_reduce_rows(hb_ring* r, const long long* c, const long long* gidx, int nrows,
+                     unsigned long long* out) {
+  if (nrows <= 0) return 0;
+  const int n = r->dev.n;
+  DevBufs d;
+  long long* dc;
+  int* dg;
+  u64* dout;
+  std::vector<int> g32(nrows);
+  for (int i = 0; i < nrows; ++i) {
+    if (gidx[i] < 0 || gidx[i] >= r->dev.nprimes)
+      return fail(cudaErrorInvalidValue, "hear_reduce_rows");
+    g32[i] = (int)gidx[i];
+  }
+  cudaError_t e;
+  if ((e = d.get(&dc, sizeof(long long) * n, c)) || (e = d.get(&dg, sizeof(int) * nrows, g32.data())) ||
+      (e = d.get(&dout, sizeof(u64) * n * nrows)) ||
+      (e = launch_reduce_rows(dc, dg, nrows, r->dev.primes, dout, n, 0)) ||
+      (e = cudaDeviceSynchronize()) ||
+      (e = cudaMemcpy(out, dout, sizeof(u64) * n * nrows, cudaMemcpyDeviceToHost)))
+    return fail(e, "hear_reduce_rows");
+  return 0;
 }
 
 }  // extern "C"

@@ -10,19 +10,6 @@
 
 namespace hb {
 
-enum EwOp : int {
-  EW_ADD = 0,       // dst = a + b                       (ring.py:159 pw_add)
-  EW_SUB = 1,       // dst = a - b                       (ring.py:167 pw_sub)
-  EW_MUL = 2,       // dst = a * b                       (ring.py:127 pw_mul)
-  EW_MUL_SCALAR = 3,// dst = a * scal                    (ring.py:175 scalar_mul)
-  EW_MULADD = 4,    // dst = a * b + c                   (engine.py:202-203)
-  EW_ADD_SCALED = 5,// dst = a + b * scal                (engine.py:204-208)
-  EW_COPY = 6,      // dst = a
-  EW_PERM = 7,      // dst = a[perm]  (b reinterpreted as int32 perm)
-  EW_SUB_SCALED = 8,// dst = (a - b) * scal              (ring.py:210 sub_scaled_inv)
-  EW_PERM_ADD = 9,  // dst = a[perm] + b[perm]  (c reinterpreted as int32 perm): the
-                    // Galois gather of a rotation applied after ModDown (engine.py:350)
-};
 
 constexpr int EW_THREADS = 256;
 
@@ -622,6 +609,44 @@ k_ks_inner2(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ pri
   ra.y = a1.fold(P);
   *reinterpret_cast<ulonglong2*>(tk.out_b + b * tk.out_bstride + j) = rb;
   *reinterpret_cast<ulonglong2*>(tk.out_a + b * tk.out_bstride + j) = ra;
+}
+
+// ring.py:186 lift_center: residues mod p -> centred int64 in (-p/2, p/2].
+__global__ void k_lift_center(const u64* __restrict__ x, u64 p, long long* __restrict__ out,
+                              int n) {
+  HB_PDL_ENTRY();
+  const u64 half = p >> 1;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const u64 v = x[j];
+    out[j] = v > half ? (long long)v - (long long)p : (long long)v;
+  }
+}
+
+// ring.py:198 reduce_rows: one centred int64 coefficient vector -> residues
+// under the prime of every output row (grid.y = row).
+__global__ void k_reduce_rows(const long long* __restrict__ c, const int* __restrict__ gidx,
+                              const HbPrime* __restrict__ primes, u64* __restrict__ out, int n) {
+  HB_PDL_ENTRY();
+  const long long p = (long long)primes[gidx[blockIdx.y]].p;
+  u64* o = out + (size_t)blockIdx.y * n;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    long long v = c[j] % p;
+    o[j] = (u64)(v < 0 ? v + p : v);
+  }
+}
+
+cudaError_t launch_lift_center(const u64* x, u64 p, long long* out, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  (void)hb_launch(k_lift_center, dim3((n + 255) / 256), dim3(256), 0, st, x, p, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_rows(const long long* c, const int* gidx, int nrows,
+                               const HbPrime* primes, u64* out, int n, cudaStream_t st) {
+  if (n <= 0 || nrows <= 0) return cudaSuccess;
+  (void)hb_launch(k_reduce_rows, dim3((n + 255) / 256, nrows), dim3(256), 0, st, c, gidx, primes,
+                  out, n);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ks_inner2(const void* tasks, int ntasks, int nb, const HbPrime* primes, int n,

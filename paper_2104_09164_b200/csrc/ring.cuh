@@ -146,6 +146,21 @@ struct HbEwTask {
   int _pad;
 };
 
+// Element-wise ops of ops.cu k_ew (launch_ew / hb_ew).
+enum EwOp : int {
+  EW_ADD = 0,       // dst = a + b                       (ring.py:159 pw_add)
+  EW_SUB = 1,       // dst = a - b                       (ring.py:167 pw_sub)
+  EW_MUL = 2,       // dst = a * b                       (ring.py:127 pw_mul)
+  EW_MUL_SCALAR = 3,// dst = a * scal                    (ring.py:175 scalar_mul)
+  EW_MULADD = 4,    // dst = a * b + c                   (engine.py:202-203)
+  EW_ADD_SCALED = 5,// dst = a + b * scal                (engine.py:204-208)
+  EW_COPY = 6,      // dst = a
+  EW_PERM = 7,      // dst = a[perm]  (b reinterpreted as int32 perm)
+  EW_SUB_SCALED = 8,// dst = (a - b) * scal              (ring.py:210 sub_scaled_inv)
+  EW_PERM_ADD = 9,  // dst = a[perm] + b[perm]  (c reinterpreted as int32 perm): the
+                    // Galois gather of a rotation applied after ModDown (engine.py:350)
+};
+
 // Special-FFT tables of the canonical embedding (fft.cu).
 struct HbFftTables {
   int logn2;            // log2(N/2)
