@@ -42,11 +42,23 @@ def parse():
     ap.add_argument("--net", default="1d-w64")
     ap.add_argument("--mode", default="fast", choices=["fast", "hear"])
     ap.add_argument("--strategy", default="full", choices=["full", "giant", "baby"])
-    ap.add_argument("--batch", type=int, default=128, help="clips per GPU per step")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="clips per GPU per step (default 128); with --workload config2 the "
+                         "clips per graph replay (default 64: the N=2^15 graph's temporaries "
+                         "at 128 clips plus 4096 resident clips exceed 180 GB)")
+    ap.add_argument("--workload", default="default",
+                    choices=["default", "config0", "config2", "config3"],
+                    help="config2: BASELINE config 2 -- 4096 clips per step at N=2^15 "
+                         "(fast-hear ladder), sharded across the ranks (strong scaling); "
+                         "config0 / config3: BASELINE's temporal networks (tcn.py) at "
+                         "fast-hear (N=2^14) / tcn-2^16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--check-launch", action="store_true",
                     help="multi-rank plumbing only: spawn, key replication, max-over-ranks")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.batch is None:   # config3: N = 2^16 rows are 4x the default ring's
+        args.batch = {"config2": 64, "config3": 32}.get(args.workload, 128)
+    return args
 
 
 def profile_of(mode: str) -> str:
@@ -110,27 +122,94 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- CPU arm
 
+def workload_params(args):
+    from paper_2104_09164_b200.ckks import params as P
+    if args.workload == "config2":
+        return P.fast_hear_ring(15)
+    if args.workload == "config3":
+        return P.tcn_ring16()
+    return P.gen_params(profile_of(args.mode))
+
+
+class Workload:
+    """One network on one parameter set, behind the calls the harness
+    makes: the reference's HEAR networks (compile_pipeline / ModelEncoder /
+    run_pipeline) or the temporal networks of BASELINE configs 0 and 3
+    (tcn.compile_tcn / TcnEncoder / run_tcn)."""
+
+    def __init__(self, args):
+        self.params = workload_params(args)
+        self.tcn = args.workload in ("config0", "config3")
+        if self.tcn:
+            from paper_2104_09164_b200 import tcn
+            self.T = tcn
+            self.shape = tcn.tcn_by_name(args.workload)
+            self.model = tcn.make_random_tcn(self.shape, 1, tcn.TCN_WEIGHT_STD[args.workload])
+            self.plan = tcn.compile_tcn(self.shape, self.params)
+            self.name = (f"BASELINE {args.workload} temporal network "
+                         f"({'; '.join(f'conv k={c.kernel} f={c.filters} s={c.stride}' for c in self.shape.convs)}"
+                         f"; {'/'.join(self.shape.acts)}; {self.shape.classes} classes)")
+        else:
+            from paper_2104_09164_b200.fastpath import compile_pipeline
+            from paper_2104_09164_b200.model import collapse_layers, make_random_model
+            from paper_2104_09164_b200.model import net_by_name
+            self.shape = net_by_name(args.net)
+            self.model = collapse_layers(make_random_model(self.shape, 1), self.shape)
+            self.plan = compile_pipeline(self.shape, args.mode, args.strategy, self.params)
+            self.name = f"HEAR CNN {args.net} {args.mode}/{args.strategy}"
+
+    def encoder(self, be):
+        if self.tcn:
+            return self.T.TcnEncoder(self.plan, self.model, be).prepare()
+        from paper_2104_09164_b200.modelenc import ModelEncoder
+        return ModelEncoder(self.plan, self.model, be).prepare()
+
+    @property
+    def run(self):
+        if self.tcn:
+            return self.T.run_tcn
+        from paper_2104_09164_b200.fastpath import run_pipeline
+        return run_pipeline
+
+    def make_input(self, seed: int):
+        if self.tcn:
+            return self.T.make_random_clip(self.shape, seed)
+        from paper_2104_09164_b200.model import make_random_input
+        return make_random_input(self.shape, seed)
+
+    def encrypt(self, x, be):
+        if self.tcn:
+            return self.T.encrypt_tcn_input(x, self.plan, be)
+        from paper_2104_09164_b200.fastpath import encrypt_input
+        return encrypt_input(x, self.plan, be)
+
+    def dec(self, out, enc, be):
+        if self.tcn:
+            return self.T.dec_tcn_logits(out, enc, be)
+        from paper_2104_09164_b200.fastpath import dec_logits
+        return dec_logits(out, self.plan, be)
+
+    def clear(self, x):
+        if self.tcn:
+            return self.T.infer_clear_tcn(self.model, x)
+        from paper_2104_09164_b200.model import infer_clear
+        return infer_clear(self.model, x)
+
+
 def cpu_oracle_run(args, n_clips: int, warm: int = 0):
     """Time the CPU oracle (oracle/, C + OpenMP port of the reference engine)
     on `n_clips` single-clip inferences.  Returns (clips/s, threads, per-clip s)."""
     from oracle.cpu_engine import OracleCkks, lib
-    from paper_2104_09164_b200.ckks.params import gen_params
-    from paper_2104_09164_b200.fastpath import compile_pipeline, encrypt_input, run_pipeline
-    from paper_2104_09164_b200.model import collapse_layers, make_random_input, make_random_model
-    from paper_2104_09164_b200.model import net_by_name
-    from paper_2104_09164_b200.modelenc import ModelEncoder
-    shape = net_by_name(args.net)
-    cpar = collapse_layers(make_random_model(shape, 1), shape)
-    be = OracleCkks(gen_params(profile_of(args.mode)), seed=0)
-    cp = compile_pipeline(shape, args.mode, args.strategy, be.params)
-    be.ensure_rotation_keys(cp.rotations)
-    enc = ModelEncoder(cp, cpar, be).prepare()   # model encoding is setup, not per clip
-    cts = [encrypt_input(make_random_input(shape, 1000 + i), cp, be) for i in range(warm + n_clips)]
+    wl = Workload(args)
+    be = OracleCkks(wl.params, seed=0)
+    be.ensure_rotation_keys(wl.plan.rotations)
+    enc = wl.encoder(be)   # model encoding is setup, not per clip
+    cts = [wl.encrypt(wl.make_input(1000 + i), be) for i in range(warm + n_clips)]
     for i in range(warm):
-        run_pipeline(enc, cts[i], be)
+        wl.run(enc, cts[i], be)
     t0 = time.perf_counter()
     for i in range(warm, warm + n_clips):
-        run_pipeline(enc, cts[i], be)
+        wl.run(enc, cts[i], be)
     dt = time.perf_counter() - t0
     return n_clips / dt, int(lib().or_num_threads()), dt / max(n_clips, 1)
 
@@ -142,16 +221,16 @@ def reference_arm(args):
         return
     value, cores, per_clip = cpu_oracle_run(args, args.steps, warm=args.warmup)
     sample = (f"{args.steps} timed single-clip encrypted inferences ({args.warmup} warm-up) of "
-              f"{args.net}/{args.mode}/{args.strategy} at {profile_of(args.mode)} parameters")
+              f"{args.net}/{args.mode}/{args.strategy} at {workload_params(args).name} parameters")
     line = {
         "metric": metric_name(), "value": value, "unit": "inferences/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_clip * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"HEAR CNN {args.net} {args.mode}/{args.strategy}, "
-                   f"{profile_of(args.mode)} params, 1 clip per step on the host CPU",
+        "config": {"workload": f"{Workload(args).name}, "
+                   f"{workload_params(args).name} params, 1 clip per step on the host CPU",
                    "net": args.net, "mode": args.mode, "strategy": args.strategy,
-                   "params": profile_of(args.mode), "clips_per_step": 1},
+                   "params": workload_params(args).name, "clips_per_step": 1},
         "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0,
@@ -228,7 +307,8 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     peak = peaks.get("hbm_gbs", 6650.0)
     bfly = m * r * (n // 2) * (n.bit_length() - 1)
     fp64_frac = bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12)
-    kname = "k_ntt3_fwd<FWD_MODDOWN_SCATTER>"
+    kname = ("k_ntt3_fwd<FWD_MODDOWN_SCATTER>" if lifted
+             else "k_ntt2_cols + k_ntt2_blocks<FWD_MODDOWN_SCATTER>")
     traffic = None
     try:
         with open(TRAFFIC_FILE) as f:
@@ -241,7 +321,7 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     # modular butterflies run as fp64 instructions; no tensor-core work)
     hbm_frac = gbs / peak
     bound = "hbm" if hbm_frac >= fp64_frac else "fp64"
-    return {"kernel": kname + " (rotation ModDown: cluster NTT + fused epilogue)",
+    return {"kernel": kname + " (rotation ModDown: NTT + fused epilogue)",
             "bound": bound, "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
             "frac": round(hbm_frac, 4), "traffic": traffic, "launch_us": round(sec * 1e6, 2),
             "rows_per_launch": m * r, "algorithmic_bytes_per_launch": algo,
@@ -330,11 +410,6 @@ def gpu_arm(args):
     from paper_2104_09164_b200 import parallel as par
     from paper_2104_09164_b200.ckks.engine import CkksBackend
     from paper_2104_09164_b200.ckks.params import gen_params
-    from paper_2104_09164_b200.fastpath import (compile_pipeline, dec_logits, encrypt_input,
-                                                run_pipeline)
-    from paper_2104_09164_b200.model import (collapse_layers, infer_clear, make_random_input,
-                                             make_random_model, net_by_name)
-    from paper_2104_09164_b200.modelenc import ModelEncoder
     from paper_2104_09164_b200.backend import Ct
     from paper_2104_09164_b200.ckks.engine import CtData
     from paper_2104_09164_b200.fastpath import GraphedPipeline
@@ -353,29 +428,44 @@ def gpu_arm(args):
     except OSError:
         pass
 
-    params = gen_params(profile_of(args.mode))
-    shape = net_by_name(args.net)
-    cpar = collapse_layers(make_random_model(shape, 1), shape)
-    cp = compile_pipeline(shape, args.mode, args.strategy, params)
+    if args.workload == "config2" and args.mode != "fast":
+        raise SystemExit("config2 runs the fast-hear ladder (--mode fast)")
+    wl = Workload(args)
+    params = wl.params
+    run_pipeline = wl.run
     # receivers encrypt from their own stream (never the sender's keygen stream)
     be = CkksBackend(params, seed=0, device=dev, keygen=(rank == 0),
                      enc_seed=np.random.SeedSequence(0, spawn_key=(rank,)))
     if rank == 0:
-        be.ensure_rotation_keys(cp.rotations)
+        be.ensure_rotation_keys(wl.plan.rotations)
     par.replicate_keys(be, src=0)
-    enc = ModelEncoder(cp, cpar, be).prepare()
-    bsz = args.batch
-    seeds = [10_000 * (rank + 1) + i for i in range(bsz)]
-    x = np.stack([make_random_input(shape, s) for s in seeds])
-    ct = encrypt_input(x, cp, be)
-    host_in = ct.payload.data.cpu().pin_memory()
+    enc = wl.encoder(be)
+    if args.workload == "config2":
+        # 4096 clips per step over all ranks, each rank's shard resident in
+        # HBM as handles of `batch` clips (one graph replay each)
+        mine = list(par.shard(4096, rank, ws))
+        bsz = min(args.batch, len(mine))
+        if len(mine) % bsz:
+            raise SystemExit(f"{len(mine)} clips per rank is not a multiple of --batch {bsz}")
+        seeds = [10_000 + i for i in mine]
+    else:
+        bsz = args.batch
+        seeds = [10_000 * (rank + 1) + i for i in range(bsz)]
+    chunks, xs = [], []
+    for c0 in range(0, len(seeds), bsz):
+        xc = np.stack([wl.make_input(s) for s in seeds[c0:c0 + bsz]])
+        chunks.append(wl.encrypt(xc, be))
+        xs.append(xc)
+    ct, x = chunks[0], xs[0]
+    host_in = [c.payload.data.cpu().pin_memory() for c in chunks]
     out0 = run_pipeline(enc, ct, be)
-    host_out = torch.empty(out0.payload.data.shape, dtype=torch.int64).pin_memory()
+    host_out = [torch.empty(out0.payload.data.shape, dtype=torch.int64).pin_memory()
+                for _ in chunks]
     torch.cuda.synchronize()
     maxerr = None
     if rank == 0:
-        lg = dec_logits(out0, cp, be)
-        ref = np.stack([infer_clear(cpar, xi) for xi in x])
+        lg = wl.dec(out0, enc, be)
+        ref = np.stack([wl.clear(xi) for xi in x])
         maxerr = float(np.abs(lg - ref).max())
 
     st = torch.cuda.current_stream()
@@ -384,7 +474,7 @@ def gpu_arm(args):
     run_pipeline(enc, ct, be)
     per_step_kernels = nat.kernel_launches() - k0
     # the timed loops replay the pipeline captured as one CUDA graph
-    graph = GraphedPipeline(enc, be, batch=bsz)
+    graph = GraphedPipeline(enc, be, batch=bsz, run=wl.run)
     for _ in range(args.warmup):
         graph(ct)
     torch.cuda.synchronize()
@@ -399,12 +489,13 @@ def gpu_arm(args):
             torch.cuda.profiler.start()
         e0.record(st)
         for _ in range(args.steps):
-            graph(ct)
+            for c in chunks:
+                graph(c)
         e1.record(st)
         torch.cuda.synchronize()
         if prof_range:
             torch.cuda.profiler.stop()
-    launches = per_step_kernels * args.steps
+    launches = per_step_kernels * args.steps * len(chunks)
     par.barrier()
     ms = par.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
 
@@ -422,44 +513,49 @@ def gpu_arm(args):
     ev_out = [torch.cuda.Event() for _ in range(2)]
     ev_d2h = [torch.cuda.Event() for _ in range(2)]
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nch = len(chunks)
+    jobs = args.steps * nch    # one job = one handle of bsz clips (a graph replay)
     f0.record(st)
     cs.wait_stream(st)
     with torch.cuda.stream(cs):
-        stage_in[0].copy_(host_in, non_blocking=True)
+        stage_in[0].copy_(host_in[0], non_blocking=True)
         ev_in[0].record(cs)
-    for i in range(args.steps):
+    for i in range(jobs):
         b = i % 2
         st.wait_event(ev_in[b])
         graph.inp.copy_(stage_in[b])
         ev_free[b].record(st)
-        if i + 1 < args.steps:   # next step's input, into the other staging buffer
+        if i + 1 < jobs:   # next job's input, into the other staging buffer
             with torch.cuda.stream(cs):
                 if i >= 1:
                     cs.wait_event(ev_free[1 - b])
-                stage_in[1 - b].copy_(host_in, non_blocking=True)
+                stage_in[1 - b].copy_(host_in[(i + 1) % nch], non_blocking=True)
                 ev_in[1 - b].record(cs)
         graph.graph.replay()
-        if i >= 2:   # step i-2's read-back of this staging buffer is done
+        if i >= 2:   # job i-2's read-back of this staging buffer is done
             st.wait_event(ev_d2h[b])
         stage_out[b].copy_(graph.out.payload.data)
         ev_out[b].record(st)
         with torch.cuda.stream(cs):
             cs.wait_event(ev_out[b])
-            host_out.copy_(stage_out[b], non_blocking=True)
+            host_out[i % nch].copy_(stage_out[b], non_blocking=True)
             ev_d2h[b].record(cs)
     st.wait_stream(cs)
     f1.record(st)
     torch.cuda.synchronize()
     par.barrier()
     ms_e2e = par.max_over_ranks(f0.elapsed_time(f1) / args.steps, dev)
-    if rank == 0:   # the graph's output decrypts to the clear network's logits
-        out_ct = Ct(CtData(host_out.to(dev)), 0, cp.expected("fc").scale, be.n2)
-        maxerr = max(maxerr, float(np.abs(dec_logits(out_ct, cp, be) - ref).max()))
+    if rank == 0:   # the replays' outputs decrypt to the clear network's logits
+        for q in sorted({0, nch - 1}):
+            fc = wl.plan.expected("fc")
+            out_ct = Ct(CtData(host_out[q].to(dev)), fc.level, fc.scale, be.n2)
+            refq = np.stack([wl.clear(xi) for xi in xs[q]])
+            maxerr = max(maxerr, float(np.abs(wl.dec(out_ct, enc, be) - refq).max()))
 
     # ---- per-clip latency: single-clip graph, replays timed one by one
     lat = []
-    g1 = GraphedPipeline(enc, be, batch=1)
-    one = encrypt_input(x[0], cp, be)
+    g1 = GraphedPipeline(enc, be, batch=1, run=wl.run)
+    one = wl.encrypt(x[0], be)
     for i in range(3 + max(args.steps, 10)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -474,7 +570,7 @@ def gpu_arm(args):
 
     roof = ks = steproof = None
     if rank == 0:
-        steproof = step_roofline(enc, ct, be, run_pipeline, ms, peaks)
+        steproof = step_roofline(enc, ct, be, run_pipeline, ms / len(chunks), peaks)
     if rank == 0:   # per-GPU kernel figures; the other ranks hold no secret key
         # one rotation ModDown over 64 clips (the shape of the committed ncu capture)
         roof = dominant_kernel_roofline(be, lvl=params.max_level, bsz=64, peaks=peaks)
@@ -496,22 +592,29 @@ def gpu_arm(args):
         # (DESIGN.md §2); a larger error means a broken kernel: no number
         raise SystemExit(f"decrypted logits deviate from the clear network by {maxerr}")
     if rank == 0:
-        total = bsz * ws
+        per_gpu = bsz * len(chunks)
+        total = per_gpu * ws
+        wl = (f"BASELINE config 2: 4096 clips per step sharded over {ws} GPU(s), "
+              f"{len(chunks)} handles of {bsz} clips per GPU" if args.workload == "config2"
+              else f"{bsz} clips per GPU per step")
         line = {
             "metric": metric_name(), "value": total / (ms / 1e3), "unit": "inferences/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True,
+            "scaling": "strong" if args.workload == "config2" else "weak",
+            "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
-            "config": {"workload": f"HEAR CNN {args.net} {args.mode}/{args.strategy}, "
+            "config": {"workload": f"{wl.name}, "
                        f"{params.name} params (N=2^{params.n.bit_length() - 1}, L={params.max_level}),"
-                       f" {bsz} clips per GPU per step", "net": args.net, "mode": args.mode,
-                       "strategy": args.strategy, "params": params.name, "clips_per_gpu": bsz,
+                       f" {wl}", "net": args.net, "mode": args.mode,
+                       "strategy": args.strategy, "params": params.name, "clips_per_gpu": per_gpu,
+                       "clips_per_replay": bsz,
                        "global_clips_per_step": total, "parallelism": f"clip-sharded dp{ws}",
                        "l2": "working set (keys + plaintexts + ciphertexts) >> 126 MB L2",
                        "latency_ms_per_batch": ms, "decrypt_max_abs_err_vs_clear": maxerr},
             "e2e": {"value": total / (ms_e2e / 1e3), "unit": "inferences/s",
-                    "h2d_bytes_per_step": int(host_in.numel() * 8),
-                    "d2h_bytes_per_step": int(host_out.numel() * 8)},
+                    "h2d_bytes_per_step": int(sum(h.numel() for h in host_in) * 8),
+                    "d2h_bytes_per_step": int(sum(h.numel() for h in host_out) * 8)},
             "gpu_launches": launches,
             "per_clip_latency": latency,
             "keyswitch": ks,

@@ -60,3 +60,15 @@ def test_no_cpu_fallback():
     from paper_2104_09164_b200.ckks.params import gen_params
     with pytest.raises(nat.NativeError, match="CUDA device"):
         CkksBackend(gen_params("toy-fast"), seed=1)
+
+
+def test_every_hear_symbol_is_called():
+    """Guard: the integration stub (run as written by test_gpu_boundary.py) binds
+    every hear_* entry point the header declares."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hdr = re.sub(r"/\*.*?\*/", "", open(os.path.join(root, "include", "hear_b200.h")).read(),
+                 flags=re.S)
+    declared = set(re.findall(r"\b(hear_[a-z0-9_]+)\s*\(", hdr))
+    stub = open(os.path.join(root, "integration", "hear_ring_b200.py")).read()
+    called = set(re.findall(r"_L\.(hear_[a-z0-9_]+)\b", stub))
+    assert declared == called, declared ^ called
