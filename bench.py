@@ -285,9 +285,12 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     L = nat.lib()
     st = torch.cuda.current_stream()
 
+    # two-pass rings (N >= 2^15): the ModDown gathers c0 through the Galois
+    # map instead (the scatter form exists on the cluster NTT only)
+    mode = nat.FWD_MODDOWN_SCATTER if lifted else nat.FWD_MODDOWN
+
     def launch():
-        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), nat.FWD_MODDOWN_SCATTER,
-                               st.cuda_stream), "ntt")
+        nat.check(L.hb_ntt_fwd(be.ring.handle, d.data_ptr(), len(t), mode, st.cuda_stream), "ntt")
     for _ in range(3):
         launch()
     reps = 20
@@ -308,7 +311,7 @@ def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     bfly = m * r * (n // 2) * (n.bit_length() - 1)
     fp64_frac = bfly * 8 / sec / (FP64_MEASURED_TFLOPS * 1e12)
     kname = ("k_ntt3_fwd<FWD_MODDOWN_SCATTER>" if lifted
-             else "k_ntt2_cols + k_ntt2_blocks<FWD_MODDOWN_SCATTER>")
+             else "k_ntt2_cols + k_ntt2_blocks<FWD_MODDOWN> (c0 gathered)")
     traffic = None
     try:
         with open(TRAFFIC_FILE) as f:

@@ -42,7 +42,7 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
                         const unsigned long long* psi, const unsigned long long* ipsi);
 void hb_ring_destroy(hb_ring* ring);
 int hb_ring_prime_consts(const hb_ring* ring, int prime_index, unsigned long long* out8);
-int hb_sizeof_task(int kind); /* 0 ntt, 1 ew, 2 mac, 3 mac-term, 4 ks */
+int hb_sizeof_task(int kind); /* 0 ntt, 1 ew, 2 mac, 3 mac-term, 4 ks, 5 ks2, 6 bconv */
 
 /* ---- reference-shaped host-buffer kernels (hear/ckks/ring.py) ------------ */
 /* ring.py:113 ntt_fwd(a, gidx, psi, psish, p) -- in place                     */
@@ -152,6 +152,11 @@ int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* keys
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);
+/* Fast RNS base conversion, one task per (polynomial, source basis):
+ * dst_t = sum_i [src_i * qhat_i^-1]_{q_i} * (qhat_i mod p_t) mod p_t
+ * (csrc/bconv.cu; the ModUp / ModDown of hybrid dnum-digit key switching,
+ * BASELINE config 1; the reference's per-prime digits need none).          */
+int hb_bconv(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Ciphertext tensor product d0, d1, d2 (engine.py:249-257).                  */
 int hb_tensor(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Key-switch inner product with the fused Galois gather

@@ -194,6 +194,39 @@ void or_sub_scaled_inv(u64* rowsv, const u64* corr, const u64* pinv, int rows, i
   }
 }
 
+/* Fast RNS base conversion (the standard hybrid key-switching ModUp /
+ * ModDown; no reference counterpart -- the reference uses per-prime digits):
+ * out[t][j] = sum_i [x_i[j] * qhat_inv[i]]_{q_i} * qhat_mod[i][t]  mod p_t,
+ * with the centred representative of every [.]_{q_i} (in (-q_i/2, q_i/2]):
+ * the converted integer is x + u Q, |u| <= s/2 (one source: the exact
+ * centred lift of the reference's per-prime ModUp / ModDown),
+ * source row i at src + i*src_stride, target row t at dst + dst_off[t].
+ * Plain 128-bit remainders (an independent reduction from the GPU's). */
+void or_bconv(const u64* src, int s, i64 src_stride, const i64* sprime, u64* dst, int t,
+              const i64* dst_off, const i64* tprime, int n, const u64* p, const u64* qhat_inv,
+              const u64* qhat_mod) {
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < n; ++j) {
+    u64 y[64];
+    int neg[64];
+    for (int i = 0; i < s; ++i) {
+      const u64 q = p[sprime[i]];
+      y[i] = (u64)(((u128)src[(size_t)i * src_stride + j] * qhat_inv[i]) % q);
+      neg[i] = y[i] > q / 2;            /* centred representative y - q */
+      if (neg[i]) y[i] = q - y[i];
+    }
+    for (int k = 0; k < t; ++k) {
+      const u64 pt = p[tprime[k]];
+      u64 acc = 0;
+      for (int i = 0; i < s; ++i) {
+        const u64 term = (u64)(((u128)y[i] * qhat_mod[(size_t)i * t + k]) % pt);
+        acc = neg[i] ? (acc + pt - term) % pt : (acc + term) % pt;
+      }
+      dst[dst_off[k] + j] = acc;
+    }
+  }
+}
+
 int or_num_threads(void) {
 #ifdef _OPENMP
   extern int omp_get_max_threads(void);

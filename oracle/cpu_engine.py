@@ -41,6 +41,7 @@ def lib():
         _LIB.or_lift_center.argtypes = [vp, i32, ctypes.c_uint64, vp]
         _LIB.or_reduce_rows.argtypes = [vp, i32, vp, i32, vp, vp]
         _LIB.or_sub_scaled_inv.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, vp]
+        _LIB.or_bconv.argtypes = [vp, i32, ctypes.c_int64, vp, vp, i32, vp, vp, i32, vp, vp, vp]
     return _LIB
 
 

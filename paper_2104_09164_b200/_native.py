@@ -55,6 +55,7 @@ def lib():
         L.hb_sum.argtypes = [vp, vp, i32, vp, vp]
         L.hb_ks_inner.argtypes = [vp, vp, i32, vp]
         L.hb_ks_inner2.argtypes = [vp, vp, i32, i32, vp]
+        L.hb_bconv.argtypes = [vp, vp, i32, vp]
         L.hb_mac_shared.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
         L.hb_crt_double.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
         L.hb_fft_create.restype = vp
@@ -116,6 +117,9 @@ TENSOR_TASK = np.dtype([("a0", "<u8"), ("a1", "<u8"), ("b0", "<u8"), ("b1", "<u8
                         ("d0", "<u8"), ("d1", "<u8"), ("d2", "<u8"),
                         ("prime", "<i4"), ("_pad", "<i4")])
 CRT_TASK = np.dtype([("rows", "<u8"), ("out", "<u8")])
+BCONV_TASK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("dst_off", "<u8"), ("tab", "<u8"),
+                       ("sprime", "<u8"), ("tprime", "<u8"), ("src_stride", "<i8"),
+                       ("s", "<i4"), ("t", "<i4")])
 
 # NTT fused modes (csrc/ntt.cu FwdMode)
 FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER, FWD_LIFT_KS = 0, 1, 2, 3, 4, 5
@@ -126,7 +130,8 @@ EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PER
 
 def _check_layouts():
     L = _lib
-    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, KS_TASK, KS_TASK2)):
+    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, KS_TASK, KS_TASK2,
+                               BCONV_TASK)):
         if L.hb_sizeof_task(kind) != dt.itemsize:
             raise NativeError(f"task layout {kind} mismatch: C {L.hb_sizeof_task(kind)} "
                               f"vs numpy {dt.itemsize}")

@@ -762,7 +762,9 @@ class CkksBackend(BackendBase):
                                  dst_prime=sprime, src_prime=sprime, scal=int(self.lift_once)))
         src_p = -1 if self.lift_once else self.S
         out = self.ring.empty(m, r)
-        if late and len(late) == nj and self.ring.two_pass:
+        if late and len(late) == nj and self.lift_once:
+            # (cluster NTT only: the two-pass kernels keep their intermediate
+            # in dst, which an in-place scatter would race with)
             # pre-permuted rotations: ModDown of the natural-order inner product
             # (ModDown commutes with the automorphism), c0 added at the source
             # index, result scattered through the inverse Galois map:

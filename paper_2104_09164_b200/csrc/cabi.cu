@@ -50,6 +50,8 @@ cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, 
                                int, cudaStream_t);
 cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_bconv(const void*, int, const HbPrime*, int, cudaStream_t);
+int bconv_task_size();
 cudaError_t launch_lift_center(const u64*, u64, long long*, int, cudaStream_t);
 cudaError_t launch_reduce_rows(const long long*, const int*, int, const HbPrime*, u64*, int,
                                cudaStream_t);
@@ -288,6 +290,7 @@ int hb_sizeof_task(int kind) {
     case 3: return (int)sizeof(HbMacTerm);
     case 4: return (int)sizeof(HbKsTask);
     case 5: return (int)sizeof(HbKsTask2);
+    case 6: return bconv_task_size();
     default: return -1;
   }
 }
@@ -398,6 +401,12 @@ int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream)
       ? launch_ks_inner2_f64(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream)
       : launch_ks_inner2(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_inner2") : 0;
+}
+
+// Fast RNS base conversion (bconv.cu): hybrid key switching ModUp / ModDown.
+int hb_bconv(hb_ring* r, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_bconv(tasks, count, r->dev.primes, r->dev.n, (cudaStream_t)stream);
+  return e ? fail(e, "hb_bconv") : 0;
 }
 
 int hb_crt_double(hb_ring* r, const void* tasks, int count, const unsigned long long* consts,

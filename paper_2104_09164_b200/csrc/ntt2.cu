@@ -89,7 +89,7 @@ k_ntt2_cols(const HbNttTask* __restrict__ tasks, HbRing R) {
   const typename Pol::Tw* tw = FWD ? Pol::fwd_table(R, tk.dst_prime) : Pol::inv_table(R, tk.dst_prime);
   const int c = threadIdx.x % CW, gq = threadIdx.x / CW;
   u64 ps = 0, ps_half = 0;
-  if (FWD && (MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER)) {
+  if (FWD && (MODE == FWD_LIFT || MODE == FWD_MODDOWN)) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
@@ -229,25 +229,9 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
       // ModDown epilogue operands are issued before the butterflies so their
       // HBM latency overlaps the fp64 work (profiled: these loads were the
       // block pass's top stall)
-      constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
+      constexpr bool MD = MODE == FWD_MODDOWN;
       ulonglong2 ax[4];
       u64 ad[8];
-      int2 sc[4];
-      if (MODE == FWD_MODDOWN_SCATTER) {
-        // pre-permuted rotation: addend and x_r in natural order (coalesced),
-        // result scattered to dst[perm[j]] (perm = inverse Galois map)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const size_t j = base + e0 + 2 * v;
-          ax[v] = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
-          sc[v] = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
-          if (tk.add) {
-            const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
-            ad[2 * v] = a2.x;
-            ad[2 * v + 1] = a2.y;
-          }
-        }
-      }
       if (MODE == FWD_MODDOWN) {
 #pragma unroll
         for (int v = 0; v < 4; ++v)
@@ -290,19 +274,12 @@ k_ntt2_blocks(const HbNttTask* __restrict__ tasks, HbRing R) {
             o.x = add_mod(o.x, ad[2 * v], p);
             o.y = add_mod(o.y, ad[2 * v + 1], p);
           }
-          if (tk.add2) {   // post-addend at the destination index
-            const size_t d0 = MODE == FWD_MODDOWN_SCATTER ? (size_t)sc[v].x : j;
-            const size_t d1 = MODE == FWD_MODDOWN_SCATTER ? (size_t)sc[v].y : j + 1;
-            o.x = add_mod(o.x, __ldg(tk.add2 + d0), p);
-            o.y = add_mod(o.y, __ldg(tk.add2 + d1), p);
+          if (tk.add2) {   // post-addend (the rotate-and-sum add)
+            o.x = add_mod(o.x, __ldg(tk.add2 + j), p);
+            o.y = add_mod(o.y, __ldg(tk.add2 + j + 1), p);
           }
         }
-        if (MODE == FWD_MODDOWN_SCATTER) {
-          tk.dst[sc[v].x] = o.x;
-          tk.dst[sc[v].y] = o.y;
-        } else {
-          *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
-        }
+        *reinterpret_cast<ulonglong2*>(tk.dst + j) = o;
       }
     }
   } else {
@@ -390,7 +367,11 @@ static cudaError_t fwd2_mode(const HbNttTask* tasks, int count, const HbRing& R,
     case FWD_LIFT: return fwd2_t<LOGN, F64, FWD_LIFT>(tasks, count, R, st);
     case FWD_MODDOWN: return fwd2_t<LOGN, F64, FWD_MODDOWN>(tasks, count, R, st);
     case FWD_I64: return fwd2_t<LOGN, F64, FWD_I64>(tasks, count, R, st);
-    case FWD_MODDOWN_SCATTER: return fwd2_t<LOGN, F64, FWD_MODDOWN_SCATTER>(tasks, count, R, st);
+    // the two-pass intermediate lives in dst, so a scatter through the
+    // inverse Galois map would overwrite tiles other CTAs have not read yet:
+    // scatter ModDowns run on the cluster NTT only (the engine gathers after
+    // a plain ModDown on the two-pass rings)
+    case FWD_MODDOWN_SCATTER: return cudaErrorNotSupported;
     default: return cudaErrorInvalidValue;
   }
 }

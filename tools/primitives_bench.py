@@ -1,15 +1,20 @@
 """CKKS primitive microbench (BASELINE config 1): N = 2^16, 24 x 50-bit chain
-primes + one 60-bit special prime; a batch of ciphertexts with residues
-uniform mod q_i from a seed runs through NTT/INTT, HMult + relinearise,
-HRotate by random steps and rescale on the GPU engine.
+primes + one 60-bit special prime, dnum = 3; a batch of ciphertexts with
+residues uniform mod q_i from a seed runs through NTT/INTT, HMult +
+relinearise, HRotate by random steps (single and hoisted) and rescale on the
+GPU engine.
 
-Key switching uses the reference's design (one special prime, per-prime
-digits: dnum = L + 1 = 24); BASELINE's "dnum = 3" hybrid key switching is not
-part of the reference and is not implemented (DESIGN.md §0 (f)).  The 50/60-bit
-primes exceed the fp64 path's 2^42 bound, so this ring runs the 64-bit Shoup
-integer transforms.
+Key switching: `--dnum 3` (default) is the hybrid key switch of
+ckks/hybrid.py (8-prime digits, fast base conversion ModUp/ModDown,
+csrc/bconv.cu); `--dnum 24` the reference design (per-prime digits, the
+engine's own path).  `--specials K` uses K special primes of `--special-bits`.
+The 50/60-bit primes exceed the fp64 path's 2^42 bound, so this ring runs the
+64-bit integer-pipe transforms.  `noise_ok` reports whether the
+configuration's key-switch noise leaves the result decryptable (one 60-bit
+special prime against 400-bit digits does not: BASELINE's config 1 is a
+throughput configuration).
 
-    python tools/primitives_bench.py [--cts 1024] [--batch 16]
+    python tools/primitives_bench.py [--cts 1024] [--batch 16] [--dnum 3] [--specials 1]
 """
 
 from __future__ import annotations
@@ -36,13 +41,32 @@ def main():
     ap.add_argument("--cts", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--logn", type=int, default=16)
+    ap.add_argument("--dnum", type=int, default=3)
+    ap.add_argument("--specials", type=int, default=1)
+    ap.add_argument("--special-bits", type=int, default=60)
     args = ap.parse_args()
-    ps = gen_params_custom(1 << args.logn, [50] * 24, 60, 40, name="microbench-2^16")
+    from paper_2104_09164_b200.ckks.params import _search
+    ps = gen_params_custom(1 << args.logn, [50] * 24, args.special_bits, 40,
+                           name="microbench-2^16")
     be = CkksBackend(ps, seed=0)
     lvl, n = ps.max_level, ps.n
     rng = np.random.default_rng(1)
     steps = sorted({int(s) for s in rng.integers(1, ps.n2, 8)})
-    be.ensure_rotation_keys({s: lvl for s in steps})
+    hybrid = not (args.dnum == lvl + 1 and args.specials == 1)
+    if hybrid:
+        from paper_2104_09164_b200.ckks.hybrid import HybridKeySwitch
+        sp = [ps.special_prime] + _search(args.special_bits, 2 * n, args.specials - 1,
+                                          set(ps.chain_primes) | {ps.special_prime})
+        hk = HybridKeySwitch(be, args.dnum, sp[:args.specials], seed=1)
+        hk.ensure_rotation_keys(steps)
+        mult = hk.mult
+        rot1 = lambda b: hk.rot(b, steps[0])       # noqa: E731
+        rotm = lambda b: hk.rot_many(b, steps)     # noqa: E731
+    else:
+        be.ensure_rotation_keys({s: lvl for s in steps})
+        mult = be._raw_mult
+        rot1 = lambda b: be._raw_rot_each([(b, steps[0])])   # noqa: E731
+        rotm = lambda b: be._raw_rot_many(b, steps)          # noqa: E731
     bsz = args.batch
     nb = max(1, args.cts // bsz)
 
@@ -53,9 +77,12 @@ def main():
         return Ct(CtData(t), lvl, Fraction(ps.msg_scale), be.n2)
 
     batches = [rand_batch() for _ in range(nb)]
-    res = {"config": {"workload": "CKKS primitive microbench", "N": n, "chain_primes": "24 x 50-bit",
-                      "special_prime": "1 x 60-bit", "dnum": lvl + 1, "ciphertexts": nb * bsz,
-                      "batch_per_launch": bsz, "rotation_steps": steps}}
+    res = {"config": {"workload": "CKKS primitive microbench (BASELINE config 1)", "N": n,
+                      "chain_primes": "24 x 50-bit",
+                      "special_primes": f"{args.specials} x {args.special_bits}-bit",
+                      "dnum": args.dnum if hybrid else lvl + 1,
+                      "key_switch": "hybrid (ckks/hybrid.py)" if hybrid else "reference design",
+                      "ciphertexts": nb * bsz, "batch_per_launch": bsz, "rotation_steps": steps}}
 
     def timed(fn, ops):
         fn(batches[0])
@@ -79,10 +106,17 @@ def main():
         be.ring.ntt_inv(t)
 
     res["ntt_plus_intt_rows_per_s"] = timed(ntt, rows)
-    res["hmult_relin_per_s"] = timed(lambda b: be._raw_mult(b, b), bsz)
-    res["hrotate_per_s"] = timed(lambda b: be._raw_rot_each([(b, steps[0])]), bsz)
-    res["hrotate_hoisted8_per_s"] = timed(lambda b: be._raw_rot_many(b, steps), bsz * len(steps))
+    res["hmult_relin_per_s"] = timed(lambda b: mult(b, b), bsz)
+    res["hrotate_per_s"] = timed(rot1, bsz)
+    res["hrotate_hoisted8_per_s"] = timed(rotm, bsz * len(steps))
     res["rescale_per_s"] = timed(lambda b: be._raw_rescale(b), bsz)
+    # decryptability of this key-switch configuration: mult + rescale of a
+    # fresh encryption against the slot product
+    v = np.random.default_rng(2).uniform(-1, 1, ps.n2)
+    ct = be.enc(v)
+    err = float(np.abs(be.dec(be.rescale(mult(ct, ct))) - v * v).max())
+    res["mult_decrypt_max_err"] = err
+    res["noise_ok"] = bool(err < 1e-3)
     res["unit"] = "ciphertext ops/s (one op = one ciphertext)"
     print(json.dumps(res), flush=True)
 
