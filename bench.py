@@ -597,9 +597,9 @@ def gpu_arm(args):
     if rank == 0:
         per_gpu = bsz * len(chunks)
         total = per_gpu * ws
-        wl = (f"BASELINE config 2: 4096 clips per step sharded over {ws} GPU(s), "
-              f"{len(chunks)} handles of {bsz} clips per GPU" if args.workload == "config2"
-              else f"{bsz} clips per GPU per step")
+        per_step = (f"BASELINE config 2: 4096 clips per step sharded over {ws} GPU(s), "
+                    f"{len(chunks)} handles of {bsz} clips per GPU" if args.workload == "config2"
+                    else f"{bsz} clips per GPU per step")
         line = {
             "metric": metric_name(), "value": total / (ms / 1e3), "unit": "inferences/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -609,7 +609,8 @@ def gpu_arm(args):
             "data": "synthetic",
             "config": {"workload": f"{wl.name}, "
                        f"{params.name} params (N=2^{params.n.bit_length() - 1}, L={params.max_level}),"
-                       f" {wl}", "net": args.net, "mode": args.mode,
+                       f" {per_step}", "net": args.net if not wl.tcn else args.workload,
+                       "mode": args.mode,
                        "strategy": args.strategy, "params": params.name, "clips_per_gpu": per_gpu,
                        "clips_per_replay": bsz,
                        "global_clips_per_step": total, "parallelism": f"clip-sharded dp{ws}",

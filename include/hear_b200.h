@@ -42,7 +42,7 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
                         const unsigned long long* psi, const unsigned long long* ipsi);
 void hb_ring_destroy(hb_ring* ring);
 int hb_ring_prime_consts(const hb_ring* ring, int prime_index, unsigned long long* out8);
-int hb_sizeof_task(int kind); /* 0 ntt, 1 ew, 2 mac, 3 mac-term, 4 ks, 5 ks2, 6 bconv */
+int hb_sizeof_task(int kind); /* 0 ntt, 1 ew, 2 mac/sum, 3 mac-term, 5 ks2, 6 bconv */
 
 /* ---- reference-shaped host-buffer kernels (hear/ckks/ring.py) ------------ */
 /* ring.py:113 ntt_fwd(a, gidx, psi, psish, p) -- in place                     */
@@ -117,9 +117,6 @@ int hb_set_pdl(int on);
  * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,
  * 8 (a-b)*c (ring.py:210).                                                   */
 int hb_ew(hb_ring* ring, int op, const void* tasks, int count, void* stream);
-/* Plaintext multiply-accumulate rows: sum_t pt_t * ct_t (the mult_plain/add
- * chains of hear/convolution.py:276-312, fastpath.py:168-180).               */
-int hb_mac(hb_ring* ring, const void* tasks, int count, const void* terms, void* stream);
 /* Many-term sums dst = sum_k srcs[term_off + k] (mod p) over HbMacTask rows
  * (the add chains of sum_each: hear/fastpath.py rotate-and-sum and FC
  * partial sums, ring.py:159 pw_add), srcs a device array of row pointers;
@@ -141,14 +138,11 @@ int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* d
  * with K = keys[..] + r*N for r < rows-1 and K = keys_last[..] (the key's
  * special row) and the special prime prime_last for r = rows-1.  de is
  * [ndig] row-block base pointers shared by every job, or [nout/2][ndig]
- * (each job its own digits) when de_per_job.  last_term_bstride != 0: the
- * last term has its own clip stride (a rotation's c0 against rows of P mod
- * q_r, folding the ModDown addend into the inner product).  Pointer tables
- * live in device memory.  fp64 rings only.                                  */
+ * (each job its own digits) when de_per_job.  Pointer tables live in device
+ * memory.  fp64 rings only.                                                  */
 int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* keys_last,
                const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
-               long long dst_bstride, int prime_last, int de_per_job,
-               long long last_term_bstride, void* stream);
+               long long dst_bstride, int prime_last, int de_per_job, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);
@@ -159,9 +153,6 @@ int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stre
 int hb_bconv(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Ciphertext tensor product d0, d1, d2 (engine.py:249-257).                  */
 int hb_tensor(hb_ring* ring, const void* tasks, int count, void* stream);
-/* Key-switch inner product with the fused Galois gather
- * (ring.py:136-156 pw_mul_accum_perm).                                       */
-int hb_ks_inner(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Exact CRT of `keep` coefficient rows to centred doubles (engine.py:156-175). */
 int hb_crt_double(hb_ring* ring, const void* tasks, int count, const unsigned long long* consts,
                   const int* prime_idx, int keep, int nl, void* stream);

@@ -47,13 +47,11 @@ def lib():
         L.hb_ntt_fused_ks.argtypes = [vp]
         L.hb_set_pdl.argtypes = [i32]
         L.hb_ks_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_longlong,
-                                 ctypes.c_longlong, i32, i32, ctypes.c_longlong, vp]
+                                 ctypes.c_longlong, i32, i32, vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
-        L.hb_mac.argtypes = [vp, vp, i32, vp, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
         L.hb_sum.argtypes = [vp, vp, i32, vp, vp]
-        L.hb_ks_inner.argtypes = [vp, vp, i32, vp]
         L.hb_ks_inner2.argtypes = [vp, vp, i32, i32, vp]
         L.hb_bconv.argtypes = [vp, vp, i32, vp]
         L.hb_mac_shared.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
@@ -106,9 +104,6 @@ MAC_TASK = np.dtype([("dst", "<u8"), ("prime", "<i4"), ("nterms", "<i4"),
                      ("term_off", "<i4"), ("_pad", "<i4")])
 MAC_TERM = np.dtype([("pt", "<u8"), ("ct", "<u8")])
 MAC_OUT = np.dtype([("dst", "<u8"), ("nterms", "<i4"), ("term_off", "<i4")])
-KS_TASK = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
-                    ("out_a", "<u8"), ("perm", "<u8"), ("de_stride", "<i8"),
-                    ("key_stride", "<i8"), ("ndig", "<i4"), ("prime", "<i4")])
 KS_TASK2 = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
                      ("out_a", "<u8"), ("perm", "<u8"), ("de_bstride", "<i8"),
                      ("de_dstride", "<i8"), ("key_stride", "<i8"), ("out_bstride", "<i8"),
@@ -122,7 +117,7 @@ BCONV_TASK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("dst_off", "<u8"), ("tab
                        ("s", "<i4"), ("t", "<i4")])
 
 # NTT fused modes (csrc/ntt.cu FwdMode)
-FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER, FWD_LIFT_KS = 0, 1, 2, 3, 4, 5
+FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER = 0, 1, 2, 3, 4
 # element-wise ops (csrc/ops.cu EwOp)
 EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PERM, \
     EW_SUB_SCALED, EW_PERM_ADD = range(10)
@@ -130,9 +125,9 @@ EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PER
 
 def _check_layouts():
     L = _lib
-    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, KS_TASK, KS_TASK2,
+    for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, None, KS_TASK2,
                                BCONV_TASK)):
-        if L.hb_sizeof_task(kind) != dt.itemsize:
+        if dt is not None and L.hb_sizeof_task(kind) != dt.itemsize:
             raise NativeError(f"task layout {kind} mismatch: C {L.hb_sizeof_task(kind)} "
                               f"vs numpy {dt.itemsize}")
 

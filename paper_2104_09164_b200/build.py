@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libhear_b200.so")
-SOURCES = ["ntt.cu", "ntt2.cu", "ntt3.cu", "ops.cu", "mac.cu", "dot.cu", "fft.cu", "bconv.cu",
+SOURCES = ["ntt.cu", "ntt2.cu", "ntt3.cu", "ops.cu", "mac.cu", "fft.cu", "bconv.cu",
            "cabi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

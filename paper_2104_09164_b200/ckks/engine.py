@@ -81,16 +81,6 @@ class _Ksk:
         self.ap = None
 
 
-class _Digits:
-    """Lazy ModUp: the INTT'd digit rows (coefficient form) and the input
-    rows, for the fused ModUp + inner product (ntt3 mode FWD_LIFT_KS) that
-    never materialises the [B, l+1, l+2, N] digit expansion."""
-
-    def __init__(self, coef: torch.Tensor, ptrs: np.ndarray):
-        self.coef, self.ptrs = coef, ptrs
-        self.shape = (coef.shape[0],)
-
-
 class KeyMaterial:
     def __init__(self):
         self.s_coeffs = None
@@ -168,10 +158,6 @@ class CkksBackend(BackendBase):
         # product (ks_gemm); smaller ones the per-job kernel (ks_inner2), which
         # has the lower latency at one or two clips
         self.ks_gemm_min = int(os.environ.get("HEAR_B200_KS_GEMM_MIN", "8"))
-        # opt-in (HEAR_B200_FOLD_C0=1): rotations through the GEMM fold their c0
-        # into the inner product (P c0 as one more term) instead of the ModDown
-        # epilogue's addend load; bit-exact, measured 0.4 % slower
-        self.fold_c0 = os.environ.get("HEAR_B200_FOLD_C0", "0") == "1"
         # hoisted rotations of several handles share one ModUp / ModDown launch
         # when each handle carries at most `batch_hoist_max` clips: at one clip
         # per handle the merged launches fill the GPU (B=1 latency 4.77 -> 4.15
@@ -179,12 +165,6 @@ class CkksBackend(BackendBase):
         # HEAR_B200_BATCH_HOIST=1 / 0 forces it on / off for every batch size.
         self.batch_hoist_max = {"1": 1 << 30, "0": 0}.get(
             os.environ.get("HEAR_B200_BATCH_HOIST", ""), 16)
-        # opt-in (HEAR_B200_KS_FUSED=1): single-job key switches (relinearisation,
-        # rot_each) with the ModUp fused into the inner product in the cluster
-        # NTT (64-bit atomic accumulation, no digit expansion through HBM);
-        # bit-exact, measured 7 % slower on the bench step than ModUp + GEMM
-        self.ks_fused = (os.environ.get("HEAR_B200_KS_FUSED", "0") == "1"
-                         and bool(nat.lib().hb_ntt_fused_ks(self.ring.handle)))
         # cluster NTT: inverse transforms whose rows feed ModUp / ModDown /
         # rescale write centred lifts as doubles (task scal = 1) and the
         # forward transforms read them with src_prime = -1: one lift per row
@@ -576,7 +556,7 @@ class CkksBackend(BackendBase):
                    d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
                    prime=self._row_primes(bsz, r))
         self.ring.tensor(t)
-        de = self._decompose(dr[:, 2], lvl, lazy=self.ks_fused and bsz >= self.ks_gemm_min)
+        de = self._decompose(dr[:, 2], lvl)
         out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
@@ -600,7 +580,7 @@ class CkksBackend(BackendBase):
 
     # ------------------------------------------------------------------ key switching
 
-    def _decompose(self, d, lvl: int, lazy: bool = False):
+    def _decompose(self, d, lvl: int):
         """Digits of d extended to chain rows 0..lvl plus the special prime:
         de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303).
 
@@ -618,20 +598,7 @@ class CkksBackend(BackendBase):
             ptrs = np.asarray(d, dtype=np.uint64)
         bsz = ptrs.shape[0]
         ndig, rows = lvl + 1, lvl + 2
-        rp = self.ring.row_ptrs
         coef = self.ring.empty(bsz, ndig)
-        prim = self._row_primes(bsz, ndig)
-        if lazy:   # the caller's key switch runs the fused ModUp + inner product
-            self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                     dst_prime=prim, src_prime=prim,
-                                     scal=int(self.lift_once)))
-            return _Digits(coef, ptrs)
-        return self._lift_digits(coef, ptrs, lvl, inverse_done=False)
-
-    def _lift_digits(self, coef, ptrs, lvl: int, inverse_done: bool = True) -> torch.Tensor:
-        """The [B, l+1, l+2, N] digit expansion from INTT'd digits (ModUp)."""
-        bsz = ptrs.shape[0]
-        ndig, rows = lvl + 1, lvl + 2
         rp = self.ring.row_ptrs
         prim = self._row_primes(bsz, ndig)
         de = self.ring.empty(bsz, ndig, rows)
@@ -642,14 +609,11 @@ class CkksBackend(BackendBase):
         dp = np.tile(gidx, bsz * ndig)
         ident = sp == np.tile(np.tile(np.arange(rows), ndig), bsz)
         lift = ~ident
-        if inverse_done:
-            self._ew(nat.EW_COPY, dst[ident], ptrs.ravel(), primes=prim)
-        else:
-            # the inverse transform also copies each input row to its identity
-            # digit position of de (add2), so no separate copy launch
-            self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
-                                     dst_prime=prim, src_prime=prim, add2=dst[ident],
-                                     scal=int(self.lift_once)))
+        # the inverse transform also copies each input row to its identity
+        # digit position of de (add2), so no separate copy launch
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                 dst_prime=prim, src_prime=prim, add2=dst[ident],
+                                 scal=int(self.lift_once)))
         self.ring.ntt_fwd(_tasks(nat.NTT_TASK, int(lift.sum()), src=src[lift], dst=dst[lift],
                                  src_prime=-1 if self.lift_once else sp[lift],
                                  dst_prime=dp[lift]), nat.FWD_LIFT)
@@ -667,17 +631,9 @@ class CkksBackend(BackendBase):
         ndig, rows = lvl + 1, lvl + 2
         nj = len(jobs)
         rp = self.ring.row_ptrs
-        fused = False
-        if isinstance(de, _Digits):
-            offs0 = [job[4] if len(job) > 4 else 0 for job in jobs]
-            fused = (self.ks_fused and len(set(offs0)) == nj
-                     and all(job[1] is None or (job[0].bp is not None and self.preperm)
-                             for job in jobs))
-            if not fused:   # shared digit sets or gathered digits: materialise
-                de = self._lift_digits(de.coef, de.ptrs, lvl)
         ip = self.ring.empty(nj * bsz * 2, rows)
         ipr = rp(ip).reshape(nj, bsz, 2, rows)
-        der = None if fused else rp(de).reshape(de.shape[0], ndig, rows)
+        der = rp(de).reshape(de.shape[0], ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         parts = []
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
@@ -694,7 +650,7 @@ class CkksBackend(BackendBase):
             kb_t, ka_t = (key.bp, key.ap) if prepermuted else (key.b, key.a)
             kbr = rp(kb_t).reshape(kb_t.shape[0], key.lmax + 2)[0, krow]
             kar = rp(ka_t).reshape(ka_t.shape[0], key.lmax + 2)[0, krow]
-            parts.append(None if fused else _tasks(
+            parts.append(_tasks(
                 nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
                 out_a=ipr[j, 0, 1],
                 perm=perm.data_ptr() if perm is not None and not prepermuted else 0,
@@ -710,9 +666,7 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        if fused:
-            self._ks_fused(de, lvl, jobs, [natural[j] for j in range(nj)], ip, ipr, bsz)
-        elif natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
+        if natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
             # every natural-order inner product in ONE GEMM launch: a hoisted
             # group shares its digit set, rot_each / relinearisation jobs bring
             # their own (one output pair per tile)
@@ -735,13 +689,7 @@ class CkksBackend(BackendBase):
                 # contiguous, so it is one (b, a) GEMM over all their clips
                 self._ks_gemm(der, lvl, keys[:1], ipr[js[:1]], bsz * len(js), offs[:1])
             else:
-                # rotations on pre-permuted keys: fold c0 into the inner
-                # product as one more GEMM term (P c0 on the b rows), so the
-                # ModDown epilogue loads no addend
-                c0s = self._foldable_c0(late, js, bsz) if self.fold_c0 else None
-                self._ks_gemm(der, lvl, keys, ipr[js], bsz, offs, c0s)
-                if c0s is not None:
-                    late = [(j, perm, None) for j, perm, _ in late]
+                self._ks_gemm(der, lvl, keys, ipr[js], bsz, offs)
             rest = [parts[j] for j in range(nj) if j not in natural]
             if rest:
                 self.ring.ks_inner2(np.concatenate(rest), bsz)
@@ -833,87 +781,7 @@ class CkksBackend(BackendBase):
                                  primes=np.tile(np.arange(r), bsz * 2))
         return res
 
-    def _ks_fused(self, dg: _Digits, lvl: int, jobs, keys, ip, ipr, bsz: int):
-        """Inner products of single-job key switches with the ModUp fused in
-        (ntt3 FWD_LIFT_KS): every (digit i, target row t != i) transform is
-        multiplied by the job's two key rows in the NTT epilogue and added to
-        the inner product rows with 64-bit atomics; the identity digit rows
-        contribute x_t * k[t][t] directly; one reduction canonicalises.
-        Same canonical inner product as the GEMM over the materialised digits
-        (modular arithmetic), without the 13x digit expansion through HBM."""
-        ndig, rows, n8 = lvl + 1, lvl + 2, np.uint64(8 * self.n)
-        nj = len(jobs)
-        rp = self.ring.row_ptrs
-        ip.zero_()
-        coefr = rp(dg.coef).reshape(dg.coef.shape[0], ndig)
-        offs = np.array([job[4] if len(job) > 4 else 0 for job in jobs])
-        gidx = np.array(list(range(lvl + 1)) + [self.S])
-        # key row pointers: kp[j, c, i, t] for digit i, target row t (krow)
-        kp = np.zeros((nj, 2, ndig, rows), dtype=np.uint64)
-        for j, (kb, ka, lmax) in enumerate(keys):
-            krow = np.array(list(range(lvl + 1)) + [lmax + 1], dtype=np.uint64)
-            for c, t in enumerate((kb, ka)):
-                kp[j, c] = (np.uint64(t.data_ptr())
-                            + (np.arange(ndig, dtype=np.uint64)[:, None] * np.uint64(lmax + 2)
-                               + krow[None, :]) * n8)
-        # identity digits: ip_c[j, b, i] = x[off_j + b, i] * k_c[i][i]
-        xs = np.stack([dg.ptrs[o:o + bsz] for o in offs])             # [nj, bsz, ndig]
-        diag = kp[:, :, np.arange(ndig), np.arange(ndig)]             # [nj, 2, ndig]
-        dst = ipr[:, :, :, :ndig]                                     # [nj, bsz, 2, ndig]
-        a = np.broadcast_to(xs[:, :, None, :], dst.shape)
-        b = np.broadcast_to(diag[:, None, :, :], dst.shape)
-        self._ew(nat.EW_MUL, dst.ravel(), np.ascontiguousarray(a).ravel(),
-                 np.ascontiguousarray(b).ravel(), primes=np.tile(np.arange(ndig), nj * bsz * 2))
-        # fused ModUp x key rows: tasks (j, b, i, t != i), target rows fastest
-        # (consecutive clusters share the source digit row, not the accumulator)
-        jj, bb, ii, tt = np.meshgrid(np.arange(nj), np.arange(bsz), np.arange(ndig),
-                                     np.arange(rows), indexing="ij")
-        keep = (ii != tt).ravel()
-        jj, bb, tt, ii = jj.ravel()[keep], bb.ravel()[keep], tt.ravel()[keep], ii.ravel()[keep]
-        t = _tasks(nat.NTT_TASK, len(jj), src=coefr[offs[jj] + bb, ii],
-                   src_prime=-1 if self.lift_once else ii,
-                   dst_prime=gidx[tt], dst=ipr[jj, bb, 0, tt], add2=ipr[jj, bb, 1, tt],
-                   aux=kp[jj, 0, ii, tt], add=kp[jj, 1, ii, tt])
-        self.ring.ntt_fwd(t, nat.FWD_LIFT_KS)
-        # canonicalise the accumulated sums (< ndig * p < 2^64): Shoup by 1
-        m = nj * bsz * 2
-        pr = np.tile(gidx, m)
-        one_sh = np.array([(1 << 64) // p for p in self.ring.primes], dtype=np.uint64)
-        self._ew(nat.EW_MUL_SCALAR, rp(ip), rp(ip), primes=pr,
-                 scal=np.ones(m * rows, dtype=np.uint64), scal_sh=one_sh[pr])
-
-    def _foldable_c0(self, late, js, bsz: int):
-        """Per GEMM job, (row-0 pointer, clip stride in elements) of the c0 to
-        fold into its inner product, or None when some job cannot fold (not a
-        pre-permuted rotation, no c0, or clips not uniformly strided)."""
-        c0 = {j: c for j, _, c in late}
-        out = []
-        for j in js:
-            c = c0.get(j)
-            if c is None:
-                return None
-            c = np.asarray(c, dtype=np.uint64).reshape(bsz, -1)
-            if bsz > 1:
-                d = np.diff(c[:, 0].astype(np.int64))
-                if not np.all(d == d[0]) or d[0] % 8:
-                    return None
-                stride = int(d[0]) // 8
-            else:
-                stride = 0
-            out.append((int(c[0, 0]), stride))
-        strides = {st for _, st in out}
-        return out if len(strides) == 1 else None
-
-    def _fold_rows(self):
-        """[L+2, N] rows of P mod q_r (special row 0) and an all-zero block."""
-        if getattr(self, "_pmod_rows", None) is None:
-            rows = np.zeros((self.L + 2, self.n), dtype=np.uint64)
-            rows[:self.L + 1] = self._pmod[:, None]
-            self._pmod_rows = self._dev(rows)
-            self._zero_rows = self.ring.zeros(self.L + 2)
-        return self._pmod_rows, self._zero_rows
-
-    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs, c0s=None):
+    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
         """Natural-order key-switch inner products of several jobs as one
         per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): terms = digits,
         outputs = (job, component), the special row (its own prime and key
@@ -936,22 +804,8 @@ class CkksBackend(BackendBase):
             dep = der[offs[0], :, 0]                    # [ndig] row 0 of each digit
         else:
             dep = np.stack([der[o, :, 0] for o in offs])   # [njobs, ndig]
-        last_bs = 0
-        if c0s is not None and (not shared or len({c for c, _ in c0s}) == 1):
-            # extra term: c0 x (P mod q_r) on b outputs, x 0 on a outputs
-            pm, zr = self._fold_rows()
-            pmp, zrp = np.uint64(pm.data_ptr()), np.uint64(zr.data_ptr())
-            kcol = np.array([pmp, zrp] * len(keys), dtype=np.uint64)[:, None]
-            kp = np.concatenate([kp, kcol], axis=1)
-            kps = np.concatenate([kps, np.full((len(kp), 1), zrp, dtype=np.uint64)], axis=1)
-            c0p = np.array([c for c, _ in c0s], dtype=np.uint64)
-            dep = (np.concatenate([dep, c0p[:1]]) if shared
-                   else np.concatenate([dep, c0p[:, None]], axis=1))
-            last_bs = c0s[0][1] if bsz > 1 else 1
-        elif c0s is not None:
-            raise ValueError("shared digit set with different c0 rows")
         self.ring.ks_gemm(dep, kp, kps, dp, rows, bsz, ndig * rows * self.n,
-                          2 * rows * self.n, self.S, last_bs)
+                          2 * rows * self.n, self.S)
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)
@@ -1123,7 +977,7 @@ class CkksBackend(BackendBase):
                 c1 = np.concatenate([
                     self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
                     for i in chunk])
-                de = self._decompose(c1, lvl, lazy=self.ks_fused and bsz >= self.ks_gemm_min)
+                de = self._decompose(c1, lvl)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1147,8 +1001,7 @@ class CkksBackend(BackendBase):
                 chunk = idx[c0:c0 + step]
                 rows = [self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)
                         for i in chunk]
-                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl,
-                                     lazy=self.ks_fused and bsz >= self.ks_gemm_min)
+                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1178,8 +1031,7 @@ class CkksBackend(BackendBase):
                     b0=xr[:, :, 0].ravel(), b1=xr[:, :, 1].ravel(), d0=dr[:, :, 0].ravel(),
                     d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
                     prime=self._row_primes(k * bsz, r)))
-                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl,
-                                     lazy=self.ks_fused and bsz >= self.ks_gemm_min)
+                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de

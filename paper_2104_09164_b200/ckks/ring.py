@@ -239,8 +239,7 @@ class RingContext:
     @property
     def two_pass(self) -> bool:
         """The default two-pass transform (csrc/ntt2.cu) is in use."""
-        return 12 <= self.logn <= 16 and not (os.environ.get("HEAR_B200_NTT1") == "1"
-                                              and self.logn <= 14)
+        return 12 <= self.logn <= 16
 
     def coeff_automorphism(self, coeffs: np.ndarray, g: int) -> np.ndarray:
         """X -> X^g on signed integer coefficients."""
@@ -262,8 +261,7 @@ class RingContext:
 
     _FWD_NAMES = {nat.FWD_PLAIN: "ntt_fwd", nat.FWD_LIFT: "ntt_fwd_modup_lift",
                   nat.FWD_MODDOWN: "ntt_fwd_moddown", nat.FWD_I64: "ntt_fwd_i64",
-                  nat.FWD_MODDOWN_SCATTER: "ntt_fwd_moddown_scatter",
-                  nat.FWD_LIFT_KS: "ntt_fwd_lift_ks"}
+                  nat.FWD_MODDOWN_SCATTER: "ntt_fwd_moddown_scatter"}
 
     def _ntt_account(self, fam: str, tasks: np.ndarray, kernels: int):
         row = 8 * self.n
@@ -322,12 +320,6 @@ class RingContext:
                     nbytes += _uniq(tasks["c"]) * 4 * self.n
                 _STATS.add("elementwise", nbytes,
                            len(tasks) * self.n * self._EW_MULS.get(op, 0) * StepStats.FP64_PER_MODMUL)
-
-    def mac(self, tasks: np.ndarray, terms: np.ndarray):
-        if len(tasks):
-            d, t = _upload(tasks, self.device), _upload(terms, self.device)
-            nat.check(self._lib.hb_mac(self.handle, _ptr(d), len(tasks), _ptr(t), self.stream),
-                      "mac")
 
     def mac_strided(self, outs: np.ndarray, terms: np.ndarray, rows: int, bc: int):
         if len(outs):
@@ -393,8 +385,7 @@ class RingContext:
         return bool(self._lib.hb_ring_uses_f64(self.handle))
 
     def ks_gemm(self, de: np.ndarray, keys: np.ndarray, keys_last: np.ndarray, dsts: np.ndarray,
-                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int,
-                last_term_bstride: int = 0):
+                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int):
         """Natural-order key-switch inner products as one per-coefficient GEMM
         (csrc/mac.cu launch_ks_gemm): de [ndig] shared or [njobs, ndig] per job,
         keys / keys_last [nout, ndig], dsts [nout]."""
@@ -410,7 +401,7 @@ class RingContext:
             e0 = _STATS.begin() if _STATS else None
             nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
                                            de_bstride, dst_bstride, prime_last, per_job,
-                                           last_term_bstride, self.stream), "ks_gemm")
+                                           self.stream), "ks_gemm")
             if _STATS:   # digit sets [bc, ndig, rows] once, key rows once, outputs
                 _STATS.end("keyswitch_gemm", e0)
                 nbytes = (_uniq(de) * bc * rows + _uniq(keys) * (rows - 1) + _uniq(keys_last)
@@ -423,12 +414,6 @@ class RingContext:
             d = _upload(tasks, self.device)
             nat.check(self._lib.hb_ks_inner2(self.handle, _ptr(d), len(tasks), nb, self.stream),
                       "ks_inner2")
-
-    def ks_inner(self, tasks: np.ndarray):
-        if len(tasks):
-            d = _upload(tasks, self.device)
-            nat.check(self._lib.hb_ks_inner(self.handle, _ptr(d), len(tasks), self.stream),
-                      "ks_inner")
 
     # ---- row-pointer helpers ---------------------------------------------------
 

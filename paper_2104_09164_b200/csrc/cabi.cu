@@ -28,14 +28,10 @@ cudaError_t launch_ntt_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 int ntt_kernels(const HbRing&, int);
 bool ntt3_supported(const HbRing& R);
 cudaError_t launch_ew(int, const HbEwTask*, int, const HbPrime*, int, cudaStream_t);
-cudaError_t launch_mac(const HbMacTask*, int, const HbMacTerm*, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_tensor(const void*, int, const HbPrime*, int, bool, cudaStream_t);
 cudaError_t launch_mac_strided(const void*, int, const HbMacTerm*, const HbPrime*, int, int, int,
                                bool, cudaStream_t);
-cudaError_t launch_ks_inner(const HbKsTask*, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_sum_rows(const HbMacTask*, int, const void*, const HbPrime*, int, cudaStream_t);
-cudaError_t launch_mac_shared(const void*, const void*, const void*, int, int, const HbPrime*, int,
-                              int, int, cudaStream_t);
 cudaError_t launch_mac_gemm(const void*, const void*, const void*, int, int, const HbPrime*, int,
                             int, int, cudaStream_t);
 cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int, const HbPrime*,
@@ -44,11 +40,8 @@ cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cud
 cudaError_t launch_mac_pipe(const void*, const void*, const void*, int, int, const HbRing&, int,
                             int, cudaStream_t);
 cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, int, int,
-                           const HbRing&, int, int, long long, long long, int, int, long long,
+                           const HbRing&, int, int, long long, long long, int, int,
                            cudaStream_t);
-cudaError_t launch_mac_gemm_c3(const void*, const void*, const void*, int, int, const HbRing&, int,
-                               int, cudaStream_t);
-cudaError_t launch_ks_inner_c3(const void*, int, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_bconv(const void*, int, const HbPrime*, int, cudaStream_t);
 int bconv_task_size();
@@ -77,8 +70,6 @@ struct hb_ring {
   double* tw1_inv_dev;
   HbTwD* tw3_fwd_dev = nullptr;
   HbTwD* tw3_inv_dev = nullptr;
-  double* chunk_dev = nullptr;
-  std::vector<double> chunk_host;
   std::vector<HbPrime> primes_host;
   int last_err;
 };
@@ -155,30 +146,6 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   for (int i = 0; i < nprimes; ++i) f64 = f64 && primes[i] < (1ull << 42);
   const char* force = getenv("HEAR_B200_INT_NTT");
   r->dev.use_f64 = (f64 && !(force && force[0] == '1')) ? 1 : 0;
-  // chunked dot products: B = max prime bits, three w-bit limbs (w = ceil(B/3)),
-  // F terms per exact fp64 accumulation with F * 2^(B+w) + 2^B <= 2^53
-  {
-    int B = 0;
-    for (int i = 0; i < nprimes; ++i) B = std::max(B, 64 - __builtin_clzll(primes[i]));
-    const int w = (B + 2) / 3;
-    const int room = 53 - B - w - 1;
-    // opt-in: measured no faster than fmod_mul products (the dot-product
-    // kernels are load-latency bound, profiles/r01_*), kept for experiments
-    const char* on = getenv("HEAR_B200_CHUNK");
-    r->dev.chunk_w = w;
-    r->dev.chunk_fold = (r->dev.use_f64 && room >= 1 && (on && on[0] == '1'))
-                            ? (1 << std::min(room, 8)) : 0;
-    r->chunk_host.resize((size_t)nprimes * 4);
-    for (int i = 0; i < nprimes; ++i) {
-      const unsigned long long p = primes[i];
-      const unsigned long long s1 = (unsigned long long)(((unsigned __int128)1 << w) % p);
-      const unsigned long long s2 = (unsigned long long)(((unsigned __int128)s1 * s1) % p);
-      r->chunk_host[4 * i + 0] = (double)s1;
-      r->chunk_host[4 * i + 1] = (double)s1 / (double)p;
-      r->chunk_host[4 * i + 2] = (double)s2;
-      r->chunk_host[4 * i + 3] = (double)s2 / (double)p;
-    }
-  }
   std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
   std::vector<HbTwD> tfd((size_t)nprimes * n), tid((size_t)nprimes * n);
   std::vector<double> t1f((size_t)nprimes * n), t1i((size_t)nprimes * n);
@@ -250,13 +217,6 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   r->dev.tw1_inv = r->tw1_inv_dev;
   r->dev.tw3_fwd = r->tw3_fwd_dev;
   r->dev.tw3_inv = r->tw3_inv_dev;
-  if (cudaMalloc(&r->chunk_dev, sizeof(double) * r->chunk_host.size()) ||
-      cudaMemcpy(r->chunk_dev, r->chunk_host.data(), sizeof(double) * r->chunk_host.size(),
-                 cudaMemcpyHostToDevice)) {
-    snprintf(g_err, sizeof(g_err), "hb_ring_create: chunk constants upload failed");
-    return nullptr;
-  }
-  r->dev.chunk_consts = r->chunk_dev;
   return r;
 }
 
@@ -271,7 +231,6 @@ void hb_ring_destroy(hb_ring* r) {
   cudaFree(r->tw1_inv_dev);
   cudaFree(r->tw3_fwd_dev);
   cudaFree(r->tw3_inv_dev);
-  cudaFree(r->chunk_dev);
   delete r;
 }
 
@@ -288,7 +247,6 @@ int hb_sizeof_task(int kind) {
     case 1: return (int)sizeof(HbEwTask);
     case 2: return (int)sizeof(HbMacTask);
     case 3: return (int)sizeof(HbMacTerm);
-    case 4: return (int)sizeof(HbKsTask);
     case 5: return (int)sizeof(HbKsTask2);
     case 6: return bconv_task_size();
     default: return -1;
@@ -323,12 +281,6 @@ int hb_ew(hb_ring* r, int op, const void* tasks, int count, void* stream) {
   return e ? fail(e, "hb_ew") : 0;
 }
 
-int hb_mac(hb_ring* r, const void* tasks, int count, const void* terms, void* stream) {
-  cudaError_t e = launch_mac((const HbMacTask*)tasks, count, (const HbMacTerm*)terms,
-                             r->dev.primes, r->dev.n, (cudaStream_t)stream);
-  return e ? fail(e, "hb_mac") : 0;
-}
-
 int hb_mac_strided(hb_ring* r, const void* outs, int nout, const void* terms, int rows, int bc,
                    void* stream) {
   cudaError_t e = launch_mac_strided(outs, nout, (const HbMacTerm*)terms, r->dev.primes, r->dev.n,
@@ -348,35 +300,18 @@ int hb_tensor(hb_ring* r, const void* tasks, int count, void* stream) {
   return e ? fail(e, "hb_tensor") : 0;
 }
 
-int hb_ks_inner(hb_ring* r, const void* tasks, int count, void* stream) {
-  cudaError_t e = launch_ks_inner((const HbKsTask*)tasks, count, r->dev.primes, r->dev.n,
-                                  (cudaStream_t)stream);
-  return e ? fail(e, "hb_ks_inner") : 0;
-}
-
 int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts, int nterms,
                   int nout, int rows, int bc, void* stream) {
-  const char* old = getenv("HEAR_B200_MAC_SHARED");
-  const char* pipe = getenv("HEAR_B200_MAC_PIPE");   // "0": register-prefetch kernels
+  // fp64 rings: the cp.async-pipelined GEMM (mac.cu) at every batch size
+  // (measured: also the lower latency at one clip); it declines term tables
+  // larger than its shared memory, which take the register-tile GEMM
   cudaError_t e = cudaErrorNotSupported;
-  // the cp.async-pipelined GEMM at every batch size (measured: also the lower
-  // latency at one clip); HEAR_B200_MAC_PIPE_MIN raises the threshold
-  static int pipe_min = -1;
-  if (pipe_min < 0) {
-    const char* v = getenv("HEAR_B200_MAC_PIPE_MIN");
-    pipe_min = v ? atoi(v) : 1;
-  }
-  if (r->dev.use_f64 && bc >= pipe_min && !(pipe && pipe[0] == '0') && !(old && old[0] == '1')) {
+  if (r->dev.use_f64) {
     e = launch_mac_pipe(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream);
-    if (e == cudaErrorNotSupported) (void)cudaGetLastError();   // term table too large
+    if (e == cudaErrorNotSupported) (void)cudaGetLastError();
   }
   if (e == cudaErrorNotSupported)
-    e = (old && old[0] == '1')
-      ? launch_mac_shared(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
-                          (cudaStream_t)stream)
-      : r->dev.chunk_fold
-      ? launch_mac_gemm_c3(cts, pts, dsts, nterms, nout, r->dev, rows, bc, (cudaStream_t)stream)
-      : r->dev.use_f64
+    e = r->dev.use_f64
       ? launch_mac_gemm_f64(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
                             (cudaStream_t)stream)
       : launch_mac_gemm(cts, pts, dsts, nterms, nout, r->dev.primes, r->dev.n, rows, bc,
@@ -386,18 +321,15 @@ int hb_mac_shared(hb_ring* r, const void* cts, const void* pts, const void* dsts
 
 int hb_ks_gemm(hb_ring* r, const void* de, const void* keys, const void* keys_last,
                const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
-               long long dst_bstride, int prime_last, int de_per_job,
-               long long last_term_bstride, void* stream) {
+               long long dst_bstride, int prime_last, int de_per_job, void* stream) {
   cudaError_t e = launch_ks_gemm(de, keys, keys_last, dsts, ndig, nout, r->dev, rows, bc,
                                  de_bstride, dst_bstride, prime_last, de_per_job,
-                                 last_term_bstride, (cudaStream_t)stream);
+                                 (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_gemm") : 0;
 }
 
 int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {
-  cudaError_t e = r->dev.chunk_fold
-      ? launch_ks_inner_c3(tasks, count, nb, r->dev, (cudaStream_t)stream)
-      : r->dev.use_f64
+  cudaError_t e = r->dev.use_f64
       ? launch_ks_inner2_f64(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream)
       : launch_ks_inner2(tasks, count, nb, r->dev.primes, r->dev.n, (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_inner2") : 0;

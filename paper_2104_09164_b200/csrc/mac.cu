@@ -14,9 +14,8 @@
 // 16-byte cp.async copies, so S-1 terms are in flight while one is
 // multiplied (the register-prefetch kernel in ops.cu stalled 47 % of its
 // samples on the HBM latency of the ct loads, profiles/r01_*).  A warp owns
-// TO x TB outputs per lane; products on the fp64 pipe either as fmod_mul
-// (6 ops, balanced residue) or, when the ring enables chunked dot products,
-// as three exact DFMAs against w-bit limbs of ct (dot.cu).
+// TO x TB outputs per lane; products on the fp64 pipe as fmod_mul (5 ops,
+// balanced residue), summed in double, canonicalised once.
 #include <cstdint>
 #include <cstdlib>
 #include "ring.cuh"
@@ -42,8 +41,6 @@ struct HbMacGroupP {
   const u64* const* pts_last;   // ... except the last row when set: its pt rows
   int prime_last;               //     (pointers to the row itself) and prime
   int cts_per_tile;       // cts is [output tile][T] (each tile has its own terms)
-  long long ct_last_bstride;  // != 0: the last term's clip stride (a folded-in
-                              // c0 term of the key switch, see launch_ks_gemm)
 };
 
 namespace {
@@ -56,14 +53,6 @@ HB_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 HB_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-HB_DEV double limb_f(u64 x, int sh, u64 mask) { return u64_to_f((x >> sh) & mask); }
-
-HB_DEV u64 recombine3(double s0, double s1, double s2, const double* cc, double p, double pinv) {
-  const double r0 = fmod_reduce(s0, p, pinv);
-  const double r1 = fmod_mul(fmod_reduce(s1, p, pinv), cc[0], cc[1], p);
-  const double r2 = fmod_mul(fmod_reduce(s2, p, pinv), cc[2], cc[3], p);
-  return fmod_canon(r0 + r1 + r2, p, pinv);
-}
 
 // Operand conversion of the GEMM: the magic-number path (LOP + DADD on the
 // fp64 pipe) by default; -DHB_MAC_I2F moves it to the conversion pipe
@@ -77,7 +66,7 @@ HB_DEV double mac_to_f(u64 x) {
 #endif
 }
 
-template <int TO, int TB, int WO, int WB, bool C3, int S>
+template <int TO, int TB, int WO, int WB, int S>
 __global__ void __launch_bounds__(256)
 k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   HB_PDL_ENTRY();
@@ -119,9 +108,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
         const u64* src;
         if (row < CB) {
           const int b = bc + row < BC ? bc + row : BC - 1;
-          const long long bs = (g.ct_last_bstride && t == T - 1) ? g.ct_last_bstride
-                                                                 : g.ct_bstride;
-          src = ptab[t] + (size_t)b * bs + rj0 + part * 2;
+          src = ptab[t] + (size_t)b * g.ct_bstride + rj0 + part * 2;
         } else {
           src = ptab[T + (row - CB) * T + t] + prow + part * 2;
         }
@@ -139,17 +126,11 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   const int prime = last ? g.prime_last : g.prime_off + r;
   const HbPrime P = RG.primes[prime];
   const double p = P.pd, pinv = P.pinv;
-  const int wbits = RG.chunk_w, fold = RG.chunk_fold;
-  const u64 mask = (1ull << wbits) - 1;
-  constexpr int NA = C3 ? 3 : 1;
-  double acc[TO][TB][NA];
+  double acc[TO][TB];
 #pragma unroll
   for (int o = 0; o < TO; ++o)
 #pragma unroll
-    for (int b = 0; b < TB; ++b)
-#pragma unroll
-      for (int k = 0; k < NA; ++k) acc[o][b][k] = 0.0;
-  int since = 0;
+    for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
   for (int t = 0; t < T; ++t) {
     cp_wait<S - 2>();
     __syncthreads();                 // term t landed for every thread; stage t-1 is free
@@ -159,57 +140,25 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     double a[TO];
 #pragma unroll
     for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
-    if constexpr (C3) {
+    double c[TB];
 #pragma unroll
-      for (int b = 0; b < TB; ++b) {
-        const u64 v = st[(bs + b) * 32 + lane];
-        const double c0 = limb_f(v, 0, mask), c1 = limb_f(v, wbits, mask);
-        const double c2 = u64_to_f(v >> (2 * wbits));
+    for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
 #pragma unroll
-        for (int o = 0; o < TO; ++o) {
-          acc[o][b][0] = __fma_rn(a[o], c0, acc[o][b][0]);
-          acc[o][b][1] = __fma_rn(a[o], c1, acc[o][b][1]);
-          acc[o][b][2] = __fma_rn(a[o], c2, acc[o][b][2]);
-        }
-      }
-      if (++since == fold) {
-        since = 0;
+    for (int o = 0; o < TO; ++o) {
+      const double aq = a[o] * pinv;
 #pragma unroll
-        for (int o = 0; o < TO; ++o)
+      for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a[o], aq, p);
+    }
+    if ((t & 255) == 255) {   // |balanced residue| < p/2: 2^9 terms fit 2^53
 #pragma unroll
-          for (int b = 0; b < TB; ++b)
+      for (int o = 0; o < TO; ++o)
 #pragma unroll
-            for (int k = 0; k < 3; ++k) acc[o][b][k] = fmod_reduce(acc[o][b][k], p, pinv);
-      }
-    } else {
-      double c[TB];
-#pragma unroll
-      for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
-#pragma unroll
-      for (int o = 0; o < TO; ++o) {
-        const double aq = a[o] * pinv;
-#pragma unroll
-        for (int b = 0; b < TB; ++b) acc[o][b][0] += fmod_mul(c[b], a[o], aq, p);
-      }
-      if ((t & 255) == 255) {
-#pragma unroll
-        for (int o = 0; o < TO; ++o)
-#pragma unroll
-          for (int b = 0; b < TB; ++b) acc[o][b][0] = fmod_reduce(acc[o][b][0], p, pinv);
-      }
+        for (int b = 0; b < TB; ++b) acc[o][b] = fmod_reduce(acc[o][b], p, pinv);
     }
   }
   cp_wait<0>();
-  double cc[4] = {0, 0, 0, 0};
-  if constexpr (C3) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = __ldg(RG.chunk_consts + 4 * prime + k);
-  }
   const size_t rj = rj0 + lane;
-  auto value = [&](int o, int b) {
-    return C3 ? recombine3(acc[o][b][0], acc[o][b][1], acc[o][b][2], cc, p, pinv)
-              : fmod_canon(acc[o][b][0], p, pinv);
-  };
+  auto value = [&](int o, int b) { return fmod_canon(acc[o][b], p, pinv); };
   if (oc + OB <= O && bc + CB <= BC) {   // full tile (the common case): no bounds checks
 #pragma unroll
     for (int o = 0; o < TO; ++o) {
@@ -233,17 +182,17 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   }
 }
 
-template <int TO, int TB, int WO, int WB, bool C3, int S>
+template <int TO, int TB, int WO, int WB, int S>
 cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cudaStream_t st) {
   constexpr int OB = TO * WO, CB = TB * WB;
   const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + sizeof(void*) * (size_t)g.nterms * (1 + OB);
   if (smem > 220 * 1024) return cudaErrorNotSupported;   // caller falls back
   static int smem_cur = 0;
-  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, C3, S>, (int)((int)smem), &smem_cur);
+  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S>, (int)((int)smem), &smem_cur);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
   dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32));
-  (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, C3, S>, dim3(grid), dim3(block), smem, st, g, RG, R, BC);
+  (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S>, dim3(grid), dim3(block), smem, st, g, RG, R, BC);
   return cudaGetLastError();
 }
 
@@ -251,33 +200,21 @@ cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cu
 
 static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
                                      cudaStream_t st) {
-  if (RG.chunk_fold) {
-    if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, true, 4>(g, RG, rows, BC, st);
-    return mac_pipe_t<4, 2, 4, 2, true, 4>(g, RG, rows, BC, st);
-  }
-  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  constexpr int S = HB_MAC_STAGES;
+  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, S>(g, RG, rows, BC, st);
   // one (b, a) output pair per tile when every job brings its own digits
-  if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, S>(g, RG, rows, BC, st);
   // output tile sized to the layer so no warp idles on absent outputs
-  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
-  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
-  static int tile = -1;   // HEAR_B200_GEMM_TILE: experiment knob for the wide tiles
-  if (tile < 0) {
-    const char* v = getenv("HEAR_B200_GEMM_TILE");
-    tile = v ? atoi(v) : 0;
-  }
-  if (g.nout <= 8) {
-    if (tile == 44) return mac_pipe_t<4, 4, 2, 4, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
-    return mac_pipe_t<8, 4, 1, 8, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
-  }
-  if (tile == 48) return mac_pipe_t<4, 8, 4, 2, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
-  if (tile == 44) return mac_pipe_t<4, 4, 4, 2, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, S>(g, RG, rows, BC, st);
+  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, S>(g, RG, rows, BC, st);
+  if (g.nout <= 8) return mac_pipe_t<8, 4, 1, 8, S>(g, RG, rows, BC, st);
   // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
   // operand feeds twice the products of the 4x4 tile; measured +1.6 % on
-  // the bench step (hoisted key-switch GEMM and conv MAC).  Long term lists
-  // (conv layers) keep a deeper pipeline (HB_MAC_STAGES_LONG)
-  if (g.nterms > 32) return mac_pipe_t<8, 4, 2, 4, false, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
-  return mac_pipe_t<8, 4, 2, 4, false, HB_MAC_STAGES>(g, RG, rows, BC, st);
+  // the bench step (hoisted key-switch GEMM and conv MAC) over 4x4 and 4x8
+  // (round-1 tile sweep).  Long term lists (conv layers) may take a deeper
+  // pipeline (HB_MAC_STAGES_LONG)
+  if (g.nterms > 32) return mac_pipe_t<8, 4, 2, 4, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
+  return mac_pipe_t<8, 4, 2, 4, S>(g, RG, rows, BC, st);
 }
 
 // fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
@@ -296,7 +233,6 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
   g.pts_last = nullptr;
   g.prime_last = 0;
   g.cts_per_tile = 0;
-  g.ct_last_bstride = 0;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
@@ -307,14 +243,10 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
 // primes 0..rows-2 and the last row in prime_last with its own key rows
 // (keys_last).  de_per_job: de is [job][ndig] (each job its own digits,
 // one output pair per tile) instead of [ndig] shared by every job.
-// last_term_bstride != 0: the last of the ndig terms is not a digit but the
-// rotation's c0 (its own clip stride) against P mod q_r (b outputs) or zero
-// rows (a outputs): ModDown(x + P c0) = ModDown(x) + c0 exactly, so the
-// ModDown epilogue needs no addend load.
 cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_last,
                            const void* dsts, int ndig, int nout, const HbRing& RG, int rows,
                            int BC, long long de_bstride, long long dst_bstride, int prime_last,
-                           int de_per_job, long long last_term_bstride, cudaStream_t st) {
+                           int de_per_job, cudaStream_t st) {
   if (nout <= 0 || ndig <= 0) return cudaSuccess;
   if (!RG.use_f64) return cudaErrorNotSupported;
   HbMacGroupP g;
@@ -329,7 +261,6 @@ cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_la
   g.pts_last = reinterpret_cast<const u64* const*>(keys_last);
   g.prime_last = prime_last;
   g.cts_per_tile = de_per_job;
-  g.ct_last_bstride = last_term_bstride;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 

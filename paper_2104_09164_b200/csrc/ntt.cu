@@ -283,16 +283,10 @@ cudaError_t launch_ntt3_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 cudaError_t launch_ntt2_fwd(const HbNttTask*, int, const HbRing&, int, cudaStream_t);
 cudaError_t launch_ntt2_inv(const HbNttTask*, int, const HbRing&, cudaStream_t);
 
-// Default: the two-pass transform (ntt2.cu) for 2^12..2^16; this file's
-// one-row-per-CTA kernel for smaller rings or when HEAR_B200_NTT1=1.
-static bool use_two_pass(int logn) {
-  static int force1 = -1;
-  if (force1 < 0) {
-    const char* v = getenv("HEAR_B200_NTT1");
-    force1 = (v && v[0] == '1') ? 1 : 0;
-  }
-  return ntt2_supported(logn) && !(force1 && logn <= 14);
-}
+// The cluster NTT (ntt3.cu) for fp64 rings at 2^13 / 2^14, the two-pass
+// transform (ntt2.cu) for the other rings of 2^12..2^16; this file's
+// one-row-per-CTA kernel for rings below 2^12.
+static bool use_two_pass(int logn) { return ntt2_supported(logn); }
 
 int ntt2_chunk();
 
@@ -311,9 +305,6 @@ cudaError_t launch_ntt_fwd(const HbNttTask* tasks, int count, const HbRing& R, i
   switch (R.logn) {
     case 10: return launch_fwd_t<10>(tasks, count, R, mode, st);
     case 11: return launch_fwd_t<11>(tasks, count, R, mode, st);
-    case 12: return launch_fwd_t<12>(tasks, count, R, mode, st);
-    case 13: return launch_fwd_t<13>(tasks, count, R, mode, st);
-    case 14: return launch_fwd_t<14>(tasks, count, R, mode, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -325,9 +316,6 @@ cudaError_t launch_ntt_inv(const HbNttTask* tasks, int count, const HbRing& R, c
   switch (R.logn) {
     case 10: return launch_inv_t<10>(tasks, count, R, st);
     case 11: return launch_inv_t<11>(tasks, count, R, st);
-    case 12: return launch_inv_t<12>(tasks, count, R, st);
-    case 13: return launch_inv_t<13>(tasks, count, R, st);
-    case 14: return launch_inv_t<14>(tasks, count, R, st);
     default: return cudaErrorInvalidValue;
   }
 }

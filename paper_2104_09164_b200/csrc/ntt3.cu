@@ -146,10 +146,6 @@ HB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar)
       "l"(src), "r"(bytes), "r"(b)
       : "memory");
 }
-// fire-and-forget 64-bit add to global memory (no return value: RED)
-HB_DEV void red_add_u64(const u64* p, u64 v) {
-  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 // a second bulk copy on a barrier already armed for its bytes
 HB_DEV void bulk_g2s_more(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
   const uint32_t d = smem_addr(dst), b = smem_addr(mbar);
@@ -294,8 +290,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   // (written by the inverse transform, task scal = 1), lifted once for all
   // target primes instead of once per target row
   const bool lifted = tk.src_prime < 0;
-  if ((MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER ||
-       MODE == FWD_LIFT_KS) && !lifted) {
+  if ((MODE == FWD_LIFT || MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER) && !lifted) {
     ps = R.primes[tk.src_prime].p;
     ps_half = ps >> 1;
   }
@@ -364,13 +359,12 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     }
   }
   constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
-  constexpr bool KS = MODE == FWD_LIFT_KS;   // aux = key row b, add = key row a
-  if ((MD || KS) && HB_NTT3_SB) {
+  if (MD && HB_NTT3_SB) {
     if (t == 0 && HB_NTT3_L2PF) {   // the epilogue's x_r / addend tiles into L2 meanwhile
       l2_prefetch(tk.aux + (size_t)rank * TILE3, TILE3 * 8);
       if (tk.add && !(MODE == FWD_MODDOWN && tk.perm)) l2_prefetch(tk.add + (size_t)rank * TILE3, TILE3 * 8);
     }
-  } else if (MD || KS) {
+  } else if (MD) {
     // the column slice is consumed: prefetch the epilogue's x_r tile into it
     // (TMA bulk copy) while the block pass runs
     __syncthreads();
@@ -421,7 +415,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {   // back in place: balanced (ModDown) or canonical
       const int pc = swz3_chunk((e0 >> 1) + v);
-      if (MD || KS) {
+      if (MD) {
         rb[2 * pc] = x[2 * v];
         rb[2 * pc + 1] = x[2 * v + 1];
       } else {
@@ -437,28 +431,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   // chain cost ~30 integer instructions per element)
   const double pd = P.pd, pinv = P.pinv;
   const double sd = u64_to_f(tk.scal), sq = sd * pinv;
-  if ((MD || KS) && !HB_NTT3_SB) mbar_wait0(mbar + 1);
-  if (KS) {
-    // fused key-switch inner product: this digit's transformed row times the
-    // two key rows, accumulated with 64-bit atomic adds of canonical products
-    // (a digit set of d digits sums below d * p < 2^64; reduced afterwards)
-#pragma unroll 4
-    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-      const int k = t + i * THREADS3;
-      const size_t j = base + 2 * k;
-      const int pc = swz3_chunk(k);
-      const ulonglong2 kb = HB_NTT3_SB ? __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j))
-                                       : *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
-      const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
-      const double y0 = rb[2 * pc], y1 = rb[2 * pc + 1];
-      const double y0q = y0 * pinv, y1q = y1 * pinv;
-      red_add_u64(tk.dst + j, fmod_canon(fmod_mul(u64_to_f(kb.x), y0, y0q, pd), pd, pinv));
-      red_add_u64(tk.dst + j + 1, fmod_canon(fmod_mul(u64_to_f(kb.y), y1, y1q, pd), pd, pinv));
-      red_add_u64(tk.add2 + j, fmod_canon(fmod_mul(u64_to_f(ka.x), y0, y0q, pd), pd, pinv));
-      red_add_u64(tk.add2 + j + 1, fmod_canon(fmod_mul(u64_to_f(ka.y), y1, y1q, pd), pd, pinv));
-    }
-    return;
-  }
+  if (MD && !HB_NTT3_SB) mbar_wait0(mbar + 1);
 #pragma unroll 4
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
     const int k = t + i * THREADS3;
@@ -719,7 +692,6 @@ cudaError_t fwd3_mode(const HbNttTask* tasks, int count, const HbRing& R, int mo
     case FWD_MODDOWN: return fwd3_t<LOGN, FWD_MODDOWN>(tasks, count, R, st);
     case FWD_I64: return fwd3_t<LOGN, FWD_I64>(tasks, count, R, st);
     case FWD_MODDOWN_SCATTER: return fwd3_t<LOGN, FWD_MODDOWN_SCATTER>(tasks, count, R, st);
-    case FWD_LIFT_KS: return fwd3_t<LOGN, FWD_LIFT_KS>(tasks, count, R, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -14,10 +14,6 @@ enum FwdMode : int {
   FWD_MODDOWN_SCATTER = 4,  // FWD_MODDOWN whose result lands at dst[perm[j]] and
                             // whose addend is read at j: a rotation computed on
                             // pre-permuted keys
-  FWD_LIFT_KS = 5,          // FWD_LIFT fused with the key-switch inner product:
-                            // y = NTT(lift(digit)); dst += y*aux, add2 += y*add
-                            // (64-bit atomic adds of canonical products;
-                            // cluster NTT only)
 };
 
 // ---------------------------------------------------------------------------

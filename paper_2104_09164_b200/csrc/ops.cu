@@ -92,44 +92,6 @@ cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* 
 }
 
 // ---------------------------------------------------------------------------
-// Plaintext multiply-accumulate: one output row = sum over its terms of
-// pt * ct (mod p).  Replaces chains of ring.py:127 pw_mul + ring.py:159
-// pw_add issued by the convolution / FC schedules; modular sums are exact,
-// so the result equals the chained ops bit for bit.  Products accumulate in
-// 128 bits and fold to a residue every 8 terms (p < 2^62 => no overflow).
-__global__ void __launch_bounds__(EW_THREADS)
-k_mac(const HbMacTask* __restrict__ tasks, int ntasks, const HbMacTerm* __restrict__ terms,
-      const HbPrime* __restrict__ primes, int n) {
-  HB_PDL_ENTRY();
-  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
-    const HbMacTask tk = tasks[t];
-    const HbPrime P = primes[tk.prime];
-    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
-    if (j >= n) continue;
-    Acc128 s0, s1;
-    for (int k = 0; k < tk.nterms; ++k) {
-      const HbMacTerm tm = terms[tk.term_off + k];
-      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(tm.pt + j));
-      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(tm.ct + j));
-      s0.mac(a.x, b.x);
-      s1.mac(a.y, b.y);
-      if ((k & 7) == 7) { s0.fold(P); s1.fold(P); }
-    }
-    ulonglong2 r;
-    r.x = s0.fold(P);
-    r.y = s1.fold(P);
-    *reinterpret_cast<ulonglong2*>(tk.dst + j) = r;
-  }
-}
-
-cudaError_t launch_mac(const HbMacTask* tasks, int ntasks, const HbMacTerm* terms,
-                       const HbPrime* primes, int n, cudaStream_t st) {
-  if (ntasks <= 0) return cudaSuccess;
-  (void)hb_launch(k_mac, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, tasks, ntasks, terms, primes, n);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
 // Tensor product of two ciphertexts row by row (engine.py:249-257):
 //   d0 = a0*b0, d1 = a0*b1 + a1*b0, d2 = a1*b1.
 struct HbTensorTask {
@@ -217,54 +179,6 @@ cudaError_t launch_tensor(const void* tasks, int ntasks, const HbPrime* primes, 
   else
     (void)hb_launch(k_tensor, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st,
                     reinterpret_cast<const HbTensorTask*>(tasks), ntasks, primes, n);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Key-switch inner product with the Galois gather fused in
-// (ring.py:136-156 pw_mul_accum_perm): for every output row r,
-//   out_b[n] = sum_i de_i[perm[n]] * kb_i[n],   out_a[n] = sum_i de_i[perm[n]] * ka_i[n].
-__global__ void __launch_bounds__(EW_THREADS)
-k_ks_inner(const HbKsTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__ primes,
-           int n) {
-  HB_PDL_ENTRY();
-  for (int t = blockIdx.y; t < ntasks; t += gridDim.y) {
-    const HbKsTask tk = tasks[t];
-    const HbPrime P = primes[tk.prime];
-    const int j = 2 * (blockIdx.x * EW_THREADS + threadIdx.x);
-    if (j >= n) continue;
-    int s0 = j, s1 = j + 1;
-    if (tk.perm) {
-      const int2 pp = __ldg(reinterpret_cast<const int2*>(tk.perm + j));
-      s0 = pp.x;
-      s1 = pp.y;
-    }
-    Acc128 b0, b1, a0, a1;
-    for (int i = 0; i < tk.ndig; ++i) {
-      const u64* de = tk.de + i * tk.de_stride;
-      const u64 x0 = __ldg(de + s0), x1 = __ldg(de + s1);
-      const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(tk.kb + i * tk.key_stride + j));
-      const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(tk.ka + i * tk.key_stride + j));
-      b0.mac(x0, kb.x);
-      b1.mac(x1, kb.y);
-      a0.mac(x0, ka.x);
-      a1.mac(x1, ka.y);
-      if ((i & 7) == 7) { b0.fold(P); b1.fold(P); a0.fold(P); a1.fold(P); }
-    }
-    ulonglong2 rb, ra;
-    rb.x = b0.fold(P);
-    rb.y = b1.fold(P);
-    ra.x = a0.fold(P);
-    ra.y = a1.fold(P);
-    *reinterpret_cast<ulonglong2*>(tk.out_b + j) = rb;
-    *reinterpret_cast<ulonglong2*>(tk.out_a + j) = ra;
-  }
-}
-
-cudaError_t launch_ks_inner(const HbKsTask* tasks, int ntasks, const HbPrime* primes, int n,
-                            cudaStream_t st) {
-  if (ntasks <= 0) return cudaSuccess;
-  (void)hb_launch(k_ks_inner, dim3(ew_grid(ntasks, n)), dim3(EW_THREADS), 0, st, tasks, ntasks, primes, n);
   return cudaGetLastError();
 }
 
@@ -491,13 +405,10 @@ cudaError_t launch_mac_strided(const void* outs, int nout, const HbMacTerm* term
 namespace hb {
 
 // ---------------------------------------------------------------------------
-// Shared-term multiply-accumulate: a group of outputs that sum products with
-// the SAME ciphertext term list (hconv's giant/baby partial sums, the FC
-// diagonals): out_o = sum_t pt[o][t] * ct[t].  Block = 32 coefficient pairs
-// x up to 8 clip-components (bc); a thread keeps 8 outputs' 128-bit
-// accumulators while streaming the terms, so each ciphertext row is read
-// once per 8 outputs instead of once per output, and the 8 bc-warps of a
-// block read the same plaintext addresses (L1 broadcast).
+// Shared-term multiply-accumulate group: outputs that sum products with the
+// SAME ciphertext term list (hconv's giant/baby partial sums, the FC
+// diagonals): out_o = sum_t pt[o][t] * ct[t] (mac.cu k_mac_pipe, and the
+// k_mac_gemm fallbacks below).
 struct HbMacGroup {
   const u64* const* cts;   // [nterms] ciphertext bases ([BC, R, N] blocks)
   const u64* const* pts;   // [nout][nterms] plaintext bases (rows at +r*N)
@@ -505,66 +416,6 @@ struct HbMacGroup {
   int nterms;
   int nout;
 };
-
-constexpr int MAC_OT = 8;
-
-__global__ void __launch_bounds__(256)
-k_mac_shared(HbMacGroup g, const HbPrime* __restrict__ primes, int n, int R, int BC) {
-  HB_PDL_ENTRY();
-  const int jp = blockIdx.x * 32 + threadIdx.x;       // coefficient pair
-  const int r = blockIdx.y % R;
-  const int bc = (blockIdx.y / R) * blockDim.y + threadIdx.y;
-  const int o0 = blockIdx.z * MAC_OT;
-  const int j = 2 * jp;
-  if (j >= n || bc >= BC) return;
-  const HbPrime P = primes[r];
-  const int no = min(MAC_OT, g.nout - o0);
-  const size_t ct_off = ((size_t)bc * R + r) * n + j;
-  const size_t pt_off = (size_t)r * n + j;
-  Acc128 acc[MAC_OT][2];
-  for (int t = 0; t < g.nterms; ++t) {
-    const ulonglong2 c = __ldg(reinterpret_cast<const ulonglong2*>(g.cts[t] + ct_off));
-#pragma unroll
-    for (int o = 0; o < MAC_OT; ++o) {
-      if (o < no) {
-        const ulonglong2 a =
-            __ldg(reinterpret_cast<const ulonglong2*>(g.pts[(size_t)(o0 + o) * g.nterms + t] + pt_off));
-        acc[o][0].mac(a.x, c.x);
-        acc[o][1].mac(a.y, c.y);
-      }
-    }
-    if ((t & 7) == 7) {
-#pragma unroll
-      for (int o = 0; o < MAC_OT; ++o) { acc[o][0].fold(P); acc[o][1].fold(P); }
-    }
-  }
-#pragma unroll
-  for (int o = 0; o < MAC_OT; ++o) {
-    if (o < no) {
-      ulonglong2 v;
-      v.x = acc[o][0].fold(P);
-      v.y = acc[o][1].fold(P);
-      *reinterpret_cast<ulonglong2*>(g.dsts[o0 + o] + ct_off) = v;
-    }
-  }
-}
-
-cudaError_t launch_mac_shared(const void* cts, const void* pts, const void* dsts, int nterms,
-                              int nout, const HbPrime* primes, int n, int R, int BC,
-                              cudaStream_t st) {
-  if (nout <= 0 || nterms <= 0) return cudaSuccess;
-  HbMacGroup g;
-  g.cts = reinterpret_cast<const u64* const*>(cts);
-  g.pts = reinterpret_cast<const u64* const*>(pts);
-  g.dsts = reinterpret_cast<u64* const*>(dsts);
-  g.nterms = nterms;
-  g.nout = nout;
-  const int by = BC < 8 ? BC : 8;
-  dim3 block(32, by);
-  dim3 grid((n / 2 + 31) / 32, R * ((BC + by - 1) / by), (nout + MAC_OT - 1) / MAC_OT);
-  (void)hb_launch(k_mac_shared, dim3(grid), dim3(block), 0, st, g, primes, n, R, BC);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------------------
 // Key-switch inner product, clip-blocked: one task per (job, output row r);
@@ -762,9 +613,6 @@ cudaError_t launch_mac_gemm(const void* cts, const void* pts, const void* dsts, 
   g.nterms = nterms;
   g.nout = nout;
   if (BC <= 2) return mac_gemm_t<4, 2, 8, 1>(g, primes, n, R, BC, st);
-  const char* v = getenv("HEAR_B200_MAC_TILE");
-  if (v && v[0] == '8') return mac_gemm_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
-  if (v && v[0] == '2') return mac_gemm_t<2, 8, 4, 2>(g, primes, n, R, BC, st);
   return mac_gemm_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
 }
 
@@ -884,11 +732,8 @@ cudaError_t launch_mac_gemm_f64(const void* cts, const void* pts, const void* ds
   g.nterms = nterms;
   g.nout = nout;
   if (BC <= 2) return mac_gemm_f64_t<4, 2, 8, 1>(g, primes, n, R, BC, st);
-  if (BC <= 8) return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
-  // 4x4 tiles measured fastest on the conv shapes (tools/mac_sweep.sh): 4x8
+  // 4x4 tiles measured fastest on the conv shapes (round-1 tile sweep): 4x8
   // needs ~156 registers (one CTA per SM), too few warps to cover load latency
-  const char* v = getenv("HEAR_B200_MAC_TILE");
-  if (v && v[0] == '8') return mac_gemm_f64_t<4, 8, 2, 4>(g, primes, n, R, BC, st);
   return mac_gemm_f64_t<4, 4, 4, 2>(g, primes, n, R, BC, st);
 }
 

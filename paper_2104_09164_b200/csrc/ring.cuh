@@ -66,12 +66,6 @@ struct HbRing {
   //   off = {0, 4, 6}
   const HbTwD* tw3_fwd;   // [nprimes][n] (7n/8 used)
   const HbTwD* tw3_inv;
-  // chunked exact dot products (ops.cu k_mac_gemm_c3): ciphertext residues
-  // split into three chunk_w-bit limbs; products summed exactly in fp64 for
-  // chunk_fold terms between reductions (0 = disabled for this ring)
-  int chunk_w;
-  int chunk_fold;
-  const double* chunk_consts;  // [nprimes][4]: 2^w mod p, fl(./p), 2^2w mod p, fl(./p)
 };
 
 // Raise a kernel's dynamic shared-memory limit only when a launch needs more
@@ -118,21 +112,6 @@ struct HbMacTerm {
   const u64* ct;
 };
 
-// One output row pair of the key-switch inner product:
-//   out_b[n] = sum_i de_i[perm[n]] * kb_i[n],  out_a likewise with ka.
-// de_i = de + i * de_stride, kb_i = kb + i * key_stride.
-struct HbKsTask {
-  const u64* de;
-  const u64* kb;
-  const u64* ka;
-  u64* out_b;
-  u64* out_a;
-  const int* perm;
-  long long de_stride;
-  long long key_stride;
-  int ndig;
-  int prime;
-};
 
 // Generic element-wise row op.
 struct HbEwTask {
