@@ -27,14 +27,17 @@ strides so far); one ciphertext holds n2 / B blocks, so every layer of both
 networks is ONE ciphertext handle (which may carry a batch of clips).
 
 Convolution (valid padding, stride s), baby-step / giant-step over the
-slot-block offset d = c_in - f_out (the rotate-and-sum of HEAR §3.2 with
-the giant/baby refinement of §3.4, Eqs. 3-4):
+slot-block offset d = c_in - f_out = g D + e (0 <= e < g; the rotate-and-
+sum of HEAR §3.2 with the giant/baby refinement of §3.4, Eqs. 3-4):
 
-    y = sum_d rot( sum_k W'_{d,k} * rot(x, k ts), d B )
+    y = sum_D rot( sum_{e,k} W''_{D,e,k} * rot(x, e B + k ts), g D B )
 
-with W'_{d,k}[c B + s t' ts] = W[c - d, c, k] for every valid output t':
-K - 1 hoisted baby rotations of the input, one giant rotation per offset,
-one plaintext product per (d, k).  Weights are zero off the output lattice
+with W''_{D,e,k}[(f + g D) B + s t' ts] = W[f, f + g D + e, k] for every
+valid output t': K g - 1 hoisted baby rotations of the input (one ModUp),
+one giant rotation per D, one plaintext product per nonzero (D, e, k).  The
+baby width g minimises (K g) x (hoisted cost) + (#D) x (full key-switch
+cost): a hoisted rotation costs the ModDown (2 (l+1) NTTs), a giant one
+ModUp + ModDown ((l+1)(l+2) + 2 (l+1) NTTs).  Weights are zero off the output lattice
 and outside the filter range, so every slot outside the valid lattice stays
 EXACTLY zero through the network (no masks), which lets the polynomial
 activation add its constant term only on the lattice and lets the pooling
@@ -202,7 +205,8 @@ class TcnPlan:
     params: object
     delta: Fraction
     ts: list                          # slot stride of the time axis per layer (input first)
-    offsets: list                     # per conv: giant-step block offsets d
+    offsets: list                     # per conv: block offsets d = c_in - f_out
+    bsgs: list = field(default_factory=list)   # per conv: (g, [giant D], {D: [(e, k)]})
     steps: dict = field(default_factory=dict)
     rotations: dict = field(default_factory=dict)
 
@@ -218,6 +222,24 @@ def _need_rot(rot: dict, amount: int, level: int, n2: int):
     a = amount % n2
     if a:
         rot[a] = max(rot.get(a, -1), level)
+
+
+def _bsgs_split(offs, kernel: int, lvl: int):
+    """(g, giant steps D, {D: [(e, k)]}) covering every block offset
+    d = g D + e of `offs` with the fewest NTT-equivalents: baby rotations
+    are hoisted (ModDown: 2 (l+1) NTTs each), giant ones full key switches
+    ((l+1)(l+2) ModUp + 2 (l+1) ModDown NTTs)."""
+    r = lvl + 1
+    best = None
+    for g in range(1, 33):
+        ds = sorted({d // g for d in offs})   # floor division: e = d - g D in [0, g)
+        cost = (kernel * g) * 2 * r + len([D for D in ds if D]) * (r * (r + 1) + 2 * r)
+        if best is None or cost < best[0]:
+            best = (cost, g, ds)
+    _, g, ds = best
+    terms = {D: sorted({(d - g * D, k) for d in offs if d // g == D for k in range(kernel)})
+             for D in ds}
+    return g, ds, terms
 
 
 def compile_tcn(shape: TcnShape, params) -> TcnPlan:
@@ -242,10 +264,13 @@ def compile_tcn(shape: TcnShape, params) -> TcnPlan:
         cin = chans[i]
         offs = sorted({c - f for c in range(cin) for f in range(cv.filters)})
         plan.offsets.append(offs)
-        for k in range(1, cv.kernel):
-            _need_rot(rot, k * ts[i], lvl, n2)
-        for d in offs:
-            _need_rot(rot, d * B, lvl, n2)
+        g, giants, terms = _bsgs_split(offs, cv.kernel, lvl)
+        plan.bsgs.append((g, giants, terms))
+        for e in range(g):
+            for k in range(cv.kernel):
+                _need_rot(rot, e * B + k * ts[i], lvl, n2)
+        for D in giants:
+            _need_rot(rot, g * D * B, lvl, n2)
         lvl -= 1                                   # conv rescale -> scale delta
         scale = delta
         plan.steps[f"conv{i + 1}"] = TcnStep(f"conv{i + 1}", lvl, scale)
@@ -306,7 +331,8 @@ class TcnEncoder:
         return self.compiled.expected("input" if i == 0 else f"act{i}").level
 
     def conv_pts(self, i: int) -> dict:
-        """{(d, k): plaintext} of conv i (0-based)."""
+        """{(D, e, k): plaintext W''} of conv i (0-based): value
+        W[f, f + g D + e, k] at block f + g D on the output lattice."""
         key = ("conv", i)
         if key not in self._pts:
             pl, sh = self.compiled, self.compiled.shape
@@ -315,14 +341,16 @@ class TcnEncoder:
             tout = sh.lengths()[i + 1]
             cin = sh.channels()[i]
             lattice = np.arange(tout) * cv.stride * ts
+            g, giants, terms = pl.bsgs[i]
             keys, vecs = [], []
-            for d in pl.offsets[i]:
-                cs = np.arange(max(d, 0), min(cin, cv.filters + d))   # c with f = c - d valid
-                for k in range(cv.kernel):
+            for D in giants:
+                for e, k in terms[D]:
+                    d = g * D + e
+                    fs = np.arange(max(-d, 0), min(cv.filters, cin - d))   # c = f + d valid
                     v = np.zeros(n2)
-                    for c in cs:
-                        v[c * B + lattice] = w[c - d, c, k]
-                    keys.append((d, k))
+                    for f in fs:
+                        v[(f + g * D) % (n2 // B) * B + lattice] = w[f, f + d, k]
+                    keys.append((D, e, k))
                     vecs.append(v)
             lvl = self._in_level(i)
             pts = self._enc(vecs, lvl, self._pscale(lvl, self._in_scale(i)))
@@ -407,17 +435,18 @@ def run_tcn(encoder: TcnEncoder, ct: Ct, backend: BackendBase) -> Ct:
         with backend.layer(f"conv{i + 1}"):
             ts = pl.ts[i]
             pts = encoder.conv_pts(i)
-            baby = backend.rot_many(ct, [k * ts for k in range(cv.kernel)])
-            offs = pl.offsets[i]
+            g, giants, terms = pl.bsgs[i]
+            baby = backend.rot_many(ct, [e * B + k * ts for e in range(g)
+                                         for k in range(cv.kernel)])
             acc = None
-            # giant steps in groups of GIANT_GROUP offsets: the inner sums of
-            # one group are live at a time (93 offsets x B clips at N = 2^16
-            # would not fit HBM); same op counts as one flat sum
-            for g0 in range(0, len(offs), GIANT_GROUP):
-                grp = offs[g0:g0 + GIANT_GROUP]
-                inner = backend.mac_many([[(baby[k * ts % backend.n2], pts[(d, k)])
-                                           for k in range(cv.kernel)] for d in grp])
-                giant = backend.rot_each([(x, d * B) for x, d in zip(inner, grp)])
+            # giant steps in groups of GIANT_GROUP: the inner sums of one
+            # group are live at a time (B clips x rows per handle); same op
+            # counts as one flat sum
+            for g0 in range(0, len(giants), GIANT_GROUP):
+                grp = giants[g0:g0 + GIANT_GROUP]
+                inner = backend.mac_many([[(baby[(e * B + k * ts) % backend.n2], pts[(D, e, k)])
+                                           for e, k in terms[D]] for D in grp])
+                giant = backend.rot_each([(x, g * D * B) for x, D in zip(inner, grp)])
                 part = backend.sum_each([giant])[0]
                 acc = part if acc is None else backend.add(acc, part)
             ct = backend.rescale(acc)
