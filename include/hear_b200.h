@@ -149,8 +149,10 @@ int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stre
 /* Fast RNS base conversion, one task per (polynomial, source basis):
  * dst_t = sum_i [src_i * qhat_i^-1]_{q_i} * (qhat_i mod p_t) mod p_t
  * (csrc/bconv.cu; the ModUp / ModDown of hybrid dnum-digit key switching,
- * BASELINE config 1; the reference's per-prime digits need none).          */
-int hb_bconv(hb_ring* ring, const void* tasks, int count, void* stream);
+ * BASELINE config 1; the reference's per-prime digits need none).  nsrc:
+ * the source count shared by every task (selects a register-resident
+ * kernel), 0 when the tasks differ.                                           */
+int hb_bconv(hb_ring* ring, const void* tasks, int count, int nsrc, void* stream);
 /* Ciphertext tensor product d0, d1, d2 (engine.py:249-257).                  */
 int hb_tensor(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Exact CRT of `keep` coefficient rows to centred doubles (engine.py:156-175). */

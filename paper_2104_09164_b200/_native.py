@@ -53,7 +53,7 @@ def lib():
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
         L.hb_sum.argtypes = [vp, vp, i32, vp, vp]
         L.hb_ks_inner2.argtypes = [vp, vp, i32, i32, vp]
-        L.hb_bconv.argtypes = [vp, vp, i32, vp]
+        L.hb_bconv.argtypes = [vp, vp, i32, i32, vp]
         L.hb_mac_shared.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
         L.hb_crt_double.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
         L.hb_fft_create.restype = vp

@@ -561,21 +561,18 @@ class CkksBackend(BackendBase):
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
     def _raw_rescale(self, a: Ct) -> Ct:
-        """Exact RNS division by the top prime (engine.py:263-281)."""
-        lvl = a.level
-        x = a.payload.data
-        bsz = x.shape[0]
-        top = x[:, :, lvl].contiguous().reshape(bsz * 2, self.n)
-        topc = self._intt_rows(top, np.full(bsz * 2, lvl))
-        out = self.ring.empty(bsz * 2, lvl)
-        aux = x[:, :, :lvl].contiguous().reshape(bsz * 2, lvl, self.n)
-        inv, inv_sh = self._resc[lvl]
-        self._moddown_into(out, self.ring.row_ptrs(topc), lvl, aux, inv, inv_sh)
-        scale = a.scale / self.params.chain_primes[lvl]
-        return Ct(CtData(out.reshape(bsz, 2, lvl, self.n)), lvl - 1, scale, self.n2)
+        """Exact RNS division by the top prime (engine.py:263-281): the
+        batched form on row pointers (no copies of the input rows)."""
+        return self._raw_rescale_each([a])[0]
 
     def _raw_mod_down(self, a: Ct, to_level: int) -> Ct:
-        out = a.payload.data[:, :, :to_level + 1].contiguous()
+        """Drop the rows above to_level: one copy launch of the kept rows
+        (k_ew COPY on row pointers) into a contiguous handle."""
+        x = a.payload.data
+        bsz, r = x.shape[0], to_level + 1
+        out = self.ring.empty(bsz, 2, r)
+        src = self.ring.row_ptrs(x).reshape(bsz * 2, x.shape[2])[:, :r].ravel()
+        self._ew(nat.EW_COPY, self.ring.row_ptrs(out), src, primes=self._row_primes(2 * bsz, r))
         return Ct(CtData(out), to_level, a.scale, self.n2)
 
     # ------------------------------------------------------------------ key switching

@@ -150,10 +150,14 @@ class HybridKeySwitch:
             off = self._offsets(tuple(rows))
             t[q] = (src_ptr, dst_ptr, off.data_ptr(), tab.data_ptr(), sp.data_ptr(),
                     tp.data_ptr(), self.n, len(src), len(dst))
-        for c0 in range(0, len(jobs), 65535):
-            d = _upload(t[c0:c0 + 65535], self.dev)
-            nat.check(nat.lib().hb_bconv(self.ring.handle, d.data_ptr(), len(t[c0:c0 + 65535]),
-                                         self.ring.stream), "bconv")
+        # one launch per source count (the register-resident kernel variant)
+        for ns in np.unique(t["s"]):
+            sub = t[t["s"] == ns]
+            for c0 in range(0, len(sub), 65535):
+                d = _upload(sub[c0:c0 + 65535], self.dev)
+                nat.check(nat.lib().hb_bconv(self.ring.handle, d.data_ptr(),
+                                             len(sub[c0:c0 + 65535]), int(ns), self.ring.stream),
+                          "bconv")
 
     def _offsets(self, rows: tuple) -> torch.Tensor:
         key = ("off", rows)

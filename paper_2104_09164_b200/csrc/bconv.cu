@@ -37,16 +37,21 @@ struct HbBconvTask {
   int s, t;
 };
 
+// SRC > 0: the source count is a compile-time constant (the scaled residues
+// stay in registers); SRC = 0: any count up to BCONV_MAXS (local memory).
+template <int SRC>
 __global__ void __launch_bounds__(BCONV_THREADS)
 k_bconv(const HbBconvTask* __restrict__ tasks, const HbPrime* __restrict__ primes, int n) {
   HB_PDL_ENTRY();
   const HbBconvTask tk = tasks[blockIdx.y];
   const int j = blockIdx.x * BCONV_THREADS + threadIdx.x;
   if (j >= n) return;
-  u64 y[BCONV_MAXS];
+  const int s = SRC ? SRC : tk.s;
+  u64 y[SRC ? SRC : BCONV_MAXS];
   unsigned neg = 0;   // bit i: term i uses the centred representative y_i - q_i
-#pragma unroll 4
-  for (int i = 0; i < tk.s; ++i) {
+#pragma unroll
+  for (int i = 0; i < (SRC ? SRC : BCONV_MAXS); ++i) {
+    if (i >= s) break;
     const u64 q = primes[__ldg(tk.sprime + i)].p;
     u64 v = mul_shoup(__ldg(tk.src + i * tk.src_stride + j), __ldg(tk.tab + 2 * i),
                       __ldg(tk.tab + 2 * i + 1), q);
@@ -56,26 +61,37 @@ k_bconv(const HbBconvTask* __restrict__ tasks, const HbPrime* __restrict__ prime
     }
     y[i] = v;
   }
-  const u64* m = tk.tab + 2 * tk.s;
+  const u64* m = tk.tab + 2 * s;
   for (int t = 0; t < tk.t; ++t) {
     const HbPrime P = primes[__ldg(tk.tprime + t)];
-    Acc128 pos, ngt;   // positive and negative terms, one reduction each
-    for (int i = 0; i < tk.s; ++i) {
+    Acc128 acc;   // a negative term -y * w enters as y * (p_t - w): one accumulator
+#pragma unroll
+    for (int i = 0; i < (SRC ? SRC : BCONV_MAXS); ++i) {
+      if (i >= s) break;
       const u64 w = __ldg(m + i * tk.t + t);
-      if (neg >> i & 1) ngt.mac(y[i], w); else pos.mac(y[i], w);
-      if ((i & 7) == 7) { pos.fold(P); ngt.fold(P); }
+      acc.mac(y[i], (neg >> i & 1) ? P.p - w : w);
+      if ((i & 7) == 7) acc.fold(P);
     }
-    tk.dst[__ldg(tk.dst_off + t) + j] = sub_mod(pos.fold(P), ngt.fold(P), P.p);
+    tk.dst[__ldg(tk.dst_off + t) + j] = acc.fold(P);
   }
 }
 
-cudaError_t launch_bconv(const void* tasks, int ntasks, const HbPrime* primes, int n,
+cudaError_t launch_bconv(const void* tasks, int ntasks, int nsrc, const HbPrime* primes, int n,
                          cudaStream_t st) {
   if (ntasks <= 0) return cudaSuccess;
   if (ntasks > 65535) return cudaErrorInvalidValue;
   const dim3 grid((n + BCONV_THREADS - 1) / BCONV_THREADS, ntasks);
-  (void)hb_launch(k_bconv, grid, dim3(BCONV_THREADS), 0, st,
-                  reinterpret_cast<const HbBconvTask*>(tasks), primes, n);
+  const HbBconvTask* t = reinterpret_cast<const HbBconvTask*>(tasks);
+  // nsrc: the source count every task of the launch shares (a ModUp's
+  // digit size, a ModDown's special-prime count), 0 when they differ
+  switch (nsrc) {
+#define HB_BCONV(S) \
+  case S: (void)hb_launch(k_bconv<S>, grid, dim3(BCONV_THREADS), 0, st, t, primes, n); break;
+    HB_BCONV(1) HB_BCONV(2) HB_BCONV(3) HB_BCONV(4) HB_BCONV(5) HB_BCONV(6) HB_BCONV(7)
+    HB_BCONV(8)
+#undef HB_BCONV
+    default: (void)hb_launch(k_bconv<0>, grid, dim3(BCONV_THREADS), 0, st, t, primes, n);
+  }
   return cudaGetLastError();
 }
 

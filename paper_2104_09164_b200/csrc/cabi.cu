@@ -43,7 +43,7 @@ cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, i
                            const HbRing&, int, int, long long, long long, int, int,
                            cudaStream_t);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
-cudaError_t launch_bconv(const void*, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_bconv(const void*, int, int, const HbPrime*, int, cudaStream_t);
 int bconv_task_size();
 cudaError_t launch_lift_center(const u64*, u64, long long*, int, cudaStream_t);
 cudaError_t launch_reduce_rows(const long long*, const int*, int, const HbPrime*, u64*, int,
@@ -336,8 +336,9 @@ int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream)
 }
 
 // Fast RNS base conversion (bconv.cu): hybrid key switching ModUp / ModDown.
-int hb_bconv(hb_ring* r, const void* tasks, int count, void* stream) {
-  cudaError_t e = launch_bconv(tasks, count, r->dev.primes, r->dev.n, (cudaStream_t)stream);
+int hb_bconv(hb_ring* r, const void* tasks, int count, int nsrc, void* stream) {
+  if (nsrc < 0 || nsrc > 32) return fail(cudaErrorInvalidValue, "hb_bconv: source count");
+  cudaError_t e = launch_bconv(tasks, count, nsrc, r->dev.primes, r->dev.n, (cudaStream_t)stream);
   return e ? fail(e, "hb_bconv") : 0;
 }
 
