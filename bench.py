@@ -244,7 +244,7 @@ def reference_arm(args):
 FP64_MEASURED_TFLOPS = 17.93   # DFMA/s measured on this pool (profiles/r01_microbench.txt)
 
 
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
 
 
 def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
