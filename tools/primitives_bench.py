@@ -85,7 +85,8 @@ def main():
                       "ciphertexts": nb * bsz, "batch_per_launch": bsz, "rotation_steps": steps}}
 
     def timed(fn, ops):
-        fn(batches[0])
+        for b in batches[:4]:   # warm-up (clocks, caches, allocator)
+            fn(b)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
