@@ -260,22 +260,6 @@ class CkksBackend(BackendBase):
                                  dst=self.ring.row_ptrs(out), dst_prime=primes, src_prime=primes))
         return out
 
-    def _moddown_into(self, out: torch.Tensor, src_coef_ptrs, src_prime, aux: torch.Tensor,
-                      scal, scal_sh, add_ptrs=None, perm_ptr=0):
-        """out[..., r, :] = (aux[..., r, :] - lift(src) mod p_r) * scal_r (+ add).
-
-        out/aux: [M, R, N]; src_coef_ptrs: [M] coefficient rows mod src_prime."""
-        m, r = out.shape[0], out.shape[1]
-        f = dict(src=np.repeat(src_coef_ptrs, r), dst=self.ring.row_ptrs(out),
-                 aux=self.ring.row_ptrs(aux), src_prime=np.repeat(np.asarray(src_prime), r)
-                 if np.ndim(src_prime) else src_prime,
-                 dst_prime=np.tile(np.arange(r), m), scal=np.tile(scal, m),
-                 scal_sh=np.tile(scal_sh, m))
-        if add_ptrs is not None:
-            f["add"] = add_ptrs
-            f["perm"] = perm_ptr
-        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * r, **f), nat.FWD_MODDOWN)
-
     # ------------------------------------------------------------------ keygen
 
     def _keygen(self):
@@ -415,11 +399,9 @@ class CkksBackend(BackendBase):
         b = d.shape[0]
         rp = self.ring.row_ptrs
         m = self.ring.empty(b, keep)
-        c0 = d[:, 0, :keep].contiguous()
-        c1 = d[:, 1, :keep].contiguous()
-        s = self.keys.s_ntt[:keep].contiguous()
-        self._ew(nat.EW_MULADD, rp(m), rp(c1), np.tile(rp(s), b), rp(c0),
-                 primes=self._row_primes(b, keep))
+        dr = rp(d).reshape(b, 2, d.shape[2])[:, :, :keep]   # row pointers, no copies
+        self._ew(nat.EW_MULADD, rp(m), dr[:, 1].ravel(), np.tile(rp(self.keys.s_ntt)[:keep], b),
+                 dr[:, 0].ravel(), primes=self._row_primes(b, keep))
         coef = self._intt_rows(m, self._row_primes(b, keep))
         consts, idx, nl = self._crt_consts(keep)
         out = torch.empty(b, self.n, dtype=torch.float64, device=self.dev)
@@ -462,17 +444,16 @@ class CkksBackend(BackendBase):
             noise[i, 2] = self._gauss()
         uee = self._coeffs_to_ntt(self._dev(noise).reshape(3 * b, self.n), gidx).reshape(b, 3, r, self.n)
         sel = rows + [self.L + 1]
-        pkb = self.keys.pk_b[sel].contiguous()
-        pka = self.keys.pk_a[sel].contiguous()
         rp = self.ring.row_ptrs
+        pkb, pka = rp(self.keys.pk_b)[sel], rp(self.keys.pk_a)[sel]   # row pointers, no copies
         ext = self.ring.empty(b, 2, r)
         er = rp(ext).reshape(b, 2, r)
         ur = rp(uee).reshape(b, 3, r)
         prim = self._row_primes(b, r, gidx)
         # c0 = u*pk_b + e0, c1 = u*pk_a + e1
-        self._ew(nat.EW_MULADD, er[:, 0].ravel(), ur[:, 0].ravel(), np.tile(rp(pkb), b),
+        self._ew(nat.EW_MULADD, er[:, 0].ravel(), ur[:, 0].ravel(), np.tile(pkb, b),
                  ur[:, 1].ravel(), primes=prim)
-        self._ew(nat.EW_MULADD, er[:, 1].ravel(), ur[:, 0].ravel(), np.tile(rp(pka), b),
+        self._ew(nat.EW_MULADD, er[:, 1].ravel(), ur[:, 0].ravel(), np.tile(pka, b),
                  ur[:, 2].ravel(), primes=prim)
         # c0[:level+1] += P * m
         c0rows = er[:, 0, :level + 1].ravel()
@@ -485,13 +466,19 @@ class CkksBackend(BackendBase):
     def _drop_special(self, ext: torch.Tensor, level: int) -> torch.Tensor:
         """ext [M, 2, level+2, N] (special row last) -> (x - [x]_P)/P on the
         chain rows, [M, 2, level+1, N] (engine.py:213-227)."""
-        m = ext.shape[0]
-        flat = ext.reshape(m * 2, level + 2, self.n)
-        spc = self._intt_rows(flat[:, level + 1].contiguous(), np.full(m * 2, self.S))
-        out = self.ring.empty(m * 2, level + 1)
-        self._moddown_into(out, self.ring.row_ptrs(spc), self.S, flat[:, :level + 1].contiguous(),
-                           self._pinv[:level + 1], self._pinv_sh[:level + 1])
-        return out.reshape(m, 2, level + 1, self.n)
+        m, r = ext.shape[0] * 2, level + 1
+        rows = self.ring.row_ptrs(ext).reshape(m, level + 2)   # row pointers, no copies
+        spc = self.ring.empty(m)
+        sp = np.full(m, self.S)
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=rows[:, level + 1], dst=self.ring.row_ptrs(spc),
+                                 dst_prime=sp, src_prime=sp))
+        out = self.ring.empty(m, r)
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * r, src=np.repeat(self.ring.row_ptrs(spc), r),
+                                 dst=self.ring.row_ptrs(out), aux=rows[:, :r].ravel(),
+                                 src_prime=self.S, dst_prime=np.tile(np.arange(r), m),
+                                 scal=np.tile(self._pinv[:r], m),
+                                 scal_sh=np.tile(self._pinv_sh[:r], m)), nat.FWD_MODDOWN)
+        return out.reshape(m // 2, 2, r, self.n)
 
     # ------------------------------------------------------------------ arithmetic
 
