@@ -4,7 +4,6 @@ alloc_keys + the sender's key_tensors + finish_keys must evaluate key
 switches bit-exactly like the sender, and must encrypt from its own random
 stream (not the sender's keygen stream)."""
 
-from fractions import Fraction
 
 import numpy as np
 import pytest

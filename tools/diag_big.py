@@ -3,7 +3,6 @@ N=2^15, config 3 at N=2^16) for batched and clip-by-clip evaluation."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-import torch
 from paper_2104_09164_b200.ckks.engine import CkksBackend
 from paper_2104_09164_b200.ckks.params import fast_hear_ring, tcn_ring16
 which = sys.argv[1]
