@@ -1,4 +1,4 @@
-// Cluster-fused negacyclic NTT (default for fp64 rings at N = 2^13, 2^14).
+// Cluster-fused negacyclic NTT (default for fp64 rings at N = 2^13 .. 2^15).
 //
 // Same transform and fused modes as ntt2.cu (hear/ckks/ring.py:71-124, true
 // inverse), same split of the stages into a column pass (stages 0..S1-1 over
@@ -698,7 +698,7 @@ cudaError_t fwd3_mode(const HbNttTask* tasks, int count, const HbRing& R, int mo
 
 }  // namespace
 
-// fp64 rings at N = 2^13 / 2^14 (clusters of 2 / 4 CTAs); HEAR_B200_NTT3=0
+// fp64 rings at N = 2^13 / 2^14 / 2^15 (clusters of 2 / 4 / 8 CTAs); HEAR_B200_NTT3=0
 // falls back to the two-pass kernels.
 bool ntt3_supported(const HbRing& R) {
   static int off = -1;
@@ -706,10 +706,12 @@ bool ntt3_supported(const HbRing& R) {
     const char* v = getenv("HEAR_B200_NTT3");
     off = (v && v[0] == '0') ? 1 : 0;
   }
-  // 2^15 (clusters of 8) compiles and is exact, but at 77 KB of shared memory
-  // per CTA only two CTAs fit an SM and it measured 5-20 % slower than the
-  // two-pass kernels (tools/ntt_modes.py, NTT_MODES_LOGN=15): not selected
-  return !off && R.use_f64 && R.logn >= 13 && R.logn <= 14;
+  // 2^15 (clusters of 8, the portable maximum): with the one-buffer layout
+  // (44.5 KB per CTA, four CTAs per SM) 14-27 % faster per launch than the
+  // two-pass kernels and config 2 252 -> 320 inferences/s (round 2,
+  // tools/ab_ntt3_15.sh; the round-1 two-buffer layout, 77 KB per CTA, had
+  // measured 5-20 % slower)
+  return !off && R.use_f64 && R.logn >= 13 && R.logn <= 15;
 }
 
 cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,
