@@ -236,11 +236,6 @@ class RingContext:
             raise KeyError("unknown permutation")
         return hit
 
-    @property
-    def two_pass(self) -> bool:
-        """The default two-pass transform (csrc/ntt2.cu) is in use."""
-        return 12 <= self.logn <= 16
-
     def coeff_automorphism(self, coeffs: np.ndarray, g: int) -> np.ndarray:
         """X -> X^g on signed integer coefficients."""
         k = np.arange(self.n, dtype=np.int64)
