@@ -47,37 +47,17 @@ namespace {
 
 constexpr int TILE3 = 4096;
 constexpr int THREADS3 = 256;
-// local buffer, receive buffer, staged twiddles (TW3 x 16 B), 2 mbarriers
-#ifndef HB_NTT3_SB
-#define HB_NTT3_SB 1
-#endif
-// HB_NTT3_SB = 1 (default): ONE 32 KB tile buffer per CTA -- the exchange
-// lands in the buffer the first pass worked in, after a cluster barrier
-// (arrive.release once the last local read is done, wait just before the
-// pushes).  42.5 KB of shared memory and <= 64 registers: four CTAs (32
-// warps) per SM instead of three.  The ModDown x_r tile is then prefetched
-// into L2 (cp.async.bulk.prefetch) instead of into shared memory.
-constexpr int NBUF3 = HB_NTT3_SB ? 1 : 2;
-#ifndef HB_NTT3_L2PF
-#define HB_NTT3_L2PF 1
-#endif
+// Shared memory per CTA: ONE 32 KB tile buffer -- the exchange lands in the
+// buffer the first pass worked in, after a cluster barrier (arrive.release
+// once the last local read is done, wait just before the pushes) -- the
+// staged twiddles (TW3 x 16 B) and one mbarrier: 42.5 KB and <= 64
+// registers, four CTAs (32 warps) per SM.  (Round 1 measured the
+// two-buffer layout with three CTAs per SM, and a TMA-prefetched c0 tile
+// with two, both slower.)  The ModDown x_r / c0 tiles are prefetched into L2
+// (cp.async.bulk.prefetch) while the block pass runs.
 template <int LOGN>
-__host__ __device__ constexpr int smem3() { return NBUF3 * TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
-#ifndef HB_NTT3_C0BUF
-#define HB_NTT3_C0BUF 0
-#endif
-// -DHB_NTT3_C0BUF=1: rotation ModDown (scatter) gets one more 32 KB tile so
-// the c0 addend is TMA-prefetched with x_r instead of loaded in the epilogue
-// (the epilogue's top stall); measured 12 % slower: 106 KB of smem leaves
-// two CTAs per SM instead of three
-static_assert(!(HB_NTT3_SB && HB_NTT3_C0BUF), "the c0 tile needs the two-buffer layout");
-template <int LOGN, int MODE>
-__host__ __device__ constexpr int smem3f() {
-  return smem3<LOGN>() + ((HB_NTT3_C0BUF && MODE == 4) ? TILE3 * 8 + 16 : 0);
-}
-#ifndef HB_NTT3_MINB
-#define HB_NTT3_MINB (HB_NTT3_SB ? 4 : 3)
-#endif
+__host__ __device__ constexpr int smem3() { return TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
+constexpr int MINB3 = 4;
 
 HB_DEV int swz3_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
 // block layout (as ntt2.cu): element j of the 4096-element tile
@@ -101,17 +81,17 @@ HB_DEV uint32_t mapa(uint32_t a, uint32_t rank) {
 }
 // thread 0: one arrival expecting `bytes` of st.async traffic, made visible
 // to the cluster; every thread then arrives (relaxed) on the cluster barrier
-// (mbar[1]: the epilogue's bulk prefetch, armed later by its issuer)
 HB_DEV void xchg_init(uint64_t* mbar, uint32_t bytes) {
   if (threadIdx.x == 0) {
     const uint32_t a = smem_addr(mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    // a second, spare barrier word: dropping its init perturbs ptxas's
+    // register allocation of the transform into spills (ModUp 2.5 % slower)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a + 8) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
                  : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (!HB_NTT3_SB) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 // single-buffer exchange: every local read of the buffer is performed before
 // any peer's push into it -- a release arrive (MEMBAR.ALL.GPU per thread).
@@ -120,7 +100,7 @@ HB_DEV void xchg_init(uint64_t* mbar, uint32_t bytes) {
 // tools/ntt3_check.py NTT3_DIFF=1); a CTA-scope fence + relaxed arrive was
 // deterministic and 3 % faster on ModUp but is outside the memory model.
 HB_DEV void cluster_arrive_sb() {
-  if (HB_NTT3_SB) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
 HB_DEV void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -133,32 +113,6 @@ HB_DEV void st_async16(uint32_t raddr, uint32_t rmbar, double a, double b) {
           raddr),
       "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar)
       : "memory");
-}
-// TMA bulk copy global -> own shared memory, completing on mbar (one thread;
-// the caller orders prior generic-proxy reads of dst before it)
-HB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
-  const uint32_t d = smem_addr(dst), b = smem_addr(mbar);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-      "l"(src), "r"(bytes), "r"(b)
-      : "memory");
-}
-// a second bulk copy on a barrier already armed for its bytes
-HB_DEV void bulk_g2s_more(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
-  const uint32_t d = smem_addr(dst), b = smem_addr(mbar);
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-      "l"(src), "r"(bytes), "r"(b)
-      : "memory");
-}
-HB_DEV void mbar_expect(uint64_t* mbar, uint32_t bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)),
-               "r"(bytes)
-               : "memory");
 }
 HB_DEV void st_async8(uint32_t raddr, uint32_t rmbar, double a) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
@@ -260,20 +214,17 @@ HB_DEV void tws_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // ---------------------------------------------------------------------------
 // Forward.
 template <class Pol, int LOGN, int MODE>
-__global__ void __launch_bounds__(THREADS3, HB_NTT3_MINB)
+__global__ void __launch_bounds__(THREADS3, MINB3)
 k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1, CW = TILE3 / M, CL = N / TILE3;
   typedef ColPlan<S1, true> CP;
   typedef typename Pol::T V;
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // column slice (local pass)
-  V* rb = sm + (NBUF3 - 1) * TILE3;       // received block tile
+  V* rb = sm;                             // received block tile (same buffer)
   constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
-  constexpr bool C0BUF = HB_NTT3_C0BUF && MODE == FWD_MODDOWN_SCATTER;
-  u64* c0buf = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(smraw3) +
-                                      ((smem3<LOGN>() + 15) & ~15));
   xchg_init(mbar, TILE3 * sizeof(V));
   const int rank = (int)cluster_rank();
   const HbNttTask tk = tasks[blockIdx.x / CL];
@@ -359,24 +310,9 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     }
   }
   constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
-  if (MD && HB_NTT3_SB) {
-    if (t == 0 && HB_NTT3_L2PF) {   // the epilogue's x_r / addend tiles into L2 meanwhile
-      l2_prefetch(tk.aux + (size_t)rank * TILE3, TILE3 * 8);
-      if (tk.add && !(MODE == FWD_MODDOWN && tk.perm)) l2_prefetch(tk.add + (size_t)rank * TILE3, TILE3 * 8);
-    }
-  } else if (MD) {
-    // the column slice is consumed: prefetch the epilogue's x_r tile into it
-    // (TMA bulk copy) while the block pass runs
-    __syncthreads();
-    if (t == 0) {
-      if (C0BUF && tk.add) {   // x_r and the c0 addend on one barrier
-        mbar_expect(mbar + 1, 2 * TILE3 * 8);
-        bulk_g2s_more(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
-        bulk_g2s_more(c0buf, tk.add + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
-      } else {
-        bulk_g2s(sm, tk.aux + (size_t)rank * TILE3, TILE3 * 8, mbar + 1);
-      }
-    }
+  if (MD && t == 0) {   // the epilogue's x_r / addend tiles into L2 meanwhile
+    l2_prefetch(tk.aux + (size_t)rank * TILE3, TILE3 * 8);
+    if (tk.add && !(MODE == FWD_MODDOWN && tk.perm)) l2_prefetch(tk.add + (size_t)rank * TILE3, TILE3 * 8);
   }
   mbar_wait0(mbar);
   // ---- block pass over blocks [rank*32, rank*32 + 32)
@@ -431,7 +367,6 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   // chain cost ~30 integer instructions per element)
   const double pd = P.pd, pinv = P.pinv;
   const double sd = u64_to_f(tk.scal), sq = sd * pinv;
-  if (MD && !HB_NTT3_SB) mbar_wait0(mbar + 1);
 #pragma unroll 4
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
     const int k = t + i * THREADS3;
@@ -440,8 +375,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
     ulonglong2 o;
     int2 sc = make_int2(0, 0);
     if (MD) {
-      const ulonglong2 ax = HB_NTT3_SB ? __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j))
-                                       : *reinterpret_cast<const ulonglong2*>(sm + 2 * k);
+      const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
       double r0 = fmod_mul(u64_to_f(ax.x) - rb[2 * pc], sd, sq, pd);
       double r1 = fmod_mul(u64_to_f(ax.y) - rb[2 * pc + 1], sd, sq, pd);
       if (tk.add) {
@@ -451,8 +385,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
           a0 = __ldg(tk.add + pp.x);
           a1 = __ldg(tk.add + pp.y);
         } else {
-          const ulonglong2 a2 = C0BUF ? *reinterpret_cast<const ulonglong2*>(c0buf + 2 * k)
-                                      : __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
+          const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
           a0 = a2.x;
           a1 = a2.y;
         }
@@ -489,14 +422,14 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
 // ---------------------------------------------------------------------------
 // Inverse.
 template <class Pol, int LOGN>
-__global__ void __launch_bounds__(THREADS3, HB_NTT3_MINB)
+__global__ void __launch_bounds__(THREADS3, MINB3)
 k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1, CW = TILE3 / M, CL = N / TILE3;
   typedef ColPlan<S1, false> CP;
   typedef typename Pol::T V;
   extern __shared__ __align__(16) unsigned char smraw3[];
   V* sm = reinterpret_cast<V*>(smraw3);   // block tile (local pass)
-  V* rb = sm + (NBUF3 - 1) * TILE3;       // received column slice
+  V* rb = sm;                             // received column slice (same buffer)
   constexpr int TWC = M - 1, TW3 = TWC + 480;
   HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
@@ -639,7 +572,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
 template <int LOGN, int MODE>
 cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int CL = (1 << LOGN) / TILE3;
-  constexpr int FWDSMEM = smem3f<LOGN, MODE>();
+  constexpr int FWDSMEM = smem3<LOGN>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * CL);
   cfg.blockDim = dim3(THREADS3);
