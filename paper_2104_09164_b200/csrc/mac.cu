@@ -55,16 +55,9 @@ HB_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memor
 
 
 // Operand conversion of the GEMM: the magic-number path (LOP + DADD on the
-// fp64 pipe) by default; -DHB_MAC_I2F moves it to the conversion pipe
-// (I2F.F64.U64), which is otherwise idle here: bit-identical, measured 0.4 %
-// slower on the bench step (profiles/r01_knob_ab.txt), so off.
-HB_DEV double mac_to_f(u64 x) {
-#ifdef HB_MAC_I2F
-  return __ull2double_rn(x);
-#else
-  return u64_to_f(x);
-#endif
-}
+// fp64 pipe).  Round 1 measured the conversion pipe (I2F.F64.U64) instead:
+// bit-identical, 0.4 % slower on the bench step.
+HB_DEV double mac_to_f(u64 x) { return u64_to_f(x); }
 
 template <int TO, int TB, int WO, int WB, int S>
 __global__ void __launch_bounds__(256)
