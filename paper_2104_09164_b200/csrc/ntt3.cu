@@ -58,6 +58,9 @@ constexpr int THREADS3 = 256;
 template <int LOGN>
 __host__ __device__ constexpr int smem3() { return TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
 constexpr int MINB3 = 4;
+#ifndef HB_NTT3_MAXLOGN
+#define HB_NTT3_MAXLOGN 15
+#endif
 
 HB_DEV int swz3_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
 // block layout (as ntt2.cu): element j of the 4096-element tile
@@ -569,6 +572,12 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   }
 }
 
+// Clusters above the portable 8 CTAs (N = 2^16: 16 CTAs) need the opt-in.
+inline cudaError_t cluster16_once(const void* fn, int cl) {
+  if (cl <= 8) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
 template <int LOGN, int MODE>
 cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int CL = (1 << LOGN) / TILE3;
@@ -589,6 +598,7 @@ cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.numAttrs = g_hb_pdl ? 2 : 1;
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, (int)(FWDSMEM), &smem_cur);
+  if (e == cudaSuccess) e = cluster16_once((const void*)k_ntt3_fwd<PolF64, LOGN, MODE>, CL);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_fwd<PolF64, LOGN, MODE>, tasks, R);
 }
@@ -612,6 +622,7 @@ cudaError_t inv3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStrea
   cfg.numAttrs = g_hb_pdl ? 2 : 1;
   static int smem_cur = 0;
   cudaError_t e = smem_attr_once((const void*)k_ntt3_inv<PolF64, LOGN>, (int)(smem3<LOGN>()), &smem_cur);
+  if (e == cudaSuccess) e = cluster16_once((const void*)k_ntt3_inv<PolF64, LOGN>, CL);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k_ntt3_inv<PolF64, LOGN>, tasks, R);
 }
@@ -644,7 +655,7 @@ bool ntt3_supported(const HbRing& R) {
   // two-pass kernels and config 2 252 -> 320 inferences/s (round 2,
   // tools/ab_ntt3_15.sh; the round-1 two-buffer layout, 77 KB per CTA, had
   // measured 5-20 % slower)
-  return !off && R.use_f64 && R.logn >= 13 && R.logn <= 15;
+  return !off && R.use_f64 && R.logn >= 13 && R.logn <= HB_NTT3_MAXLOGN;
 }
 
 cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, int mode,
@@ -654,6 +665,9 @@ cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, 
     case 13: return fwd3_mode<13>(tasks, count, R, mode, st);
     case 14: return fwd3_mode<14>(tasks, count, R, mode, st);
     case 15: return fwd3_mode<15>(tasks, count, R, mode, st);
+#if HB_NTT3_MAXLOGN >= 16
+    case 16: return fwd3_mode<16>(tasks, count, R, mode, st);
+#endif
     default: return cudaErrorInvalidValue;
   }
 }
@@ -664,6 +678,9 @@ cudaError_t launch_ntt3_inv(const HbNttTask* tasks, int count, const HbRing& R, 
     case 13: return inv3_t<13>(tasks, count, R, st);
     case 14: return inv3_t<14>(tasks, count, R, st);
     case 15: return inv3_t<15>(tasks, count, R, st);
+#if HB_NTT3_MAXLOGN >= 16
+    case 16: return inv3_t<16>(tasks, count, R, st);
+#endif
     default: return cudaErrorInvalidValue;
   }
 }
