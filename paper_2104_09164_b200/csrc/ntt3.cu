@@ -1,4 +1,4 @@
-// Cluster-fused negacyclic NTT (default for fp64 rings at N = 2^13 .. 2^15).
+// Cluster-fused negacyclic NTT (default for fp64 rings at N = 2^13 .. 2^16).
 //
 // Same transform and fused modes as ntt2.cu (hear/ckks/ring.py:71-124, true
 // inverse), same split of the stages into a column pass (stages 0..S1-1 over
@@ -58,8 +58,12 @@ constexpr int THREADS3 = 256;
 template <int LOGN>
 __host__ __device__ constexpr int smem3() { return TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
 constexpr int MINB3 = 4;
+// N = 2^16 runs 16-CTA clusters (non-portable size): per launch within
+// -6..+1 % of the two-pass kernels, but the pipeline then takes the
+// lift-once / ModDown-scatter path -- config 3 178 -> 201 inferences/s
+// (tools/ab_ntt3_16.sh)
 #ifndef HB_NTT3_MAXLOGN
-#define HB_NTT3_MAXLOGN 15
+#define HB_NTT3_MAXLOGN 16
 #endif
 
 HB_DEV int swz3_chunk(int c) { return c ^ ((c >> 3) & 7) ^ (((c >> 6) & 1) << 2); }
@@ -642,7 +646,7 @@ cudaError_t fwd3_mode(const HbNttTask* tasks, int count, const HbRing& R, int mo
 
 }  // namespace
 
-// fp64 rings at N = 2^13 / 2^14 / 2^15 (clusters of 2 / 4 / 8 CTAs); HEAR_B200_NTT3=0
+// fp64 rings at N = 2^13 .. 2^16 (clusters of 2 / 4 / 8 / 16 CTAs); HEAR_B200_NTT3=0
 // falls back to the two-pass kernels.
 bool ntt3_supported(const HbRing& R) {
   static int off = -1;
