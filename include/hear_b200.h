@@ -143,6 +143,25 @@ int hb_mac_shared(hb_ring* ring, const void* cts, const void* pts, const void* d
 int hb_ks_gemm(hb_ring* ring, const void* de, const void* keys, const void* keys_last,
                const void* dsts, int ndig, int nout, int rows, int bc, long long de_bstride,
                long long dst_bstride, int prime_last, int de_per_job, void* stream);
+/* Hoisted rotations left in the extended basis Q*P (ModDown deferred past the
+ * plaintext products, Σ_j pt_j * rot_j(ct) with ONE ModDown per output; the
+ * reference divides P out after every rotation, engine.py:305-351): the
+ * hb_ks_gemm inner product on pre-permuted keys with output o (job x
+ * component) stored through its scatter map scat[o] (int32 [N], the inverse
+ * Galois map) and, on chain rows r < rows-1 for the outputs with c0s[o] != 0
+ * (the b components), plus pmod[r] * c0[b*c0_bstride + r*N + j]  (c0: the
+ * rotated handle's c0 block, pmod[r] = P mod q_r):
+ *   dsts[o][b*dst_bstride + r*N + scat[o][j]] = <digits, key>[j] + P*c0[j].   */
+int hb_ks_gemm_rot(hb_ring* ring, const void* de, const void* keys, const void* keys_last,
+                   const void* dsts, const void* scat, const void* c0s, const void* c0,
+                   const void* pmod, int ndig, int nout, int rows, int bc, long long de_bstride,
+                   long long dst_bstride, long long c0_bstride, int prime_last, void* stream);
+/* hb_mac_shared over extended-basis blocks [bc, rows, N] whose last row is
+ * the special prime prime_last: plaintext special rows come from pts_last
+ * (pointers to the rows themselves, [nout*nterms]).                          */
+int hb_mac_shared_ext(hb_ring* ring, const void* cts, const void* pts, const void* pts_last,
+                      const void* dsts, int nterms, int nout, int rows, int bc, int prime_last,
+                      void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);

@@ -48,6 +48,8 @@ def lib():
         L.hb_set_pdl.argtypes = [i32]
         L.hb_ks_gemm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_longlong,
                                  ctypes.c_longlong, i32, i32, vp]
+        L.hb_ks_gemm_rot.argtypes = [vp] * 9 + [i32] * 4 + [ctypes.c_longlong] * 3 + [i32, vp]
+        L.hb_mac_shared_ext.argtypes = [vp] * 5 + [i32] * 5 + [vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]

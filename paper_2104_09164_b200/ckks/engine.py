@@ -68,6 +68,23 @@ class CtData:
         return h[:, 0].copy(), h[:, 1].copy()
 
 
+class CtExt:
+    """Rotated ciphertext left in the extended basis Q*P (ModDown deferred):
+    [B, 2, level+2, N], special row last.  Produced by
+    rot_many_each(lazy=True) and consumed only by mac_many, which divides P
+    out once per accumulated output; it has no `.data`, so every other op
+    fails loudly."""
+
+    __slots__ = ("xdata",)
+
+    def __init__(self, xdata: torch.Tensor):
+        self.xdata = xdata
+
+    @property
+    def batch(self) -> int:
+        return self.xdata.shape[0]
+
+
 class _Ksk:
     __slots__ = ("b", "a", "lmax", "bp", "ap")
 
@@ -169,6 +186,18 @@ class CkksBackend(BackendBase):
         # rescale write centred lifts as doubles (task scal = 1) and the
         # forward transforms read them with src_prime = -1: one lift per row
         self.lift_once = bool(nat.lib().hb_ntt_fused_ks(self.ring.handle))
+        # lazy ModDown ("double hoisting"): hoisted rotations that only feed
+        # plaintext accumulations (conv layers, strategy "full") stay in the
+        # extended basis Q*P -- the inner-product GEMM scatters them through
+        # the Galois map and adds P*c0 -- the layer MAC runs over level+2 rows
+        # (plaintexts carry their special-prime row) and P is divided out once
+        # per output: conv2/conv3 of 1d-w64 need 8/16 ModDowns instead of 94.
+        # Primitives stay bit-exact; a lazy layer differs from the reference's
+        # ciphertext by rounding noise only (one ModDown rounding instead of
+        # one per rotation).  HEAR_B200_LAZY_MODDOWN=0 restores the eager path.
+        self.lazy = (os.environ.get("HEAR_B200_LAZY_MODDOWN", "1") == "1" and self.ring.use_f64
+                     and self.preperm and self.lift_once)
+        self._pmod_dev = self._dev(self._pmod)
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -346,8 +375,10 @@ class CkksBackend(BackendBase):
     # ------------------------------------------------------------------ codec
 
     def _encode_rows(self, values: torch.Tensor, level: int, scale) -> torch.Tensor:
+        """[M, level+1, N] plaintext rows; with lazy ModDown one more row, the
+        residues under the special prime (extended-basis accumulations)."""
         coeffs = self.emb.encode_coeffs(values, float(scale))
-        return self._coeffs_to_ntt(coeffs, list(range(level + 1)))
+        return self._coeffs_to_ntt(coeffs, list(range(level + 1)) + ([self.S] if self.lazy else []))
 
     def _raw_encode(self, values, level, scale) -> Pt:
         rows = self._encode_rows(torch.as_tensor(values, dtype=torch.float64)[None], level, scale)
@@ -765,7 +796,7 @@ class CkksBackend(BackendBase):
                                  primes=np.tile(np.arange(r), bsz * 2))
         return res
 
-    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs):
+    def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs, rot=None):
         """Natural-order key-switch inner products of several jobs as one
         per-coefficient GEMM (csrc/mac.cu launch_ks_gemm): terms = digits,
         outputs = (job, component), the special row (its own prime and key
@@ -789,7 +820,7 @@ class CkksBackend(BackendBase):
         else:
             dep = np.stack([der[o, :, 0] for o in offs])   # [njobs, ndig]
         self.ring.ks_gemm(dep, kp, kps, dp, rows, bsz, ndig * rows * self.n,
-                          2 * rows * self.n, self.S)
+                          2 * rows * self.n, self.S, rot=rot)
 
     def _rot_key(self, amount: int) -> _Ksk:
         key = self.keys.rot.get(amount % self.n2)
@@ -826,6 +857,8 @@ class CkksBackend(BackendBase):
         """Groups of outputs that share one ciphertext term list (conv partial
         sums, FC diagonals) go through the shared-term kernel; the rest
         through the generic strided MAC."""
+        if isinstance(jobs[0][0][0].payload, CtExt):
+            return self._raw_mac_many_ext(jobs)
         out = [None] * len(jobs)
         groups: dict = {}
         for i, terms in enumerate(jobs):
@@ -851,6 +884,66 @@ class CkksBackend(BackendBase):
             for i, c in zip(rest, sub):
                 out[i] = c
         return out
+
+    def _raw_mac_many_ext(self, jobs) -> list:
+        """Accumulations over extended-basis rotations (lazy ModDown): the
+        shared-term GEMM over level+2 rows, then ONE ModDown per output."""
+        out = [None] * len(jobs)
+        for lvl, idx, acc in self._mac_ext(jobs):
+            bsz = acc.shape[1]
+            res = self._mod_down_ext(acc.reshape(len(idx) * bsz, 2, lvl + 2, self.n), lvl)
+            res = res.reshape(len(idx), bsz, 2, lvl + 1, self.n)
+            for q, i in enumerate(idx):
+                t0 = jobs[i][0]
+                out[i] = Ct(CtData(res[q]), lvl, t0[0].scale * t0[1].scale, self.n2)
+        return out
+
+    def _mac_ext(self, jobs) -> list:
+        """[(level, job indices, acc [len, B, 2, level+2, N])]: the products
+        summed modulo every chain prime and the special prime, per group of
+        jobs sharing one term list."""
+        groups: dict = {}
+        for i, terms in enumerate(jobs):
+            for ct, pt in terms:
+                if not isinstance(ct.payload, CtExt):
+                    raise LevelScaleError("extended-basis and plain handles mixed in one sum")
+                if pt.payload.shape[0] != pt.level + 2:
+                    raise LevelScaleError("plaintext lacks its special-prime row")
+            key = (terms[0][0].level, tuple(ct.payload.xdata.data_ptr() for ct, _ in terms))
+            groups.setdefault(key, []).append(i)
+        row8 = 8 * self.n
+        res = []
+        for (lvl, ctkey), idx in groups.items():
+            bsz = jobs[idx[0]][0][0].payload.batch
+            rows = lvl + 2
+            acc = self.ring.empty(len(idx), bsz, 2, rows)
+            dsts = self.ring.row_ptrs(acc).reshape(len(idx), -1)[:, 0]
+            pts = np.array([[pt.payload.data_ptr() for _, pt in jobs[i]] for i in idx],
+                           dtype=np.uint64)
+            last = np.array([[pt.payload.data_ptr() + (pt.level + 1) * row8 for _, pt in jobs[i]]
+                             for i in idx], dtype=np.uint64)
+            self.ring.mac_shared(np.array(ctkey, dtype=np.uint64), pts, dsts, rows, 2 * bsz,
+                                 pts_last=last, prime_last=self.S)
+            res.append((lvl, idx, acc))
+        return res
+
+    def _mod_down_ext(self, ext: torch.Tensor, level: int) -> torch.Tensor:
+        """ext [M, 2, level+2, N] -> (x - [x]_P)/P on the chain rows
+        [M, 2, level+1, N] (engine.py:213-227), the key switch's ModDown."""
+        m, r = ext.shape[0] * 2, level + 1
+        rows = self.ring.row_ptrs(ext).reshape(m, level + 2)
+        spc = self.ring.empty(m)
+        sp = np.full(m, self.S)
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=rows[:, level + 1], dst=self.ring.row_ptrs(spc),
+                                 dst_prime=sp, src_prime=sp, scal=int(self.lift_once)))
+        out = self.ring.empty(m, r)
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * r, src=np.repeat(self.ring.row_ptrs(spc), r),
+                                 dst=self.ring.row_ptrs(out), aux=rows[:, :r].ravel(),
+                                 src_prime=-1 if self.lift_once else self.S,
+                                 dst_prime=np.tile(np.arange(r), m),
+                                 scal=np.tile(self._pinv[:r], m),
+                                 scal_sh=np.tile(self._pinv_sh[:r], m)), nat.FWD_MODDOWN)
+        return out.reshape(m // 2, 2, r, self.n)
 
     def _raw_mac_strided(self, jobs) -> list:
         out = [None] * len(jobs)
@@ -1056,6 +1149,61 @@ class CkksBackend(BackendBase):
             del de
             for i in idx:
                 out[i] = res[i]
+        return out
+
+    def _lazy_ok(self, cts) -> bool:
+        lvl, bsz = cts[0].level, cts[0].payload.batch
+        return (self.lazy and bsz >= self.ks_gemm_min
+                and all(c.level == lvl and c.payload.batch == bsz for c in cts))
+
+    def _raw_rot_many_each_lazy(self, cts, ks, want0: bool) -> list:
+        """Hoisted rotations left in the extended basis Q*P: one ModUp over
+        every handle, one inner-product GEMM per handle whose epilogue
+        scatters each rotation through its Galois map and adds P*c0
+        (hb_ks_gemm_rot) -- no ModDown.  Returns {amount: Ct(CtExt)} per
+        handle (amount 0: P*ct with a zero special row when asked for)."""
+        lvl, bsz = cts[0].level, cts[0].payload.batch
+        r, rows, ndig = lvl + 1, lvl + 2, lvl + 1
+        nh, nk = len(cts), len(ks)
+        rp = self.ring.row_ptrs
+        ctr = np.stack([rp(c.payload.data).reshape(bsz, 2, r) for c in cts])   # [nh, bsz, 2, r]
+        out = [{} for _ in cts]
+        if want0:
+            x0 = self.ring.empty(nh, bsz, 2, rows)
+            z = np.uint64(self._zero_row().data_ptr())
+            b = np.full((nh, bsz, 2, rows), z, dtype=np.uint64)
+            b[..., :r] = ctr
+            m = nh * bsz * 2
+            zero1 = np.zeros(1, dtype=np.uint64)
+            self._ew(nat.EW_ADD_SCALED, rp(x0), np.full(m * rows, z, dtype=np.uint64), b.ravel(),
+                     primes=np.tile(np.array(list(range(r)) + [self.S]), m),
+                     scal=np.tile(np.concatenate([self._pmod[:r], zero1]), m),
+                     scal_sh=np.tile(np.concatenate([self._pmod_sh[:r], zero1]), m))
+            for h, c in enumerate(cts):
+                out[h][0] = Ct(CtExt(x0[h]), lvl, c.scale, self.n2)
+        de = self._decompose(ctr[:, :, 1].reshape(nh * bsz, r), lvl)
+        der = rp(de).reshape(nh * bsz, ndig, rows)
+        xr = self.ring.empty(nh, nk, bsz, 2, rows)
+        xrr = rp(xr).reshape(nh, nk, bsz, 2, rows)
+        keys, scat = [], []
+        for k in ks:
+            key = self._rot_key(k)
+            if key.lmax < lvl:
+                raise LevelScaleError(f"key switching key trimmed to level {key.lmax}, need {lvl}")
+            if key.bp is None:
+                self._permute_key(k % self.n2)
+            keys.append((key.bp, key.ap, key.lmax))
+            inv = self.ring.perm_inv_dev(self.ring.galois_element(k)).data_ptr()
+            scat += [inv, inv]
+        for h in range(nh):
+            c0s = np.zeros(2 * nk, dtype=np.uint64)
+            c0s[0::2] = ctr[h, 0, 0, 0]
+            self._ks_gemm(der, lvl, keys, xrr[h], bsz, [h * bsz] * nk,
+                          rot=(scat, c0s, 2 * r * self.n, self._pmod_dev.data_ptr()))
+        del de
+        for h, c in enumerate(cts):
+            for q, k in enumerate(ks):
+                out[h][k] = Ct(CtExt(xr[h, q]), lvl, c.scale, self.n2)
         return out
 
     def _raw_rot_many(self, a: Ct, ks) -> dict:

@@ -357,17 +357,27 @@ class RingContext:
                 _STATS.add("tensor", (rd + 3 * len(tasks)) * 8 * self.n,
                            4 * len(tasks) * self.n * StepStats.FP64_PER_MODMUL)
 
-    def mac_shared(self, cts: np.ndarray, pts: np.ndarray, dsts: np.ndarray, rows: int, bc: int):
-        """Shared-term MAC: dsts[o] = sum_t pts[o, t] * cts[t] over [bc, rows, N] blocks."""
+    def mac_shared(self, cts: np.ndarray, pts: np.ndarray, dsts: np.ndarray, rows: int, bc: int,
+                   pts_last: np.ndarray | None = None, prime_last: int = 0):
+        """Shared-term MAC: dsts[o] = sum_t pts[o, t] * cts[t] over [bc, rows, N] blocks.
+        pts_last: extended-basis blocks -- the last row is the special prime's,
+        its plaintext rows given by pointer ([nout, nterms])."""
         nout, nterms = pts.shape
         if nout:
-            buf = _upload(np.concatenate([cts.ravel(), pts.ravel(), dsts.ravel()])
-                          .astype(np.uint64), self.device)
+            parts = [cts.ravel(), pts.ravel(), dsts.ravel()]
+            if pts_last is not None:
+                parts.append(pts_last.ravel())
+            buf = _upload(np.concatenate(parts).astype(np.uint64), self.device)
             base = _ptr(buf)
+            o_pts, o_dst = base + 8 * nterms, base + 8 * (nterms + nout * nterms)
             e0 = _STATS.begin() if _STATS else None
-            nat.check(self._lib.hb_mac_shared(self.handle, base, base + 8 * nterms,
-                                              base + 8 * (nterms + nout * nterms), nterms, nout,
-                                              rows, bc, self.stream), "mac_shared")
+            if pts_last is None:
+                nat.check(self._lib.hb_mac_shared(self.handle, base, o_pts, o_dst, nterms, nout,
+                                                  rows, bc, self.stream), "mac_shared")
+            else:
+                nat.check(self._lib.hb_mac_shared_ext(self.handle, base, o_pts, o_dst + 8 * nout,
+                                                      o_dst, nterms, nout, rows, bc, prime_last,
+                                                      self.stream), "mac_shared_ext")
             if _STATS:   # ct terms [bc, rows, N] once, pt rows once, outputs
                 _STATS.end("layer_mac_gemm", e0)
                 nbytes = (_uniq(cts) * bc + _uniq(pts) + nout * bc) * rows * 8 * self.n
@@ -380,27 +390,43 @@ class RingContext:
         return bool(self._lib.hb_ring_uses_f64(self.handle))
 
     def ks_gemm(self, de: np.ndarray, keys: np.ndarray, keys_last: np.ndarray, dsts: np.ndarray,
-                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int):
+                rows: int, bc: int, de_bstride: int, dst_bstride: int, prime_last: int,
+                rot=None):
         """Natural-order key-switch inner products as one per-coefficient GEMM
         (csrc/mac.cu launch_ks_gemm): de [ndig] shared or [njobs, ndig] per job,
-        keys / keys_last [nout, ndig], dsts [nout]."""
+        keys / keys_last [nout, ndig], dsts [nout].  rot = (scat [nout], c0s
+        [nout], c0_bstride, pmod device pointer): the rotation epilogue
+        (hb_ks_gemm_rot) -- outputs scattered through scat[o] with P * c0 added
+        on the chain rows, i.e. rotated ciphertexts in the extended basis."""
         nout, ndig = keys.shape
         if nout:
             per_job = int(de.ndim == 2)
-            buf = _upload(np.concatenate([de.ravel(), keys.ravel(), keys_last.ravel(),
-                                          dsts.ravel()]).astype(np.uint64), self.device)
+            parts = [de.ravel(), keys.ravel(), keys_last.ravel(), dsts.ravel()]
+            if rot is not None:
+                parts += [np.asarray(rot[0], dtype=np.uint64), np.asarray(rot[1], dtype=np.uint64)]
+            buf = _upload(np.concatenate(parts).astype(np.uint64), self.device)
             base = _ptr(buf)
             o1 = base + 8 * de.size
             o2 = o1 + 8 * keys.size
             o3 = o2 + 8 * keys.size
             e0 = _STATS.begin() if _STATS else None
-            nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
-                                           de_bstride, dst_bstride, prime_last, per_job,
-                                           self.stream), "ks_gemm")
+            if rot is None:
+                nat.check(self._lib.hb_ks_gemm(self.handle, base, o1, o2, o3, ndig, nout, rows, bc,
+                                               de_bstride, dst_bstride, prime_last, per_job,
+                                               self.stream), "ks_gemm")
+            else:
+                o4 = o3 + 8 * nout
+                c0 = int(max(rot[1]))
+                nat.check(self._lib.hb_ks_gemm_rot(self.handle, base, o1, o2, o3, o4, o4 + 8 * nout,
+                                                   c0, rot[3], ndig, nout, rows, bc, de_bstride,
+                                                   dst_bstride, rot[2], prime_last, self.stream),
+                          "ks_gemm_rot")
             if _STATS:   # digit sets [bc, ndig, rows] once, key rows once, outputs
                 _STATS.end("keyswitch_gemm", e0)
                 nbytes = (_uniq(de) * bc * rows + _uniq(keys) * (rows - 1) + _uniq(keys_last)
                           + nout * bc * rows) * 8 * self.n
+                if rot is not None:   # c0 rows once per clip, scatter maps once
+                    nbytes += _uniq(rot[1]) * bc * (rows - 1) * 8 * self.n + _uniq(rot[0]) * 4 * self.n
                 _STATS.add("keyswitch_gemm", nbytes, nout * ndig * bc * rows * self.n
                            * StepStats.FP64_PER_MODMUL)
 

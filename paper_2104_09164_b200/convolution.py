@@ -219,7 +219,9 @@ def hconv(cts: list, weights: ConvWeights, plan: ConvPlan, backend: BackendBase,
         raise ValueError(f"expected {plan.m} input ciphertexts, got {len(cts)}")
     n2 = backend.n2
     taps, blocks = plan.tap_amounts, plan.block_amounts
-    pre = backend.rot_many_each(cts, plan.pre_amounts())
+    # "full": the rotated inputs only feed the accumulations below, so the
+    # engine may defer their ModDown past the plaintext products
+    pre = backend.rot_many_each(cts, plan.pre_amounts(), lazy=plan.strategy == "full")
     if j_chunk is None:
         j_chunk = plan.n_o
     outs = []

@@ -38,10 +38,12 @@ cudaError_t launch_mac_gemm_f64(const void*, const void*, const void*, int, int,
                                 int, int, int, cudaStream_t);
 cudaError_t launch_ks_inner2_f64(const void*, int, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_mac_pipe(const void*, const void*, const void*, int, int, const HbRing&, int,
-                            int, cudaStream_t);
+                            int, cudaStream_t, const void* pts_last = nullptr, int prime_last = 0);
 cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, int, int,
                            const HbRing&, int, int, long long, long long, int, int,
-                           cudaStream_t);
+                           cudaStream_t, const void* scat = nullptr, const void* c0s = nullptr,
+                           const void* c0 = nullptr, long long c0_bstride = 0,
+                           const void* pmod = nullptr);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_bconv(const void*, int, int, const HbPrime*, int, cudaStream_t);
 int bconv_task_size();
@@ -326,6 +328,28 @@ int hb_ks_gemm(hb_ring* r, const void* de, const void* keys, const void* keys_la
                                  de_bstride, dst_bstride, prime_last, de_per_job,
                                  (cudaStream_t)stream);
   return e ? fail(e, "hb_ks_gemm") : 0;
+}
+
+// Extended-basis (Q*P) forms of the two GEMMs, for hoisted rotations whose
+// ModDown is deferred past the plaintext products (lazy ModDown).
+int hb_mac_shared_ext(hb_ring* r, const void* cts, const void* pts, const void* pts_last,
+                      const void* dsts, int nterms, int nout, int rows, int bc, int prime_last,
+                      void* stream) {
+  if (!r->dev.use_f64) return fail(cudaErrorNotSupported, "hb_mac_shared_ext: fp64 rings only");
+  cudaError_t e = launch_mac_pipe(cts, pts, dsts, nterms, nout, r->dev, rows, bc,
+                                  (cudaStream_t)stream, pts_last, prime_last);
+  return e ? fail(e, "hb_mac_shared_ext") : 0;
+}
+
+int hb_ks_gemm_rot(hb_ring* r, const void* de, const void* keys, const void* keys_last,
+                   const void* dsts, const void* scat, const void* c0s, const void* c0,
+                   const void* pmod, int ndig, int nout, int rows, int bc, long long de_bstride,
+                   long long dst_bstride, long long c0_bstride, int prime_last, void* stream) {
+  if (!scat || !c0s || !pmod) return fail(cudaErrorInvalidValue, "hb_ks_gemm_rot: null table");
+  cudaError_t e = launch_ks_gemm(de, keys, keys_last, dsts, ndig, nout, r->dev, rows, bc,
+                                 de_bstride, dst_bstride, prime_last, 0, (cudaStream_t)stream,
+                                 scat, c0s, c0, c0_bstride, pmod);
+  return e ? fail(e, "hb_ks_gemm_rot") : 0;
 }
 
 int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {

@@ -41,9 +41,30 @@ struct HbMacGroupP {
   const u64* const* pts_last;   // ... except the last row when set: its pt rows
   int prime_last;               //     (pointers to the row itself) and prime
   int cts_per_tile;       // cts is [output tile][T] (each tile has its own terms)
+  // Rotation epilogue (EPI kernels only; lazy ModDown, engine.py
+  // _raw_rot_many_each_lazy): output o is stored through its scatter map
+  // scat[o] (the inverse Galois map of its pre-permuted key; null = natural
+  // order) and, on chain rows, gains pmod[r] * c0s[o][b*c0_bstride + r*N + j]
+  // (P times the rotated c0, so the result is the rotated ciphertext in the
+  // extended basis Q*P with no ModDown).
+  const int* const* scat;
+  const u64* const* c0s;   // per output: non-null = takes the c0 term
+  const u64* c0;           // the group's c0 block [BC][c0_bstride] (shared by its rotations)
+  long long c0_bstride;
+  const u64* pmod;
 };
 
 namespace {
+
+// HEAR_B200_MAC_JC: coefficient chunks per CTA (A/B knob; 0 = automatic)
+inline int mac_jc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HEAR_B200_MAC_JC");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
 HB_DEV uint32_t s_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 HB_DEV void cp16(uint32_t dst, const void* src) {
@@ -59,26 +80,35 @@ HB_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memor
 // bit-identical, 0.4 % slower on the bench step.
 HB_DEV double mac_to_f(u64 x) { return u64_to_f(x); }
 
-template <int TO, int TB, int WO, int WB, int S>
+// MULTI = 0: one chunk per CTA with the chunk loop and its bookkeeping
+// compiled out (the long conv-layer term lists: measured 14 % faster there
+// than the general form).
+template <int TO, int TB, int WO, int WB, int S, int EPI = 0, int MULTI = 1>
 __global__ void __launch_bounds__(256)
-k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
+k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
+  const int JC = MULTI ? JCrt : 1;
   HB_PDL_ENTRY();
   constexpr int OB = TO * WO, CB = TB * WB, ROWS = OB + CB;
   constexpr int STAGE = ROWS * 32;            // u64 per stage
   constexpr int CHUNKS = ROWS * 16;           // 16-byte copies per stage
   extern __shared__ __align__(16) u64 smem_mac[];
   u64* stages = smem_mac;                     // [S][ROWS][32]
-  const u64** ptab = reinterpret_cast<const u64**>(smem_mac + S * STAGE);
+  // EPI: scatter indices of the current / next coefficient chunk [2][OB][32]
+  int* scbuf = reinterpret_cast<int*>(smem_mac + S * STAGE);
+  const u64** ptab = reinterpret_cast<const u64**>(smem_mac + S * STAGE + (EPI ? OB * 32 : 0));
   const int T = g.nterms, O = g.nout, n = RG.n;
   const int tid = threadIdx.x + threadIdx.y * 32;
   const int oc = blockIdx.y * OB, bc = blockIdx.x * CB;   // CTA tile origin
-  const int nchunk = n / 32;
+  // a CTA walks JC consecutive 32-coefficient chunks of one RNS row through
+  // ONE copy pipeline: the pointer tables are built once and the next
+  // chunk's operands stream in while this chunk's outputs are stored
+  const int nchunk = n / 32 / JC;
   const int r = blockIdx.z / nchunk;
-  const int j0 = (blockIdx.z % nchunk) * 32;
-  const size_t rj0 = (size_t)r * n + j0;
+  const int jbase = (blockIdx.z % nchunk) * JC * 32;
+  const size_t rn = (size_t)r * n;
   const bool last = g.pts_last != nullptr && r == R - 1;
   const u64* const* pts = last ? g.pts_last : g.pts;
-  const size_t prow = last ? (size_t)j0 : rj0;            // pt offset of this row
+  const size_t prn = last ? 0 : rn;                       // pt offset of this row
   // pointer tables of this CTA's tile: ct bases [T], pt bases [OB][T]
   const u64* const* cts = g.cts + (g.cts_per_tile ? (size_t)blockIdx.y * T : 0);
   for (int i = tid; i < T * (1 + OB); i += 256) {
@@ -90,9 +120,15 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
     }
   }
   __syncthreads();
+  // EPI: the rotated c0 (times P) is one more term of the chain rows -- its
+  // ct rows stream through the pipeline like a digit's, no key operand
+  const bool c0term = EPI && !last && g.c0 != nullptr;
+  const int TT = T + (c0term ? 1 : 0);
+  const int Q = TT * JC;
   // copy plan: chunk c -> stage row c/16 (ct rows first), 16-byte part c%16
-  auto issue = [&](int t) {
-    const uint32_t sb = s_addr(stages + (t % S) * STAGE);
+  auto issue = [&](int q, int ch, int t) {
+    const uint32_t sb = s_addr(stages + (q % S) * STAGE);
+    const size_t j0 = jbase + ch * 32;
 #pragma unroll
     for (int k = 0; k < (CHUNKS + 255) / 256; ++k) {
       const int c = tid + k * 256;
@@ -101,17 +137,42 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
         const u64* src;
         if (row < CB) {
           const int b = bc + row < BC ? bc + row : BC - 1;
-          src = ptab[t] + (size_t)b * g.ct_bstride + rj0 + part * 2;
+          src = (EPI && t == T) ? g.c0 + (size_t)b * g.c0_bstride + rn + j0 + part * 2
+                                : ptab[t] + (size_t)b * g.ct_bstride + rn + j0 + part * 2;
         } else {
-          src = ptab[T + (row - CB) * T + t] + prow + part * 2;
+          if (EPI && t == T) continue;
+          src = ptab[T + (row - CB) * T + t] + prn + j0 + part * 2;
         }
         cp16(sb + (uint32_t)(row * 32 + part * 2) * 8u, src);
       }
     }
+    if (EPI && t == 0) {   // this chunk's scatter indices (4-byte copies)
+      const uint32_t sc0 = s_addr(scbuf + (ch & 1) * OB * 32);
+      for (int c = tid; c < OB * 32; c += 256) {
+        const int o = c >> 5, oo = oc + o < O ? oc + o : O - 1;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sc0 + 4u * c),
+                     "l"(g.scat[oo] + j0 + (c & 31))
+                     : "memory");
+      }
+    }
+  };
+  int iq = 0, ich = 0, it = 0;   // next (q, chunk, term) to issue
+  auto issue_next = [&]() {
+    if (iq < Q) {
+      issue(iq, ich, it);
+      ++iq;
+      if (++it == TT) { it = 0; ++ich; }
+    }
+  };
+  // feed the pipeline while term t of the current chunk is multiplied
+  auto feed = [&](int t) {
+    if (MULTI) issue_next();
+    else if (t + S - 1 < TT) issue(t + S - 1, 0, t + S - 1);
   };
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
-    if (s < T) issue(s);
+    if (MULTI) issue_next();
+    else if (s < TT) issue(s, 0, s);
     cp_commit();
   }
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -119,77 +180,153 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC) {
   const int prime = last ? g.prime_last : g.prime_off + r;
   const HbPrime P = RG.primes[prime];
   const double p = P.pd, pinv = P.pinv;
+  double pm = 0.0, pmq = 0.0;
+  unsigned c0mask = 0;   // outputs of this thread that take the c0 term
+  if (c0term) {
+    pm = u64_to_f(g.pmod[r]);
+    pmq = pm * pinv;
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+      if (oc + os + o < O && g.c0s[oc + os + o] != nullptr) c0mask |= 1u << o;
+  }
   double acc[TO][TB];
 #pragma unroll
   for (int o = 0; o < TO; ++o)
 #pragma unroll
     for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
-  for (int t = 0; t < T; ++t) {
-    cp_wait<S - 2>();
-    __syncthreads();                 // term t landed for every thread; stage t-1 is free
-    if (t + S - 1 < T) issue(t + S - 1);
-    cp_commit();
-    const u64* st = stages + (t % S) * STAGE;
-    double a[TO];
+  const bool full = oc + OB <= O && bc + CB <= BC;
+  int q = 0;
+  for (int ch = 0; ch < JC; ++ch) {
+    for (int t = 0; t < T; ++t, ++q) {
+      cp_wait<S - 2>();
+      __syncthreads();                 // term q landed for every thread; stage q-1 is free
+      feed(t);
+      cp_commit();
+      const u64* st = stages + ((MULTI ? q : t) % S) * STAGE;
+      double a[TO];
 #pragma unroll
-    for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
-    double c[TB];
+      for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
+      double c[TB];
 #pragma unroll
-    for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
+      for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
 #pragma unroll
-    for (int o = 0; o < TO; ++o) {
-      const double aq = a[o] * pinv;
+      for (int o = 0; o < TO; ++o) {
+        const double aq = a[o] * pinv;
 #pragma unroll
-      for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a[o], aq, p);
+        for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a[o], aq, p);
+      }
+      if ((t & 255) == 255) {   // |balanced residue| < p/2: 2^9 terms fit 2^53
+#pragma unroll
+        for (int o = 0; o < TO; ++o)
+#pragma unroll
+          for (int b = 0; b < TB; ++b) acc[o][b] = fmod_reduce(acc[o][b], p, pinv);
+      }
     }
-    if ((t & 255) == 255) {   // |balanced residue| < p/2: 2^9 terms fit 2^53
+    if (EPI && c0term) {               // + P * c0 on the outputs that take it
+      cp_wait<S - 2>();
+      __syncthreads();
+      feed(T);
+      cp_commit();
+      const u64* st = stages + ((MULTI ? q : T) % S) * STAGE;
+      ++q;
+#pragma unroll
+      for (int b = 0; b < TB; ++b) {
+        const double c = mac_to_f(st[(bs + b) * 32 + lane]);
+#pragma unroll
+        for (int o = 0; o < TO; ++o)
+          if ((c0mask >> o) & 1) acc[o][b] += fmod_mul(c, pm, pmq, p);
+      }
+    }
+    // ---- chunk done: store its outputs, restart the accumulators
+    const int j0 = jbase + ch * 32;
+    const size_t rj = rn + j0 + lane;
+    if (EPI) {   // rotated extended-basis outputs, scattered through the Galois map
+      const int* sc = scbuf + (ch & 1) * OB * 32;
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const int oo = oc + os + o;
+        if (oo >= O) continue;
+        u64* d = g.dsts[oo] + rn + sc[(os + o) * 32 + lane];
+#pragma unroll
+        for (int b = 0; b < TB; ++b) {
+          const int bb = bc + bs + b;
+          if (bb >= BC) continue;
+          d[(size_t)bb * g.dst_bstride] = fmod_canon(acc[o][b], p, pinv);
+        }
+      }
+    } else if (full) {   // full tile (the common case): no bounds checks
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        u64* d = g.dsts[oc + os + o] + rj;
+#pragma unroll
+        for (int b = 0; b < TB; ++b)
+          d[(size_t)(bc + bs + b) * g.dst_bstride] = fmod_canon(acc[o][b], p, pinv);
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const int oo = oc + os + o;
+        if (oo >= O) continue;
+        u64* d = g.dsts[oo];
+#pragma unroll
+        for (int b = 0; b < TB; ++b) {
+          const int bb = bc + bs + b;
+          if (bb >= BC) continue;
+          d[(size_t)bb * g.dst_bstride + rj] = fmod_canon(acc[o][b], p, pinv);
+        }
+      }
+    }
+    if (ch + 1 < JC) {
 #pragma unroll
       for (int o = 0; o < TO; ++o)
 #pragma unroll
-        for (int b = 0; b < TB; ++b) acc[o][b] = fmod_reduce(acc[o][b], p, pinv);
+        for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
     }
   }
   cp_wait<0>();
-  const size_t rj = rj0 + lane;
-  auto value = [&](int o, int b) { return fmod_canon(acc[o][b], p, pinv); };
-  if (oc + OB <= O && bc + CB <= BC) {   // full tile (the common case): no bounds checks
-#pragma unroll
-    for (int o = 0; o < TO; ++o) {
-      u64* d = g.dsts[oc + os + o] + rj;
-#pragma unroll
-      for (int b = 0; b < TB; ++b) d[(size_t)(bc + bs + b) * g.dst_bstride] = value(o, b);
-    }
-    return;
-  }
-#pragma unroll
-  for (int o = 0; o < TO; ++o) {
-    const int oo = oc + os + o;
-    if (oo >= O) continue;
-    u64* d = g.dsts[oo];
-#pragma unroll
-    for (int b = 0; b < TB; ++b) {
-      const int bb = bc + bs + b;
-      if (bb >= BC) continue;
-      d[(size_t)bb * g.dst_bstride + rj] = value(o, b);
-    }
-  }
 }
 
-template <int TO, int TB, int WO, int WB, int S>
+template <int TO, int TB, int WO, int WB, int S, int EPI = 0>
 cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cudaStream_t st) {
   constexpr int OB = TO * WO, CB = TB * WB;
-  const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + sizeof(void*) * (size_t)g.nterms * (1 + OB);
+  const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + (EPI ? 2 * OB * 32 * 4 : 0)
+      + sizeof(void*) * (size_t)g.nterms * (1 + OB);
   if (smem > 220 * 1024) return cudaErrorNotSupported;   // caller falls back
-  static int smem_cur = 0;
-  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S>, (int)((int)smem), &smem_cur);
+  static int smem_cur = 0, smem_cur1 = 0;
+  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 1>, (int)((int)smem), &smem_cur);
+  if (e == cudaSuccess)
+    e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 0>, (int)((int)smem), &smem_cur1);
   if (e != cudaSuccess) return e;
   dim3 block(32, 8);
-  dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32));
-  (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S>, dim3(grid), dim3(block), smem, st, g, RG, R, BC);
+  const int tiles = ((BC + CB - 1) / CB) * ((g.nout + OB - 1) / OB) * R;
+  // coefficient chunks per CTA: as many as still leave >= 8 CTAs per SM
+  int jc = mac_jc();
+  if (g.nterms > 32) jc = 1;   // long term lists amortise the prologue already
+  if (jc <= 0) {
+    jc = 8;
+    while (jc > 1 && (long long)tiles * (RG.n / 32 / jc) < 148LL * 8) jc >>= 1;
+  }
+  while (jc > 1 && (RG.n / 32) % jc) jc >>= 1;
+  dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32 / jc));
+  if (jc > 1)
+    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 1>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, jc);
+  else
+    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 0>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, 1);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+// hoisted rotation groups with the scatter / + P*c0 epilogue (shared digits)
+static cudaError_t mac_pipe_dispatch_rot(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
+                                         cudaStream_t st) {
+  constexpr int S = HB_MAC_STAGES;
+  if (BC <= 2) return mac_pipe_t<2, 2, 8, 1, S, 1>(g, RG, rows, BC, st);
+  if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
+  if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
+  if (g.nout <= 8) return mac_pipe_t<8, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
+  return mac_pipe_t<8, 4, 2, 4, S, 1>(g, RG, rows, BC, st);
+}
 
 static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
                                      cudaStream_t st) {
@@ -212,7 +349,8 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
 
 // fp64 rings only (RG.use_f64); returns cudaErrorNotSupported otherwise.
 cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, int nterms, int nout,
-                            const HbRing& RG, int rows, int BC, cudaStream_t st) {
+                            const HbRing& RG, int rows, int BC, cudaStream_t st,
+                            const void* pts_last, int prime_last) {
   if (nout <= 0 || nterms <= 0) return cudaSuccess;
   if (!RG.use_f64) return cudaErrorNotSupported;
   HbMacGroupP g;
@@ -223,9 +361,16 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
   g.nout = nout;
   g.ct_bstride = g.dst_bstride = (long long)rows * RG.n;
   g.prime_off = 0;
-  g.pts_last = nullptr;
-  g.prime_last = 0;
+  // extended-basis layer MAC: the last row is the special prime's, with the
+  // plaintexts' special rows (pts_last: pointers to the rows themselves)
+  g.pts_last = reinterpret_cast<const u64* const*>(pts_last);
+  g.prime_last = prime_last;
   g.cts_per_tile = 0;
+  g.scat = nullptr;
+  g.c0s = nullptr;
+  g.c0 = nullptr;
+  g.c0_bstride = 0;
+  g.pmod = nullptr;
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 
@@ -239,7 +384,8 @@ cudaError_t launch_mac_pipe(const void* cts, const void* pts, const void* dsts, 
 cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_last,
                            const void* dsts, int ndig, int nout, const HbRing& RG, int rows,
                            int BC, long long de_bstride, long long dst_bstride, int prime_last,
-                           int de_per_job, cudaStream_t st) {
+                           int de_per_job, cudaStream_t st, const void* scat, const void* c0s,
+                           const void* c0, long long c0_bstride, const void* pmod) {
   if (nout <= 0 || ndig <= 0) return cudaSuccess;
   if (!RG.use_f64) return cudaErrorNotSupported;
   HbMacGroupP g;
@@ -254,6 +400,15 @@ cudaError_t launch_ks_gemm(const void* de, const void* keys, const void* keys_la
   g.pts_last = reinterpret_cast<const u64* const*>(keys_last);
   g.prime_last = prime_last;
   g.cts_per_tile = de_per_job;
+  g.scat = reinterpret_cast<const int* const*>(scat);
+  g.c0s = reinterpret_cast<const u64* const*>(c0s);
+  g.c0 = reinterpret_cast<const u64*>(c0);
+  g.c0_bstride = c0_bstride;
+  g.pmod = reinterpret_cast<const u64*>(pmod);
+  if (scat) {
+    if (de_per_job) return cudaErrorInvalidValue;
+    return mac_pipe_dispatch_rot(g, RG, rows, BC, st);
+  }
   return mac_pipe_dispatch(g, RG, rows, BC, st);
 }
 

@@ -1,0 +1,148 @@
+"""Lazy ModDown ("double hoisting"): hoisted rotations kept in the extended
+basis Q*P, plaintext products accumulated there, P divided out once.
+
+The reference divides P out after every rotation (hear/ckks/engine.py:
+305-351) and then runs the mult_plain/add chain (hear/convolution.py:
+276-312).  The lazy form must
+  * hold exactly the rotated ciphertext: ModDown of every extended-basis
+    rotation equals the eager rotation bit for bit (the eager one is pinned
+    to the reference's digests in test_gpu_ckks.py);
+  * accumulate exactly: every row of the extended accumulator, the special
+    prime's included, equals the integer sum of products;
+  * decrypt to the eager path's values up to rounding noise, with the same
+    counters, through the conv layer and the whole network.
+"""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mulmod(a, b, p):
+    """a * b mod p on int64 tensors, a, b < p < 2^34 (17-bit split)."""
+    bh, bl = b >> 17, b & ((1 << 17) - 1)
+    return (((a * bh) % p << 17) + a * bl) % p
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import torch
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    be = CkksBackend(gen_params("fast-hear"), seed=11)
+    assert be.lazy
+    lvl, bsz, amounts = 7, 8, [1, 5, 33, 8190]
+    be.ensure_rotation_keys({a: lvl for a in amounts})
+    rng = np.random.default_rng(3)
+    cts = [be.enc(rng.uniform(-1, 1, (bsz, be.n2)), level=lvl) for _ in range(2)]
+    return be, lvl, bsz, amounts, cts, rng, torch
+
+
+def test_extended_rotations_moddown_to_eager_bits(setup):
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    eager = be._raw_rot_many_each(cts, amounts)
+    lazy = be._raw_rot_many_each_lazy(cts, amounts, True)
+    for h, ct in enumerate(cts):
+        for k in amounts:
+            x = lazy[h][k].payload.xdata
+            assert x.shape == (bsz, 2, lvl + 2, be.n)
+            assert torch.equal(be._mod_down_ext(x, lvl), eager[h][k].payload.data), (h, k)
+        # amount 0: P * ct, zero special row
+        x0 = lazy[h][0].payload.xdata
+        assert not x0[:, :, lvl + 1].any()
+        assert torch.equal(be._mod_down_ext(x0, lvl), ct.payload.data)
+
+
+def test_extended_accumulator_is_the_integer_sum(setup):
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    lazy = be._raw_rot_many_each_lazy(cts, amounts, True)
+    terms = [(h, k) for h in range(2) for k in [0] + amounts]
+    nout = 3
+    pts = be.encode_many(rng.uniform(-1, 1, (nout * len(terms), be.n2)), lvl, be.params.msg_scale)
+    jobs = [[(lazy[h][k], pts[o * len(terms) + t]) for t, (h, k) in enumerate(terms)]
+            for o in range(nout)]
+    (glvl, idx, acc), = be._mac_ext(jobs)
+    assert glvl == lvl and idx == list(range(nout))
+    primes = list(be.params.chain_primes[:lvl + 1]) + [be.params.special_prime]
+    for o in range(nout):
+        for r, p in enumerate(primes):
+            want = torch.zeros(bsz, 2, be.n, dtype=torch.int64, device=acc.device)
+            for t, (h, k) in enumerate(terms):
+                pt = pts[o * len(terms) + t].payload[r]
+                want = (want + _mulmod(lazy[h][k].payload.xdata[:, :, r], pt[None, None], p)) % p
+            assert torch.equal(acc[o, :, :, r], want), (o, r)
+
+
+def test_lazy_mac_decrypts_like_eager(setup):
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    ks = [0] + amounts
+    w = rng.uniform(-1, 1, (2 * len(ks), be.n2))
+    pts = be.encode_many(w, lvl, be.params.msg_scale)
+    xs = [be.dec(c) for c in cts]
+    clear = sum(w[h * len(ks) + q] * np.roll(xs[h], -k, axis=1)
+                for h in range(2) for q, k in enumerate(ks))
+
+    def run(lazy):
+        be.reset_counters()
+        pre = be.rot_many_each(cts, ks, lazy=lazy)
+        is_ext = not hasattr(pre[0][ks[1]].payload, "data")
+        assert is_ext == lazy
+        out = be.mac_many([[(pre[h][k], pts[h * len(ks) + q]) for h in range(2)
+                            for q, k in enumerate(ks)]])[0]
+        return be.dec(be.rescale(out)), be.counters.as_dict()
+
+    v_eager, c_eager = run(False)
+    v_lazy, c_lazy = run(True)
+    assert c_lazy == c_eager
+    # both carry the key switch's own noise (~6e-5 at this scale); they differ
+    # by the ModDown roundings (one per rotation eager, one per output lazy)
+    err_e, err_l = np.abs(v_eager - clear).max(), np.abs(v_lazy - clear).max()
+    assert err_e <= 2e-4 and err_l <= 2e-4, (err_e, err_l)
+    assert np.abs(v_lazy - v_eager).max() <= 1e-4
+    assert np.abs(clear).max() > 0.1
+
+
+def test_extended_handles_fail_outside_accumulations(setup):
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    pre = be.rot_many_each(cts[:1], amounts[:1], lazy=True)
+    with pytest.raises(AttributeError):
+        be.add(pre[0][amounts[0]], pre[0][amounts[0]])
+
+
+def test_network_lazy_vs_eager_and_reference():
+    """1d-w64 fast/full at 8 clips: the lazy conv layers give the eager
+    path's logits within 1e-4 of the logit scale, same argmax and counters,
+    and clip 0 matches the reference's CKKS logits (pipeline_golden_r2)."""
+    import json
+    import os
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    from paper_2104_09164_b200.fastpath import compile_pipeline, infer
+    from paper_2104_09164_b200.model import (collapse_layers, make_random_input, make_random_model,
+                                             net_by_name)
+    from paper_2104_09164_b200.modelenc import ModelEncoder
+    here = os.path.dirname(os.path.abspath(__file__))
+    with open(os.path.join(here, "golden", "pipeline_golden_r2.json")) as f:
+        gold = json.load(f)["1d-w64/fast/full/fast-hear"]
+    shape = net_by_name("1d-w64")
+    cpar = collapse_layers(make_random_model(shape, gold["model_seed"]), shape)
+    x = np.stack([make_random_input(shape, gold["input_seed"] + i) for i in range(8)])
+    res = {}
+    for lazy in (False, True):
+        be = CkksBackend(gen_params("fast-hear"), seed=gold["backend_seed"])
+        be.lazy = be.lazy and lazy          # plaintexts keep their special row either way
+        cp = compile_pipeline(shape, "fast", "full", be.params)
+        be.ensure_rotation_keys(cp.rotations)
+        lg, cnt, _ = infer(cpar, x, "fast", "full", be, encoder=ModelEncoder(cp, cpar, be))
+        res[lazy] = (lg, cnt.as_dict())
+    (lg_e, c_e), (lg_l, c_l) = res[False], res[True]
+    assert c_l == c_e == gold["counters"]
+    scale = np.abs(lg_e).max()
+    assert np.abs(lg_l - lg_e).max() <= 1e-4 * scale
+    assert (np.argmax(lg_l, axis=1) == np.argmax(lg_e, axis=1)).all()
+    ref = np.array(gold["logits"])
+    assert np.abs(lg_l[0] - ref).max() <= 1e-3 * np.abs(ref).max()
+    assert int(np.argmax(lg_l[0])) == int(np.argmax(ref))
