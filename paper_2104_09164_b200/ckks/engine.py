@@ -975,6 +975,8 @@ class CkksBackend(BackendBase):
         row read once instead of a pairwise add chain; modular addition, so
         bit-identical to the left-to-right chain."""
         kmax = max(len(g) for g in groups)
+        if any(isinstance(c.payload, CtExt) for g in groups for c in g):
+            return self._raw_sum_each_ext(groups)
         if kmax * max(self.ring.primes) >= 1 << 64:   # 64-bit accumulator headroom
             return super()._raw_sum_each(groups)
         out = [g[0] if len(g) == 1 else None for g in groups]
@@ -996,6 +998,39 @@ class CkksBackend(BackendBase):
                     srcs[q, :, len(g):] = np.uint64(self._zero_row().data_ptr())
             self.ring.sum_rows(rp(res), srcs.reshape(-1, k),
                                np.tile(np.arange(r), len(js) * bsz * 2))
+            for q, j in enumerate(js):
+                out[j] = Ct(CtData(res[q]), lvl, groups[j][0].scale, self.n2)
+        return out
+
+    def _raw_sum_each_ext(self, groups) -> list:
+        """Sums of extended-basis rotations (lazy ModDown, rotate-and-sum):
+        one pass over level+2 rows per group, then ONE ModDown per group
+        instead of one per rotation."""
+        out = [None] * len(groups)
+        for g in groups:
+            if not all(isinstance(c.payload, CtExt) for c in g):
+                raise LevelScaleError("extended-basis and plain handles mixed in one sum")
+        for lvl, js in self._by_level(groups, lambda g: g[0].level).items():
+            bsz = groups[js[0]][0].payload.batch
+            rows = lvl + 2
+            k = max(len(groups[j]) for j in js)
+            if k * max(self.ring.primes) >= 1 << 64:
+                raise LevelScaleError("too many terms for the 64-bit sum")
+            rp = self.ring.row_ptrs
+            acc = self.ring.empty(len(js), bsz, 2, rows)
+            nrow = bsz * 2 * rows
+            srcs = np.zeros((len(js), nrow, k), dtype=np.uint64)
+            for q, j in enumerate(js):
+                g = groups[j]
+                for t, c in enumerate(g):
+                    srcs[q, :, t] = rp(c.payload.xdata)
+                if len(g) < k:
+                    srcs[q, :, len(g):] = np.uint64(self._zero_row().data_ptr())
+            self.ring.sum_rows(rp(acc), srcs.reshape(-1, k),
+                               np.tile(np.array(list(range(lvl + 1)) + [self.S]),
+                                       len(js) * bsz * 2))
+            res = self._mod_down_ext(acc.reshape(len(js) * bsz, 2, rows, self.n), lvl)
+            res = res.reshape(len(js), bsz, 2, lvl + 1, self.n)
             for q, j in enumerate(js):
                 out[j] = Ct(CtData(res[q]), lvl, groups[j][0].scale, self.n2)
         return out

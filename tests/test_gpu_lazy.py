@@ -146,3 +146,33 @@ def test_network_lazy_vs_eager_and_reference():
     ref = np.array(gold["logits"])
     assert np.abs(lg_l[0] - ref).max() <= 1e-3 * np.abs(ref).max()
     assert int(np.argmax(lg_l[0])) == int(np.argmax(ref))
+
+
+def test_lazy_rotate_and_sum(setup):
+    """Sum of hoisted rotations with ONE ModDown (fastpath.rotate_sum_each's odd
+    part): the extended-basis sum is the exact modular sum of its terms, and
+    the result decrypts like the eager sum with the same counters."""
+    from paper_2104_09164_b200.fastpath import rotate_sum_each
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    lazy = be._raw_rot_many_each_lazy(cts, amounts, True)
+    group = [lazy[0][k] for k in [0] + amounts]
+    primes = list(be.params.chain_primes[:lvl + 1]) + [be.params.special_prime]
+    pt = torch.tensor(primes, dtype=torch.int64, device=be.dev)[None, None, :, None]
+    want = sum(c.payload.xdata for c in group) % pt
+    got = be._raw_sum_each([group])[0]
+    assert torch.equal(got.payload.data, be._mod_down_ext(want, lvl))
+    # through the schedule: 5 entries spaced 33 -> odd part 5, one hoisted group
+    be.ensure_rotation_keys({33 * j: lvl for j in range(1, 5)})
+    res = {}
+    for flag in (False, True):
+        be.lazy = flag
+        be.reset_counters()
+        out = rotate_sum_each(cts, 5, 33, be)
+        res[flag] = ([be.dec(c) for c in out], be.counters.as_dict())
+    be.lazy = True
+    assert res[True][1] == res[False][1]
+    xs = [be.dec(c) for c in cts]
+    for h in range(2):
+        clear = sum(np.roll(xs[h], -33 * j, axis=1) for j in range(5))
+        assert np.abs(res[True][0][h] - clear).max() <= 2e-4
+        assert np.abs(res[True][0][h] - res[False][0][h]).max() <= 1e-4
