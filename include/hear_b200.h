@@ -162,6 +162,19 @@ int hb_ks_gemm_rot(hb_ring* ring, const void* de, const void* keys, const void* 
 int hb_mac_shared_ext(hb_ring* ring, const void* cts, const void* pts, const void* pts_last,
                       const void* dsts, int nterms, int nout, int rows, int bc, int prime_last,
                       void* stream);
+/* Fused ModUp + key-switch inner product for non-hoisted key switches
+ * (relinearisation, rot_each, rotate-and-add; engine.py:290-326 digit
+ * expansion + ring.py:136-156 inner product in ONE kernel): one HbKsfTask per
+ * (ciphertext, target row) = {coef, ident, kb, ka, out_b, out_a, key_dstride,
+ * ndig, dst_prime, ident_digit}:
+ *   out_{b,a}[j] = sum_i NTT_dst(lift(coef_i))[j] * k{b,a}[i*key_dstride + j]
+ * where coef_i = coef + i*N holds digit i's centred lift as doubles
+ * (coefficient domain, written by hb_ntt_inv with scal = 1) and digit
+ * ident_digit is taken from the NTT-form row `ident` instead of transformed.
+ * The digit expansion is never written: the transforms run in shared memory
+ * of a thread-block cluster and the running sums live in tensor memory
+ * (csrc/ntt3.cu k_ks3).  fp64 rings with hb_ntt_fused_ks() == 1 only.          */
+int hb_ks_fused(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);

@@ -50,6 +50,7 @@ def lib():
                                  ctypes.c_longlong, i32, i32, vp]
         L.hb_ks_gemm_rot.argtypes = [vp] * 9 + [i32] * 4 + [ctypes.c_longlong] * 3 + [i32, vp]
         L.hb_mac_shared_ext.argtypes = [vp] * 5 + [i32] * 5 + [vp]
+        L.hb_ks_fused.argtypes = [vp, vp, i32, vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
@@ -118,6 +119,11 @@ BCONV_TASK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("dst_off", "<u8"), ("tab
                        ("sprime", "<u8"), ("tprime", "<u8"), ("src_stride", "<i8"),
                        ("s", "<i4"), ("t", "<i4")])
 
+KSF_TASK = np.dtype([("coef", "<u8"), ("ident", "<u8"), ("kb", "<u8"), ("ka", "<u8"),
+                     ("out_b", "<u8"), ("out_a", "<u8"), ("key_dstride", "<i8"),
+                     ("ndig", "<i4"), ("dst_prime", "<i4"), ("ident_digit", "<i4"),
+                     ("_pad", "<i4")])
+
 # NTT fused modes (csrc/ntt.cu FwdMode)
 FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER = 0, 1, 2, 3, 4
 # element-wise ops (csrc/ops.cu EwOp)
@@ -128,7 +134,7 @@ EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PER
 def _check_layouts():
     L = _lib
     for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, None, KS_TASK2,
-                               BCONV_TASK)):
+                               BCONV_TASK, KSF_TASK)):
         if dt is not None and L.hb_sizeof_task(kind) != dt.itemsize:
             raise NativeError(f"task layout {kind} mismatch: C {L.hb_sizeof_task(kind)} "
                               f"vs numpy {dt.itemsize}")

@@ -85,6 +85,23 @@ class CtExt:
         return self.xdata.shape[0]
 
 
+class _Digits:
+    """Digits of a batch of polynomials before their expansion: the centred
+    lifts in the coefficient domain (doubles, [nb, ndig, N]) and the NTT-form
+    input rows they came from (pointers [nb, ndig]).  The fused key switch
+    (csrc/ntt3.cu k_ks3) consumes this directly; `expand` materialises the
+    [nb, ndig, ndig+1, N] expansion of the unfused path."""
+
+    __slots__ = ("coef", "src", "lvl")
+
+    def __init__(self, coef, src, lvl):
+        self.coef, self.src, self.lvl = coef, src, lvl
+
+    @property
+    def shape(self):
+        return (self.coef.shape[0],)
+
+
 class _Ksk:
     __slots__ = ("b", "a", "lmax", "bp", "ap")
 
@@ -198,6 +215,15 @@ class CkksBackend(BackendBase):
         self.lazy = (os.environ.get("HEAR_B200_LAZY_MODDOWN", "1") == "1" and self.ring.use_f64
                      and self.preperm and self.lift_once)
         self._pmod_dev = self._dev(self._pmod)
+        # non-hoisted key switches (relinearisation, rot_each, rotate-and-add)
+        # run ModUp and the inner product in ONE kernel (k_ks3: transforms in
+        # cluster shared memory, sums in tensor memory) once the launch fills
+        # the GPU: the digit expansion is never written.  Bit-identical.
+        # HEAR_B200_KS_FUSED=0 disables; HEAR_B200_KS_FUSED_MIN = smallest
+        # number of (ciphertext, row) tasks that takes the fused kernel.
+        self.fuse_ks = (os.environ.get("HEAR_B200_KS_FUSED", "1") == "1" and self.ring.use_f64
+                        and self.preperm and self.lift_once)
+        self.fuse_ks_min = int(os.environ.get("HEAR_B200_KS_FUSED_MIN", "600"))
         self.keys = KeyMaterial()
         if keygen:
             self._keygen()
@@ -574,7 +600,7 @@ class CkksBackend(BackendBase):
                    d1=dr[:, 1].ravel(), d2=dr[:, 2].ravel(),
                    prime=self._row_primes(bsz, r))
         self.ring.tensor(t)
-        de = self._decompose(dr[:, 2], lvl)
+        de = self._decompose(dr[:, 2], lvl, fused_ok=True)
         out = self._ks_apply_many(de, lvl, [(self.keys.relin, None, dr[:, :2], False)])[0]
         return Ct(CtData(out), lvl, a.scale * b.scale, self.n2)
 
@@ -595,7 +621,7 @@ class CkksBackend(BackendBase):
 
     # ------------------------------------------------------------------ key switching
 
-    def _decompose(self, d, lvl: int):
+    def _decompose(self, d, lvl: int, fused_ok: bool = False):
         """Digits of d extended to chain rows 0..lvl plus the special prime:
         de [B, lvl+1 (digit), lvl+2 (row), N] (engine.py:290-303).
 
@@ -616,6 +642,11 @@ class CkksBackend(BackendBase):
         coef = self.ring.empty(bsz, ndig)
         rp = self.ring.row_ptrs
         prim = self._row_primes(bsz, ndig)
+        if fused_ok and self.fuse_ks and bsz * rows >= self.fuse_ks_min:
+            # the fused key switch transforms the lifts itself
+            self.ring.ntt_inv(_tasks(nat.NTT_TASK, bsz * ndig, src=ptrs.ravel(), dst=rp(coef),
+                                     dst_prime=prim, src_prime=prim, scal=1))
+            return _Digits(coef, ptrs.reshape(bsz, ndig).copy(), lvl)
         de = self.ring.empty(bsz, ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         src = np.repeat(rp(coef), rows)
@@ -648,7 +679,8 @@ class CkksBackend(BackendBase):
         rp = self.ring.row_ptrs
         ip = self.ring.empty(nj * bsz * 2, rows)
         ipr = rp(ip).reshape(nj, bsz, 2, rows)
-        der = rp(de).reshape(de.shape[0], ndig, rows)
+        fused = isinstance(de, _Digits)
+        der = None if fused else rp(de).reshape(de.shape[0], ndig, rows)
         gidx = np.array(list(range(lvl + 1)) + [self.S])
         parts = []
         add = np.zeros((nj, bsz, 2, lvl + 1), dtype=np.uint64)
@@ -665,13 +697,18 @@ class CkksBackend(BackendBase):
             kb_t, ka_t = (key.bp, key.ap) if prepermuted else (key.b, key.a)
             kbr = rp(kb_t).reshape(kb_t.shape[0], key.lmax + 2)[0, krow]
             kar = rp(ka_t).reshape(ka_t.shape[0], key.lmax + 2)[0, krow]
-            parts.append(_tasks(
-                nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
-                out_a=ipr[j, 0, 1],
-                perm=perm.data_ptr() if perm is not None and not prepermuted else 0,
-                de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
-                key_stride=(key.lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
-                prime=gidx))
+            if fused:
+                if perm is not None and not prepermuted:
+                    raise LevelScaleError("fused key switch needs pre-permuted rotation keys")
+                parts.append((kbr, kar, (key.lmax + 2) * self.n, off))
+            else:
+                parts.append(_tasks(
+                    nat.KS_TASK2, rows, de=der[off, 0, :], kb=kbr, ka=kar, out_b=ipr[j, 0, 0],
+                    out_a=ipr[j, 0, 1],
+                    perm=perm.data_ptr() if perm is not None and not prepermuted else 0,
+                    de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
+                    key_stride=(key.lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
+                    prime=gidx))
             if perm is None or prepermuted:
                 natural[j] = (kb_t, ka_t, key.lmax)
             if prepermuted:
@@ -681,7 +718,23 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
-        if natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
+        if fused:
+            # ModUp + inner product in one kernel: one task per (job, clip, row)
+            t = np.zeros((nj, bsz, rows), dtype=nat.KSF_TASK)
+            cr = rp(de.coef).reshape(de.coef.shape[0], ndig)
+            ident = np.zeros((de.src.shape[0], rows), dtype=np.uint64)
+            ident[:, :ndig] = de.src
+            for j, (kbr, kar, kds, off) in enumerate(parts):
+                t["coef"][j] = cr[off:off + bsz, 0][:, None]
+                t["ident"][j] = ident[off:off + bsz]
+                t["kb"][j], t["ka"][j] = kbr[None, :], kar[None, :]
+                t["key_dstride"][j] = kds
+            t["out_b"], t["out_a"] = ipr[:, :, 0], ipr[:, :, 1]
+            t["ndig"] = ndig
+            t["dst_prime"] = gidx[None, None, :]
+            t["ident_digit"] = np.array(list(range(ndig)) + [-1])[None, None, :]
+            self.ring.ks_fused(t.ravel())
+        elif natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
             # every natural-order inner product in ONE GEMM launch: a hoisted
             # group shares its digit set, rot_each / relinearisation jobs bring
             # their own (one output pair per tile)
@@ -1089,7 +1142,7 @@ class CkksBackend(BackendBase):
                 c1 = np.concatenate([
                     self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)[:, 1]
                     for i in chunk])
-                de = self._decompose(c1, lvl)
+                de = self._decompose(c1, lvl, fused_ok=True)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1113,7 +1166,8 @@ class CkksBackend(BackendBase):
                 chunk = idx[c0:c0 + step]
                 rows = [self.ring.row_ptrs(items[i][0].payload.data).reshape(bsz, 2, lvl + 1)
                         for i in chunk]
-                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl)
+                de = self._decompose(np.concatenate([rw[:, 1] for rw in rows]), lvl,
+                                     fused_ok=True)
                 jobs = []
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
@@ -1143,7 +1197,7 @@ class CkksBackend(BackendBase):
                     b0=xr[:, :, 0].ravel(), b1=xr[:, :, 1].ravel(), d0=dr[:, :, 0].ravel(),
                     d1=dr[:, :, 1].ravel(), d2=dr[:, :, 2].ravel(),
                     prime=self._row_primes(k * bsz, r)))
-                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl)
+                de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl, fused_ok=True)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
                 res = self._ks_apply_many(de, lvl, jobs, bsz)
                 del de

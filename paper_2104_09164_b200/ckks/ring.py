@@ -430,6 +430,27 @@ class RingContext:
                 _STATS.add("keyswitch_gemm", nbytes, nout * ndig * bc * rows * self.n
                            * StepStats.FP64_PER_MODMUL)
 
+    def ks_fused(self, tasks: np.ndarray):
+        """Fused ModUp + key-switch inner product (csrc/ntt3.cu k_ks3): one
+        task per (ciphertext, target row)."""
+        if len(tasks):
+            d = _upload(tasks, self.device)
+            e0 = _STATS.begin() if _STATS else None
+            nat.check(self._lib.hb_ks_fused(self.handle, _ptr(d), len(tasks), self.stream),
+                      "ks_fused")
+            if _STATS:   # digit rows once, identity rows, key rows once, two outputs per task
+                _STATS.end("keyswitch_fused", e0)
+                m = len(tasks)
+                ndig = tasks["ndig"].astype(np.int64)
+                lifts = int((ndig - (tasks["ident_digit"] >= 0)).sum())
+                keys = len({(int(a), int(n)) for a, n in zip(tasks["kb"], tasks["ndig"])})
+                nd = int(ndig.max())
+                nbytes = (_uniq(tasks["coef"]) * nd + _uniq(tasks["ident"]) + 2 * keys * nd
+                          + 2 * m) * 8 * self.n + lifts * 16 * self.n // 8
+                fp64 = lifts * (self.n // 2) * self.logn * StepStats.FP64_PER_BUTTERFLY \
+                    + 2 * int(ndig.sum()) * self.n * StepStats.FP64_PER_MODMUL
+                _STATS.add("keyswitch_fused", nbytes, fp64)
+
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):
             d = _upload(tasks, self.device)

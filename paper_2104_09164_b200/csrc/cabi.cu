@@ -45,6 +45,7 @@ cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, i
                            const void* c0 = nullptr, long long c0_bstride = 0,
                            const void* pmod = nullptr);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
+cudaError_t launch_ks3(const HbKsfTask*, int, const HbRing&, cudaStream_t);
 cudaError_t launch_bconv(const void*, int, int, const HbPrime*, int, cudaStream_t);
 int bconv_task_size();
 cudaError_t launch_lift_center(const u64*, u64, long long*, int, cudaStream_t);
@@ -251,6 +252,7 @@ int hb_sizeof_task(int kind) {
     case 3: return (int)sizeof(HbMacTerm);
     case 5: return (int)sizeof(HbKsTask2);
     case 6: return bconv_task_size();
+    case 7: return (int)sizeof(HbKsfTask);
     default: return -1;
   }
 }
@@ -350,6 +352,12 @@ int hb_ks_gemm_rot(hb_ring* r, const void* de, const void* keys, const void* key
                                  de_bstride, dst_bstride, prime_last, 0, (cudaStream_t)stream,
                                  scat, c0s, c0, c0_bstride, pmod);
   return e ? fail(e, "hb_ks_gemm_rot") : 0;
+}
+
+// Fused ModUp + key-switch inner product (ntt3.cu k_ks3, TMEM accumulators).
+int hb_ks_fused(hb_ring* r, const void* tasks, int count, void* stream) {
+  cudaError_t e = launch_ks3((const HbKsfTask*)tasks, count, r->dev, (cudaStream_t)stream);
+  return e ? fail(e, "hb_ks_fused") : 0;
 }
 
 int hb_ks_inner2(hb_ring* r, const void* tasks, int count, int nb, void* stream) {

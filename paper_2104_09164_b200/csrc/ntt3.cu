@@ -57,6 +57,9 @@ constexpr int THREADS3 = 256;
 // (cp.async.bulk.prefetch) while the block pass runs.
 template <int LOGN>
 __host__ __device__ constexpr int smem3() { return TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
+// k_ks3: + its task (64 B) behind the two barrier words
+template <int LOGN>
+__host__ __device__ constexpr int smem3k() { return smem3<LOGN>() + 64; }
 constexpr int MINB3 = 4;
 // N = 2^16 runs 16-CTA clusters (non-portable size): per launch within
 // -6..+1 % of the two-pass kernels, but the pipeline then takes the
@@ -582,6 +585,297 @@ inline cudaError_t cluster16_once(const void* fn, int cl) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Fused ModUp + key-switch inner product (non-hoisted key switches:
+// relinearisation, rot_each, rotate-and-add; engine.py:290-326 with
+// ring.py:136-156).  The unfused path writes the whole digit expansion
+// [l+1][l+2] rows per ciphertext (FWD_LIFT launches) only for the GEMM to
+// read it back: the dominant HBM traffic of a key switch.  Here one cluster
+// owns one (ciphertext, target prime t): it loops over the digits, runs the
+// forward NTT of each lifted digit under q_t in shared memory exactly as
+// k_ntt3_fwd does, multiplies the transform by the two key rows and keeps
+// the running sums of its 4096-coefficient tile in TENSOR MEMORY -- 16
+// coefficients x (b, a) per thread = 64 32-bit TMEM columns in the thread's
+// own lane (tcgen05.st / tcgen05.ld 32x32b), 128 columns per CTA, so four
+// CTAs per SM fill the 512 columns and the kernel keeps the NTT's 64
+// registers and 42.5 KB of shared memory.  Only the 2 (l+2) inner-product
+// rows are written.  Sums of balanced products (< 8p) are exact in double;
+// the canonical result is bit-identical to the unfused path.
+HB_DEV uint32_t tmem_alloc128(uint32_t* slot) {
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     smem_addr(slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  return *slot;
+}
+HB_DEV void tmem_free128(uint32_t base) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(base) : "memory");
+}
+HB_DEV void tmem_st4(uint32_t a, double v0, double v1, double v2, double v3) {
+  const u64 u0 = __double_as_longlong(v0), u1 = __double_as_longlong(v1),
+            u2 = __double_as_longlong(v2), u3 = __double_as_longlong(v3);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a),
+               "r"((uint32_t)u0), "r"((uint32_t)(u0 >> 32)), "r"((uint32_t)u1),
+               "r"((uint32_t)(u1 >> 32)), "r"((uint32_t)u2), "r"((uint32_t)(u2 >> 32)),
+               "r"((uint32_t)u3), "r"((uint32_t)(u3 >> 32))
+               : "memory");
+}
+HB_DEV void tmem_ld4(uint32_t a, double& v0, double& v1, double& v2, double& v3) {
+  uint32_t r0, r1, r2, r3, r4, r5, r6, r7;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+               : "r"(a)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  v0 = __longlong_as_double(((u64)r1 << 32) | r0);
+  v1 = __longlong_as_double(((u64)r3 << 32) | r2);
+  v2 = __longlong_as_double(((u64)r5 << 32) | r4);
+  v3 = __longlong_as_double(((u64)r7 << 32) | r6);
+}
+HB_DEV void mbar_wait_par(uint64_t* mbar, uint32_t parity) {
+  const uint32_t a = smem_addr(mbar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAITP%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITP%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+#ifndef HB_KS3_UNROLL
+#define HB_KS3_UNROLL 4   // accumulate-loop unroll (key loads in flight per thread)
+#endif
+constexpr int KS3_UNROLL = HB_KS3_UNROLL;
+template <int LOGN>
+__global__ void __launch_bounds__(THREADS3, MINB3)
+k_ks3(const HbKsfTask* __restrict__ tasks, HbRing R) {
+  constexpr int N = 1 << LOGN, S1 = LOGN - 7, M = 1 << S1, CW = TILE3 / M, CL = N / TILE3;
+  typedef PolF64 Pol;
+  typedef ColPlan<S1, true> CP;
+  typedef double V;
+  extern __shared__ __align__(16) unsigned char smraw3[];
+  V* sm = reinterpret_cast<V*>(smraw3);
+  V* rb = sm;
+  constexpr int TWC = M - 1, TW3 = TWC + 480;
+  HbTwD* tws = reinterpret_cast<HbTwD*>(rb + TILE3);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tws + TW3);
+  const int t = threadIdx.x;
+  const int rank = (int)cluster_rank();
+  // the task lives in shared memory (read where needed: its ten fields
+  // would not fit the 64-register budget next to the transform)
+  HbKsfTask* tkp = reinterpret_cast<HbKsfTask*>(mbar + 2);
+  if (t < (int)(sizeof(HbKsfTask) / 8))
+    reinterpret_cast<u64*>(tkp)[t] = reinterpret_cast<const u64*>(tasks + blockIdx.x / CL)[t];
+  __syncthreads();
+  const HbKsfTask& tk = *tkp;
+  const int dprime = tk.dst_prime;
+  const Pol pol(R.primes[dprime]);
+  if (t == 0) {
+    const uint32_t a = smem_addr(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t tbase = tmem_alloc128(reinterpret_cast<uint32_t*>(mbar + 1));
+  // this thread's 64 columns: its warp's lane quadrant, column half by warp / 4
+  const uint32_t tacc = tbase + ((uint32_t)(((t >> 5) & 3) * 32) << 16) + (uint32_t)(t >> 7) * 64;
+  auto fetch_col = [&](int s, int idx) { return tws[(1 << s) + idx - 1]; };
+  auto fetch_blk = [&](int s, int idx) {
+    const int e = s - S1;
+    return tws[TWC + 32 * ((1 << e) - 1) + idx - rank * (32 << e)];
+  };
+  constexpr int N8 = N / 8;
+  const HbTwD* t3 = R.tw3_fwd + (size_t)dprime * N;
+  auto fetch_fine = [&](int s, int idx) {
+    const int e = s - (S1 + 4), ii = idx & ((1 << e) - 1);
+    const double2 w = __ldg(reinterpret_cast<const double2*>(t3 + (((1 << e) - 1 + ii) * N8 + (idx >> e))));
+    return HbTwD{w.x, w.y};
+  };
+  HB_PDL_ENTRY();
+  stage_twiddles<LOGN, true>(tws, Pol::fwd_table(R, dprime), rank);
+  const int cg0 = rank * CW;
+  const size_t base = (size_t)rank * TILE3;
+  const double pd = pol.p, pinv = pol.pinv;
+  uint32_t phase = 0;
+  bool first = true;
+  for (int dg = 0; dg < tk.ndig; ++dg) {
+    const bool ident = dg == tk.ident_digit;
+    const bool lastd = dg == tk.ndig - 1;
+    const u64* kb = tk.kb + (size_t)dg * tk.key_dstride + base;
+    const u64* ka = tk.ka + (size_t)dg * tk.key_dstride + base;
+    if (t == 0) {   // this digit's key tiles into L2 while the transform runs
+      l2_prefetch(kb, TILE3 * 8);
+      l2_prefetch(ka, TILE3 * 8);
+    }
+    if (!ident) {
+      const u64* src = tk.coef + (size_t)dg * N;
+      if (t == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)),
+                     "r"((uint32_t)(TILE3 * sizeof(V)))
+                     : "memory");
+      }
+      __syncthreads();   // the previous digit's epilogue has left the tile
+      // ---- column pass (as k_ntt3_fwd, source rows are centred lifts)
+      {
+        const int c = t % CW, gq = t / CW;
+        V x[16];
+        const uint32_t sm0 = smem_addr(sm);
+#pragma unroll
+        for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+          const int k = t + i * THREADS3;
+          const int m = k / (CW / 2), cp2 = 2 * (k % (CW / 2));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm0 + 8u * csw<CW>(m, cp2)),
+                       "l"(src + (size_t)m * 128 + cg0 + cp2)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        tws_wait();
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (!CP::owns(0, q)) break;
+          x[q] = fmod_reduce(sm[csw<CW>(CP::m_of(0, gq, q), c)], pol.p, pol.pinv);
+        }
+#pragma unroll
+        for (int rd = 0; rd < CP::NR; ++rd) {
+          if (rd > 0) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              if (!CP::owns(rd, q)) break;
+              x[q] = sm[csw<CW>(CP::m_of(rd, gq, q), c)];
+            }
+          }
+          if (rd == CP::NR - 1) cluster_arrive_sb();
+          col_butterflies<Pol, S1, true>(x, rd, gq, fetch_col, pol);
+          if (rd < CP::NR - 1) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              if (!CP::owns(rd, q)) break;
+              sm[csw<CW>(CP::m_of(rd, gq, q), c)] = x[q];
+            }
+            __syncthreads();
+          }
+        }
+        cluster_wait();
+        const uint32_t rb0 = smem_addr(rb), mb0 = smem_addr(mbar);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (!CP::owns(CP::NR - 1, q)) break;
+          const int m = CP::m_of(CP::NR - 1, gq, q);
+          const uint32_t dst = m >> 5;
+          st_async8(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), x[q]);
+        }
+      }
+      mbar_wait_par(mbar, phase);
+      phase ^= 1;
+      // ---- block pass
+      {
+        const int blk = t >> 3, cc = t & 7;
+        V x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = rb[bsw(blk * 128 + u * 8 + cc)];
+        fwd_group_f<Pol, 4>(x, S1, rank * 32 + blk, fetch_blk, pol);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) rb[bsw(blk * 128 + u * 8 + cc)] = x[u];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int g2 = t + q * THREADS3;
+        const int b2 = g2 >> 4, G8 = g2 & 15;
+        const int e0 = b2 * 128 + G8 * 8;
+        V x[8];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int pc = swz3_chunk((e0 >> 1) + v);
+          x[2 * v] = rb[2 * pc];
+          x[2 * v + 1] = rb[2 * pc + 1];
+        }
+        fwd_group_f<Pol, 3>(x, S1 + 4, (rank * 32 + b2) * 16 + G8, fetch_fine, pol);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int pc = swz3_chunk((e0 >> 1) + v);
+          rb[2 * pc] = x[2 * v];
+          rb[2 * pc + 1] = x[2 * v + 1];
+        }
+      }
+      __syncthreads();
+    }
+    // ---- accumulate x * key into the thread's TMEM columns; after the last
+    // digit canonicalise and store instead
+#pragma unroll KS3_UNROLL
+    for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
+      const int k = t + i * THREADS3;
+      const size_t j = 2 * (size_t)k;
+      double x0, x1;
+      if (ident) {
+        const ulonglong2 xi = __ldg(reinterpret_cast<const ulonglong2*>(tk.ident + base + j));
+        x0 = u64_to_f(xi.x);
+        x1 = u64_to_f(xi.y);
+      } else {
+        const int pc = swz3_chunk(k);
+        x0 = rb[2 * pc];
+        x1 = rb[2 * pc + 1];
+      }
+      const ulonglong2 b2 = __ldg(reinterpret_cast<const ulonglong2*>(kb + j));
+      const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(ka + j));
+      double ab0 = 0.0, ab1 = 0.0, aa0 = 0.0, aa1 = 0.0;
+      if (!first) tmem_ld4(tacc + 8 * i, ab0, ab1, aa0, aa1);
+      const double kb0 = u64_to_f(b2.x), kb1 = u64_to_f(b2.y);
+      const double ka0 = u64_to_f(a2.x), ka1 = u64_to_f(a2.y);
+      ab0 += fmod_mul(x0, kb0, kb0 * pinv, pd);
+      ab1 += fmod_mul(x1, kb1, kb1 * pinv, pd);
+      aa0 += fmod_mul(x0, ka0, ka0 * pinv, pd);
+      aa1 += fmod_mul(x1, ka1, ka1 * pinv, pd);
+      if (lastd) {
+        ulonglong2 ob, oa;
+        ob.x = fmod_canon(ab0, pd, pinv);
+        ob.y = fmod_canon(ab1, pd, pinv);
+        oa.x = fmod_canon(aa0, pd, pinv);
+        oa.y = fmod_canon(aa1, pd, pinv);
+        *reinterpret_cast<ulonglong2*>(tk.out_b + base + j) = ob;
+        *reinterpret_cast<ulonglong2*>(tk.out_a + base + j) = oa;
+      } else {
+        tmem_st4(tacc + 8 * i, ab0, ab1, aa0, aa1);
+      }
+    }
+    if (!lastd) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    first = false;
+  }
+  tmem_free128(tbase);
+}
+
+template <int LOGN>
+cudaError_t ks3_t(const HbKsfTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  constexpr int CL = (1 << LOGN) / TILE3;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * CL);
+  cfg.blockDim = dim3(THREADS3);
+  cfg.dynamicSmemBytes = smem3k<LOGN>();
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_hb_pdl ? 2 : 1;
+  static int smem_cur = 0;
+  cudaError_t e = smem_attr_once((const void*)k_ks3<LOGN>, (int)(smem3k<LOGN>()), &smem_cur);
+  if (e == cudaSuccess) e = cluster16_once((const void*)k_ks3<LOGN>, CL);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k_ks3<LOGN>, tasks, R);
+}
+
+
 template <int LOGN, int MODE>
 cudaError_t fwd3_t(const HbNttTask* tasks, int count, const HbRing& R, cudaStream_t st) {
   constexpr int CL = (1 << LOGN) / TILE3;
@@ -671,6 +965,21 @@ cudaError_t launch_ntt3_fwd(const HbNttTask* tasks, int count, const HbRing& R, 
     case 15: return fwd3_mode<15>(tasks, count, R, mode, st);
 #if HB_NTT3_MAXLOGN >= 16
     case 16: return fwd3_mode<16>(tasks, count, R, mode, st);
+#endif
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Fused ModUp + inner product (k_ks3): fp64 rings on the cluster NTT.
+cudaError_t launch_ks3(const HbKsfTask* tasks, int count, const HbRing& R, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  if (!ntt3_supported(R)) return cudaErrorNotSupported;
+  switch (R.logn) {
+    case 13: return ks3_t<13>(tasks, count, R, st);
+    case 14: return ks3_t<14>(tasks, count, R, st);
+    case 15: return ks3_t<15>(tasks, count, R, st);
+#if HB_NTT3_MAXLOGN >= 16
+    case 16: return ks3_t<16>(tasks, count, R, st);
 #endif
     default: return cudaErrorInvalidValue;
   }

@@ -97,6 +97,22 @@ struct HbNttTask {
   int dst_prime;    // prime the transform runs in
 };
 
+// One (ciphertext, target row) of the fused ModUp + key-switch inner product
+// (ntt3.cu k_ks3): out_b / out_a = sum_i NTT_t(lift(digit i)) * key_{b,a}[i].
+struct HbKsfTask {
+  const u64* coef;     // digit i's centred lift as doubles, coefficient domain, at coef + i*N
+  const u64* ident;    // NTT-form row of the digit whose prime IS the target (else null)
+  const u64* kb;       // key rows of the target prime: digit i at kb + i*key_dstride
+  const u64* ka;
+  u64* out_b;          // the two inner-product rows of this target prime
+  u64* out_a;
+  long long key_dstride;
+  int ndig;
+  int dst_prime;
+  int ident_digit;     // the digit served by `ident` (-1: none, the special row)
+  int _pad;
+};
+
 // One output row of a plaintext multiply-accumulate:
 //   dst = sum_t pt_t * ct_t  (mod p)   over terms [term_off, term_off + nterms)
 struct HbMacTask {
