@@ -125,10 +125,10 @@ KSF_TASK = np.dtype([("coef", "<u8"), ("ident", "<u8"), ("kb", "<u8"), ("ka", "<
                      ("_pad", "<i4")])
 
 # NTT fused modes (csrc/ntt.cu FwdMode)
-FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER = 0, 1, 2, 3, 4
+FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER, FWD_MODDOWN2 = 0, 1, 2, 3, 4, 5
 # element-wise ops (csrc/ops.cu EwOp)
 EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PERM, \
-    EW_SUB_SCALED, EW_PERM_ADD = range(10)
+    EW_SUB_SCALED, EW_PERM_ADD, EW_MD_TOP = range(11)
 
 
 def _check_layouts():

@@ -183,6 +183,7 @@ class CkksBackend(BackendBase):
             ps = np.array(chain[:lvl], dtype=np.uint64)
             self._resc.append((inv, shoup_np(inv, ps) if lvl else inv))
         self._crt_cache: dict = {}
+        self._mdr: dict = {}   # level -> (P q_l)^-1 mod q_t, the merged ModDown + rescale
         # rotation inner products on pre-permuted keys (default; HEAR_B200_PREPERM=0
         # disables): the digits are read in natural order, so a hoisted group
         # is one GEMM over digits x (rotation, component) and the Galois map is
@@ -665,7 +666,8 @@ class CkksBackend(BackendBase):
                                  dst_prime=dp[lift]), nat.FWD_LIFT)
         return de
 
-    def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None) -> list:
+    def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None,
+                       rescale: bool = False) -> list:
         """Key-switch decomposed digits once per job and ModDown.
 
         job = (key, perm_dev | None, addend_ptrs [bsz, 2, lvl+1] uint64 (0 = none),
@@ -772,6 +774,13 @@ class CkksBackend(BackendBase):
                 post[j] = job[5]
         has_post = bool(post.any())
         iprows = rp(ip).reshape(m, rows)
+        if rescale:
+            # relinearisation followed by its rescale: ModDown, the (d0, d1)
+            # addend and the division by q_lvl in one pass per target row
+            if late or has_post or perms.any() or not add.all() or not self.lift_once:
+                raise LevelScaleError("merged ModDown + rescale: plain addend jobs only")
+            out = self._md_rescale(iprows, lvl, add.reshape(m, r)).reshape(nj, bsz, 2, lvl, self.n)
+            return [out[j] for j in range(nj)]
         spc = self.ring.empty(m)
         sprime = np.full(m, self.S)
         self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=iprows[:, lvl + 1], dst=rp(spc),
@@ -951,6 +960,21 @@ class CkksBackend(BackendBase):
                 out[i] = Ct(CtData(res[q]), lvl, t0[0].scale * t0[1].scale, self.n2)
         return out
 
+    def _raw_mac_rescale_many(self, jobs) -> list:
+        if not (isinstance(jobs[0][0][0].payload, CtExt) and self.lift_once):
+            return super()._raw_mac_rescale_many(jobs)
+        out = [None] * len(jobs)
+        for lvl, idx, acc in self._mac_ext(jobs):
+            bsz = acc.shape[1]
+            res = self._mod_down_ext(acc.reshape(len(idx) * bsz, 2, lvl + 2, self.n), lvl,
+                                     rescale=True)
+            res = res.reshape(len(idx), bsz, 2, lvl, self.n)
+            for q, i in enumerate(idx):
+                t0 = jobs[i][0]
+                out[i] = Ct(CtData(res[q]), lvl - 1, t0[0].scale * t0[1].scale
+                            / self.params.chain_primes[lvl], self.n2)
+        return out
+
     def _mac_ext(self, jobs) -> list:
         """[(level, job indices, acc [len, B, 2, level+2, N])]: the products
         summed modulo every chain prime and the special prime, per group of
@@ -980,11 +1004,51 @@ class CkksBackend(BackendBase):
             res.append((lvl, idx, acc))
         return res
 
-    def _mod_down_ext(self, ext: torch.Tensor, level: int) -> torch.Tensor:
+    def _md_rescale(self, rows: np.ndarray, lvl: int, addend) -> torch.Tensor:
+        """rescale(ModDown(x) + addend) in one step (cluster NTT): rows
+        [m, lvl+2] pointers of extended-basis rows (special last), addend
+        [m, lvl+1] pointers or None -> [m, lvl, N] at level lvl-1.
+
+        ModDown then rescale is (x_t - NTT_t(xP)) P^-1 + d_t - NTT_t(top)) / q_l
+        with top = centre(((x_l - xP) P^-1 + d_l) mod q_l) in the coefficient
+        domain; both transforms of a target row merge into ONE,
+        NTT_t(xP + P * top) (FWD_MODDOWN2), so a row costs one NTT instead
+        of two.  Same residues as the two separate steps (exact maps)."""
+        m = rows.shape[0]
+        rp = self.ring.row_ptrs
+        k = 2 if addend is None else 3
+        cf = self.ring.empty(k, m)
+        cfr = rp(cf).reshape(k, m)
+        src = [rows[:, lvl + 1], rows[:, lvl]] + ([] if addend is None else [addend[:, lvl]])
+        prim = np.repeat(np.array([self.S, lvl, lvl][:k]), m)
+        self.ring.ntt_inv(_tasks(nat.NTT_TASK, k * m, src=np.concatenate(src), dst=cfr.ravel(),
+                                 dst_prime=prim, src_prime=prim, scal=1))
+        top = self.ring.empty(m)
+        self._ew(nat.EW_MD_TOP, rp(top), cfr[1], cfr[0], c=None if addend is None else cfr[2],
+                 primes=np.full(m, lvl), scal=np.full(m, self._pinv[lvl]),
+                 scal_sh=np.full(m, self._pinv_sh[lvl]))
+        if lvl not in self._mdr:
+            chain = self.params.chain_primes
+            self._mdr[lvl] = np.array([pow(self.P * chain[lvl], -1, chain[t]) for t in range(lvl)],
+                                      dtype=np.uint64)
+        out = self.ring.empty(m, lvl)
+        f = dict(src=np.repeat(cfr[0], lvl), perm=np.repeat(rp(top), lvl), dst=rp(out),
+                 aux=rows[:, :lvl].ravel(), src_prime=-1, dst_prime=np.tile(np.arange(lvl), m),
+                 scal=np.tile(self._mdr[lvl], m), scal_sh=np.tile(self._pmod[:lvl], m))
+        if addend is not None:
+            f["add"] = addend[:, :lvl].ravel()
+            f["add2"] = np.tile(self._resc[lvl][0], m)
+        self.ring.ntt_fwd(_tasks(nat.NTT_TASK, m * lvl, **f), nat.FWD_MODDOWN2)
+        return out
+
+    def _mod_down_ext(self, ext: torch.Tensor, level: int, rescale: bool = False) -> torch.Tensor:
         """ext [M, 2, level+2, N] -> (x - [x]_P)/P on the chain rows
-        [M, 2, level+1, N] (engine.py:213-227), the key switch's ModDown."""
+        [M, 2, level+1, N] (engine.py:213-227), the key switch's ModDown;
+        rescale=True: divided by q_level as well -> [M, 2, level, N]."""
         m, r = ext.shape[0] * 2, level + 1
         rows = self.ring.row_ptrs(ext).reshape(m, level + 2)
+        if rescale:
+            return self._md_rescale(rows, level, None).reshape(m // 2, 2, level, self.n)
         spc = self.ring.empty(m)
         sp = np.full(m, self.S)
         self.ring.ntt_inv(_tasks(nat.NTT_TASK, m, src=rows[:, level + 1], dst=self.ring.row_ptrs(spc),
@@ -1179,7 +1243,7 @@ class CkksBackend(BackendBase):
                     out[i] = Ct(CtData(res[q]), lvl, ct.scale, self.n2)
         return out
 
-    def _raw_square_each(self, cts) -> list:
+    def _raw_square_each(self, cts, rescale: bool = False) -> list:
         out = [None] * len(cts)
         for lvl, idx in self._by_level(cts, lambda c: c.level).items():
             bsz = cts[idx[0]].payload.batch
@@ -1199,12 +1263,21 @@ class CkksBackend(BackendBase):
                     prime=self._row_primes(k * bsz, r)))
                 de = self._decompose(dr[:, :, 2].reshape(k * bsz, r), lvl, fused_ok=True)
                 jobs = [(self.keys.relin, None, dr[q, :, :2], False, q * bsz) for q in range(k)]
-                res = self._ks_apply_many(de, lvl, jobs, bsz)
+                res = self._ks_apply_many(de, lvl, jobs, bsz, rescale=rescale)
                 del de
                 for q, i in enumerate(chunk):
                     c = cts[i]
-                    out[i] = Ct(CtData(res[q]), lvl, c.scale * c.scale, self.n2)
+                    if rescale:
+                        out[i] = Ct(CtData(res[q]), lvl - 1,
+                                    c.scale * c.scale / self.params.chain_primes[lvl], self.n2)
+                    else:
+                        out[i] = Ct(CtData(res[q]), lvl, c.scale * c.scale, self.n2)
         return out
+
+    def _raw_square_rescale_each(self, cts) -> list:
+        if not self.lift_once:
+            return super()._raw_square_rescale_each(cts)
+        return self._raw_square_each(cts, rescale=True)
 
     def _raw_rot_many_each(self, cts, ks) -> list:
         """Hoisted rotations of several handles by the same amounts: one ModUp

@@ -256,14 +256,19 @@ class RingContext:
 
     _FWD_NAMES = {nat.FWD_PLAIN: "ntt_fwd", nat.FWD_LIFT: "ntt_fwd_modup_lift",
                   nat.FWD_MODDOWN: "ntt_fwd_moddown", nat.FWD_I64: "ntt_fwd_i64",
-                  nat.FWD_MODDOWN_SCATTER: "ntt_fwd_moddown_scatter"}
+                  nat.FWD_MODDOWN_SCATTER: "ntt_fwd_moddown_scatter",
+                  nat.FWD_MODDOWN2: "ntt_fwd_moddown_rescale"}
 
     def _ntt_account(self, fam: str, tasks: np.ndarray, kernels: int):
         row = 8 * self.n
         m = len(tasks)
         nbytes = (_uniq(tasks["src"]) + m) * row             # sources once, every output
-        nbytes += (_uniq(tasks["aux"]) + _uniq(tasks["add"]) + _uniq(tasks["add2"])) * row
-        nbytes += _uniq(tasks["perm"]) * 4 * self.n + m * 16 * self.n // 8   # perms; twiddles
+        if fam == "ntt_fwd_moddown_rescale":   # perm = second source row, add2 = a scalar
+            nbytes += (_uniq(tasks["aux"]) + _uniq(tasks["add"]) + _uniq(tasks["perm"])) * row
+            nbytes += m * 16 * self.n // 8
+        else:
+            nbytes += (_uniq(tasks["aux"]) + _uniq(tasks["add"]) + _uniq(tasks["add2"])) * row
+            nbytes += _uniq(tasks["perm"]) * 4 * self.n + m * 16 * self.n // 8   # perms; twiddles
         fp64 = m * (self.n // 2) * self.logn * StepStats.FP64_PER_BUTTERFLY
         if fam.startswith("ntt_fwd_moddown"):
             fp64 += m * self.n * StepStats.FP64_PER_MODMUL
@@ -295,7 +300,8 @@ class RingContext:
     _EW_READS = {nat.EW_ADD: ("a", "b"), nat.EW_SUB: ("a", "b"), nat.EW_MUL: ("a", "b"),
                  nat.EW_MUL_SCALAR: ("a",), nat.EW_MULADD: ("a", "b", "c"),
                  nat.EW_ADD_SCALED: ("a", "b"), nat.EW_COPY: ("a",), nat.EW_PERM: ("a",),
-                 nat.EW_SUB_SCALED: ("a", "b"), nat.EW_PERM_ADD: ("a", "b")}
+                 nat.EW_SUB_SCALED: ("a", "b"), nat.EW_PERM_ADD: ("a", "b"),
+                 nat.EW_MD_TOP: ("a", "b", "c")}
     _EW_MULS = {nat.EW_MUL: 1, nat.EW_MUL_SCALAR: 1, nat.EW_MULADD: 1, nat.EW_ADD_SCALED: 1,
                 nat.EW_SUB_SCALED: 1}
 

@@ -239,7 +239,7 @@ def hconv(cts: list, weights: ConvWeights, plan: ConvPlan, backend: BackendBase,
                 fj.append([(pre[i][(taps[k] + blocks[l]) % n2], pts[(i, k, l)])
                            for k in range(plan.f) for l in range(plan.ell_i)
                            for i in range(plan.m)])
-            outs += backend.rescale_each(backend.mac_many(fj))
+            outs += backend.mac_rescale_many(fj)
             continue
         for j in js:
             pts = weights.for_output(j)

@@ -283,6 +283,13 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
         const u64 raw = (u64)__double_as_longlong(sm[csw<CW>(CP::m_of(0, gq, q), c)]);
         if (MODE == FWD_PLAIN) x[q] = pol.from_canon(raw);
         else if (MODE == FWD_I64) x[q] = pol.from_signed((i64)raw);
+        else if (MODE == FWD_MODDOWN2) {   // src + P * y, both centred lifts
+          const int m = CP::m_of(0, gq, q);
+          const double y = __ldg(reinterpret_cast<const double*>(tk.perm) + (size_t)m * 128 + cg0 + c);
+          const double pm = u64_to_f(tk.scal_sh);
+          x[q] = fmod_reduce(__longlong_as_double((long long)raw), pol.p, pol.pinv)
+                 + fmod_mul(y, pm, pm * pol.pinv, pol.p);
+        }
         else if (lifted) x[q] = fmod_reduce(__longlong_as_double((long long)raw), pol.p, pol.pinv);
         else x[q] = pol.from_lift(raw, ps, ps_half);
       }
@@ -319,7 +326,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       st_async8(mapa(rb0 + 8u * bsw((m & 31) * 128 + cg0 + c), dst), mapa(mb0, dst), x[q]);
     }
   }
-  constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER;
+  constexpr bool MD = MODE == FWD_MODDOWN || MODE == FWD_MODDOWN_SCATTER || MODE == FWD_MODDOWN2;
   if (MD && t == 0) {   // the epilogue's x_r / addend tiles into L2 meanwhile
     l2_prefetch(tk.aux + (size_t)rank * TILE3, TILE3 * 8);
     if (tk.add && !(MODE == FWD_MODDOWN && tk.perm)) l2_prefetch(tk.add + (size_t)rank * TILE3, TILE3 * 8);
@@ -388,6 +395,14 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       const ulonglong2 ax = __ldg(reinterpret_cast<const ulonglong2*>(tk.aux + j));
       double r0 = fmod_mul(u64_to_f(ax.x) - rb[2 * pc], sd, sq, pd);
       double r1 = fmod_mul(u64_to_f(ax.y) - rb[2 * pc + 1], sd, sq, pd);
+      if (MODE == FWD_MODDOWN2) {
+        if (tk.add) {   // the addend is divided by q_l too: + add * s2
+          const ulonglong2 a2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.add + j));
+          const double s2 = u64_to_f((u64)tk.add2), s2q = s2 * pinv;
+          r0 += fmod_mul(u64_to_f(a2.x), s2, s2q, pd);
+          r1 += fmod_mul(u64_to_f(a2.y), s2, s2q, pd);
+        }
+      } else {
       if (tk.add) {
         u64 a0, a1;
         if (MODE == FWD_MODDOWN && tk.perm) {
@@ -412,6 +427,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
           r0 += u64_to_f(a2.x);
           r1 += u64_to_f(a2.y);
         }
+      }
       }
       o.x = fmod_canon(r0, pd, pinv);
       o.y = fmod_canon(r1, pd, pinv);
@@ -934,6 +950,7 @@ cudaError_t fwd3_mode(const HbNttTask* tasks, int count, const HbRing& R, int mo
     case FWD_MODDOWN: return fwd3_t<LOGN, FWD_MODDOWN>(tasks, count, R, st);
     case FWD_I64: return fwd3_t<LOGN, FWD_I64>(tasks, count, R, st);
     case FWD_MODDOWN_SCATTER: return fwd3_t<LOGN, FWD_MODDOWN_SCATTER>(tasks, count, R, st);
+    case FWD_MODDOWN2: return fwd3_t<LOGN, FWD_MODDOWN2>(tasks, count, R, st);
     default: return cudaErrorInvalidValue;
   }
 }

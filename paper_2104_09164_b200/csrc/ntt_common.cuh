@@ -14,6 +14,14 @@ enum FwdMode : int {
   FWD_MODDOWN_SCATTER = 4,  // FWD_MODDOWN whose result lands at dst[perm[j]] and
                             // whose addend is read at j: a rotation computed on
                             // pre-permuted keys
+  FWD_MODDOWN2 = 5,  // ModDown by P merged with the rescale by q_l that follows
+                     // it (cluster NTT only): src = centred lift of the special
+                     // row, perm REINTERPRETED as a second source row y (centred
+                     // doubles, the ModDown'ed top row in the coefficient
+                     // domain), scal_sh = P mod p_dst, scal = (P q_l)^-1:
+                     //   dst = (aux - NTT(src + P*y)) * scal + add * s2,
+                     // s2 = q_l^-1 mod p_dst passed by value in add2.  Equal bit
+                     // for bit to FWD_MODDOWN followed by the rescale.
 };
 
 // ---------------------------------------------------------------------------

@@ -25,6 +25,29 @@ k_ew(const HbEwTask* __restrict__ tasks, int ntasks, const HbPrime* __restrict__
     if (j >= n) continue;
     ulonglong2 a = *reinterpret_cast<const ulonglong2*>(tk.a + j);
     ulonglong2 r;
+    if (OP == EW_MD_TOP) {
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tk.b + j);
+      ulonglong2 c = make_ulonglong2(0, 0);
+      if (tk.c) c = *reinterpret_cast<const ulonglong2*>(tk.c + j);
+      auto one = [&](u64 ua, u64 ub, u64 uc) {
+        const i64 d = (i64)__longlong_as_double((long long)ua) - (i64)__longlong_as_double((long long)ub);
+        u64 m = reduce64((u64)(d < 0 ? -d : d), P);
+        if (d < 0 && m) m = p - m;
+        u64 v = mul_shoup(m, tk.scal, tk.scal_sh, p);
+        if (tk.c) {
+          const i64 e = (i64)__longlong_as_double((long long)uc);
+          u64 me = reduce64((u64)(e < 0 ? -e : e), P);
+          if (e < 0 && me) me = p - me;
+          v = add_mod(v, me, p);
+        }
+        const double dv = v > P.half ? -(double)(p - v) : (double)v;
+        return (u64)__double_as_longlong(dv);
+      };
+      r.x = one(a.x, b.x, c.x);
+      r.y = one(a.y, b.y, c.y);
+      *reinterpret_cast<ulonglong2*>(tk.dst + j) = r;
+      continue;
+    }
     if (OP == EW_ADD || OP == EW_SUB || OP == EW_MUL || OP == EW_MULADD ||
         OP == EW_ADD_SCALED || OP == EW_SUB_SCALED) {
       ulonglong2 b = *reinterpret_cast<const ulonglong2*>(tk.b + j);
@@ -85,6 +108,7 @@ cudaError_t launch_ew(int op, const HbEwTask* tasks, int ntasks, const HbPrime* 
     HB_EW_CASE(EW_PERM)
     HB_EW_CASE(EW_SUB_SCALED)
     HB_EW_CASE(EW_PERM_ADD)
+    HB_EW_CASE(EW_MD_TOP)
 #undef HB_EW_CASE
     default: return cudaErrorInvalidValue;
   }

@@ -154,6 +154,9 @@ enum EwOp : int {
   EW_SUB_SCALED = 8,// dst = (a - b) * scal              (ring.py:210 sub_scaled_inv)
   EW_PERM_ADD = 9,  // dst = a[perm] + b[perm]  (c reinterpreted as int32 perm): the
                     // Galois gather of a rotation applied after ModDown (engine.py:350)
+  EW_MD_TOP = 10,   // a, b, c, dst hold centred lifts as doubles (coefficient domain):
+                    // dst = centre(((a - b) * scal + c) mod p), c optional -- the top
+                    // row after ModDown (+ addend), input of the merged rescale
 };
 
 // Special-FFT tables of the canonical embedding (fft.cu).

@@ -453,10 +453,10 @@ def run_tcn(encoder: TcnEncoder, ct: Ct, backend: BackendBase) -> Ct:
         _check(ct, pl, f"conv{i + 1}")
         with backend.layer(f"act{i + 1}"):
             if sh.acts[i] == "square":
-                ct = backend.rescale(backend.mult(ct, ct))
+                ct = backend.square_rescale_each([ct])[0]
             else:
                 (c1, c2, c3), const = encoder.act_pts(i)
-                x2 = backend.rescale(backend.mult(ct, ct))
+                x2 = backend.square_rescale_each([ct])[0]
                 x3 = backend.rescale(backend.mult(x2, backend.mod_down(ct, x2.level)))
                 lf = x3.level
                 # x, x^2, x^3 carry different scales, so each coefficient is

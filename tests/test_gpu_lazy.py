@@ -176,3 +176,29 @@ def test_lazy_rotate_and_sum(setup):
         clear = sum(np.roll(xs[h], -33 * j, axis=1) for j in range(5))
         assert np.abs(res[True][0][h] - clear).max() <= 2e-4
         assert np.abs(res[True][0][h] - res[False][0][h]).max() <= 1e-4
+
+
+def test_merged_moddown_rescale_bit_identical(setup):
+    """ModDown merged with the rescale that follows it (one NTT per target row
+    instead of two, FWD_MODDOWN2) gives the two separate steps' residues bit
+    for bit: after a relinearisation (hear/ckks/engine.py:229-281 mult then
+    rescale) and after an extended-basis accumulation."""
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    for fused in (True, False):
+        be.fuse_ks_min = 0 if fused else 1 << 60
+        want = be.rescale_each(be.square_each(cts))
+        got = be.square_rescale_each(cts)
+        for w, g in zip(want, got):
+            assert (w.level, w.scale) == (g.level, g.scale)
+            assert torch.equal(w.payload.data, g.payload.data)
+    be.fuse_ks_min = 600
+    ks = [0] + amounts
+    pts = be.encode_many(rng.uniform(-1, 1, (2 * len(ks), be.n2)), lvl, be.params.msg_scale)
+    lazy = be._raw_rot_many_each_lazy(cts, amounts, True)
+    jobs = [[(lazy[h][k], pts[h * len(ks) + q]) for h in range(2) for q, k in enumerate(ks)]]
+    want = be.rescale_each(be.mac_many(jobs))[0]
+    be.reset_counters()
+    got = be.mac_rescale_many(jobs)[0]
+    assert (want.level, want.scale) == (got.level, got.scale)
+    assert torch.equal(want.payload.data, got.payload.data)
+    assert be.counters.total()["rescale"] == 1
