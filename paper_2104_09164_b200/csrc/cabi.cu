@@ -149,6 +149,10 @@ hb_ring* hb_ring_create(int logn, int nprimes, const unsigned long long* primes,
   for (int i = 0; i < nprimes; ++i) f64 = f64 && primes[i] < (1ull << 42);
   const char* force = getenv("HEAR_B200_INT_NTT");
   r->dev.use_f64 = (f64 && !(force && force[0] == '1')) ? 1 : 0;
+  bool small = true;   // b <= 34 bits: products of a residue and a half-residue stay below 2^51
+  for (int i = 0; i < nprimes; ++i) small = small && primes[i] < (1ull << 34);
+  const char* nosplit = getenv("HEAR_B200_MAC_SPLIT");
+  r->dev.split_ok = (small && !(nosplit && nosplit[0] == '0')) ? 1 : 0;
   std::vector<HbTw> tf((size_t)nprimes * n), ti((size_t)nprimes * n);
   std::vector<HbTwD> tfd((size_t)nprimes * n), tid((size_t)nprimes * n);
   std::vector<double> t1f((size_t)nprimes * n), t1i((size_t)nprimes * n);

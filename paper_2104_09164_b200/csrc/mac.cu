@@ -14,14 +14,25 @@
 // 16-byte cp.async copies, so S-1 terms are in flight while one is
 // multiplied (the register-prefetch kernel in ops.cu stalled 47 % of its
 // samples on the HBM latency of the ct loads, profiles/r01_*).  A warp owns
-// TO x TB outputs per lane; products on the fp64 pipe as fmod_mul (5 ops,
-// balanced residue), summed in double, canonicalised once.
+// TO x TB outputs per lane.
+//
+// Products WITHOUT a per-product reduction: the plaintext / key operand a
+// (< p < 2^b) is split at s = ceil(b/2) bits, a = a1 * 2^s + a0, and the two
+// partial sums  S0 = sum c*a0,  S1 = sum c*a1  are plain DFMA chains -- every
+// product is an integer below 2^(b+s) <= 2^51 and the sums stay below 2^53,
+// so they are EXACT in double.  They are reduced mod p every K terms (K = 3
+// for a 34-bit prime, 31 at 32 bits, 63 at 31 bits) and combined once as
+// S0 + 2^s * S1 mod p.  Two fp64-pipe ops per product instead of the six of
+// fmod_mul + accumulate; same canonical residues.
 #include <cstdint>
 #include <cstdlib>
 #include "ring.cuh"
 
 #ifndef HB_MAC_STAGES
 #define HB_MAC_STAGES 3   // cp.async pipeline depth of the GEMM (3 measured best: 2 % over 4)
+#endif
+#ifndef HB_MAC_BIG
+#define HB_MAC_BIG 4, 4, 4, 2   // TO, TB, WO, WB of the large tile (16 outputs x 8 clips)
 #endif
 #ifndef HB_MAC_STAGES_LONG
 #define HB_MAC_STAGES_LONG 3   // ... for term lists longer than 32 (conv layer MACs)
@@ -83,9 +94,16 @@ HB_DEV double mac_to_f(u64 x) { return u64_to_f(x); }
 // MULTI = 0: one chunk per CTA with the chunk loop and its bookkeeping
 // compiled out (the long conv-layer term lists: measured 14 % faster there
 // than the general form).
-template <int TO, int TB, int WO, int WB, int S, int EPI = 0, int MULTI = 1>
-__global__ void __launch_bounds__(256)
+// SPLIT = 1: the split partial sums above (long term lists on primes of at
+// most 34 bits: the conv-layer MACs, 37 -> 32 ms per bench step); SPLIT = 0:
+// fmod_mul per product into one accumulator with the 8 x 4 thread tile (the
+// short key-switch GEMMs, where the split form's smaller thread tile --
+// twice the accumulators -- re-reads the staged operands more and measured
+// 9 % slower).
+template <int TO, int TB, int WO, int WB, int S, int EPI = 0, int MULTI = 1, int SPLIT = 0>
+__global__ void __launch_bounds__(32 * WO * WB)
 k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
+  constexpr int NT = 32 * WO * WB;
   const int JC = MULTI ? JCrt : 1;
   HB_PDL_ENTRY();
   constexpr int OB = TO * WO, CB = TB * WB, ROWS = OB + CB;
@@ -111,7 +129,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
   const size_t prn = last ? 0 : rn;                       // pt offset of this row
   // pointer tables of this CTA's tile: ct bases [T], pt bases [OB][T]
   const u64* const* cts = g.cts + (g.cts_per_tile ? (size_t)blockIdx.y * T : 0);
-  for (int i = tid; i < T * (1 + OB); i += 256) {
+  for (int i = tid; i < T * (1 + OB); i += NT) {
     if (i < T) {
       ptab[i] = cts[i];
     } else {
@@ -130,8 +148,8 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
     const uint32_t sb = s_addr(stages + (q % S) * STAGE);
     const size_t j0 = jbase + ch * 32;
 #pragma unroll
-    for (int k = 0; k < (CHUNKS + 255) / 256; ++k) {
-      const int c = tid + k * 256;
+    for (int k = 0; k < (CHUNKS + NT - 1) / NT; ++k) {
+      const int c = tid + k * NT;
       if (c < CHUNKS) {
         const int row = c >> 4, part = c & 15;
         const u64* src;
@@ -148,7 +166,7 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
     }
     if (EPI && t == 0) {   // this chunk's scatter indices (4-byte copies)
       const uint32_t sc0 = s_addr(scbuf + (ch & 1) * OB * 32);
-      for (int c = tid; c < OB * 32; c += 256) {
+      for (int c = tid; c < OB * 32; c += NT) {
         const int o = c >> 5, oo = oc + o < O ? oc + o : O - 1;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sc0 + 4u * c),
                      "l"(g.scat[oo] + j0 + (c & 31))
@@ -189,37 +207,77 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
     for (int o = 0; o < TO; ++o)
       if (oc + os + o < O && g.c0s[oc + os + o] != nullptr) c0mask |= 1u << o;
   }
-  double acc[TO][TB];
+  // split point, reduce interval and recombination constant of this prime
+  const int pb = 64 - __clzll((long long)P.p), sbits = (pb + 1) >> 1;
+  const u64 amask = (1ull << sbits) - 1;
+  int kred = (int)(((1ull << 53) - (1ull << pb)) >> (pb + sbits));
+  kred = kred < 1 ? 1 : (kred > 1024 ? 1024 : kred);
+  const double two_s = (double)(1ull << sbits), two_sq = two_s * pinv;
+  double acc0[TO][TB], acc1[SPLIT ? TO : 1][SPLIT ? TB : 1];
 #pragma unroll
   for (int o = 0; o < TO; ++o)
 #pragma unroll
-    for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
+    for (int b = 0; b < TB; ++b) {
+      acc0[o][b] = 0.0;
+      if (SPLIT) acc1[o][b] = 0.0;
+    }
   const bool full = oc + OB <= O && bc + CB <= BC;
   int q = 0;
   for (int ch = 0; ch < JC; ++ch) {
+    int since = 0;
     for (int t = 0; t < T; ++t, ++q) {
       cp_wait<S - 2>();
       __syncthreads();                 // term q landed for every thread; stage q-1 is free
       feed(t);
       cp_commit();
       const u64* st = stages + ((MULTI ? q : t) % S) * STAGE;
-      double a[TO];
-#pragma unroll
-      for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
       double c[TB];
 #pragma unroll
       for (int b = 0; b < TB; ++b) c[b] = mac_to_f(st[(bs + b) * 32 + lane]);
+      if (SPLIT) {
+        double a0[TO], a1[TO];
 #pragma unroll
-      for (int o = 0; o < TO; ++o) {
-        const double aq = a[o] * pinv;
+        for (int o = 0; o < TO; ++o) {
+          const u64 a = st[(CB + os + o) * 32 + lane];
+          a0[o] = mac_to_f(a & amask);
+          a1[o] = mac_to_f(a >> sbits);
+        }
 #pragma unroll
-        for (int b = 0; b < TB; ++b) acc[o][b] += fmod_mul(c[b], a[o], aq, p);
-      }
-      if ((t & 255) == 255) {   // |balanced residue| < p/2: 2^9 terms fit 2^53
+        for (int o = 0; o < TO; ++o) {
 #pragma unroll
-        for (int o = 0; o < TO; ++o)
+          for (int b = 0; b < TB; ++b) {
+            acc0[o][b] = __fma_rn(c[b], a0[o], acc0[o][b]);
+            acc1[SPLIT ? o : 0][SPLIT ? b : 0] =
+                __fma_rn(c[b], a1[o], acc1[SPLIT ? o : 0][SPLIT ? b : 0]);
+          }
+        }
+        if (++since == kred) {   // the exact sums approach 2^53: back to residues
+          since = 0;
 #pragma unroll
-          for (int b = 0; b < TB; ++b) acc[o][b] = fmod_reduce(acc[o][b], p, pinv);
+          for (int o = 0; o < TO; ++o)
+#pragma unroll
+            for (int b = 0; b < TB; ++b) {
+              acc0[o][b] = fmod_reduce(acc0[o][b], p, pinv);
+              acc1[SPLIT ? o : 0][SPLIT ? b : 0] =
+                  fmod_reduce(acc1[SPLIT ? o : 0][SPLIT ? b : 0], p, pinv);
+            }
+        }
+      } else {
+        double a[TO];
+#pragma unroll
+        for (int o = 0; o < TO; ++o) a[o] = mac_to_f(st[(CB + os + o) * 32 + lane]);
+#pragma unroll
+        for (int o = 0; o < TO; ++o) {
+          const double aq = a[o] * pinv;
+#pragma unroll
+          for (int b = 0; b < TB; ++b) acc0[o][b] += fmod_mul(c[b], a[o], aq, p);
+        }
+        if ((t & 255) == 255) {   // |balanced residue| < p/2: 2^9 terms fit 2^53
+#pragma unroll
+          for (int o = 0; o < TO; ++o)
+#pragma unroll
+            for (int b = 0; b < TB; ++b) acc0[o][b] = fmod_reduce(acc0[o][b], p, pinv);
+        }
       }
     }
     if (EPI && c0term) {               // + P * c0 on the outputs that take it
@@ -234,9 +292,28 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
         const double c = mac_to_f(st[(bs + b) * 32 + lane]);
 #pragma unroll
         for (int o = 0; o < TO; ++o)
-          if ((c0mask >> o) & 1) acc[o][b] += fmod_mul(c, pm, pmq, p);
+          if ((c0mask >> o) & 1) {
+            if (SPLIT) acc0[o][b] = fmod_reduce(acc0[o][b], p, pinv);
+            acc0[o][b] += fmod_mul(c, pm, pmq, p);
+          }
       }
     }
+    // S0 + 2^s * S1 mod p, balanced
+    double acc[TO][TB];
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+#pragma unroll
+      for (int b = 0; b < TB; ++b) {
+        if (SPLIT) {
+          acc[o][b] = fmod_reduce(acc0[o][b], p, pinv)
+                      + fmod_mul(fmod_reduce(acc1[SPLIT ? o : 0][SPLIT ? b : 0], p, pinv), two_s,
+                                 two_sq, p);
+          acc1[SPLIT ? o : 0][SPLIT ? b : 0] = 0.0;
+        } else {
+          acc[o][b] = acc0[o][b];
+        }
+        acc0[o][b] = 0.0;
+      }
     // ---- chunk done: store its outputs, restart the accumulators
     const int j0 = jbase + ch * 32;
     const size_t rj = rn + j0 + lane;
@@ -276,28 +353,22 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
         }
       }
     }
-    if (ch + 1 < JC) {
-#pragma unroll
-      for (int o = 0; o < TO; ++o)
-#pragma unroll
-        for (int b = 0; b < TB; ++b) acc[o][b] = 0.0;
-    }
   }
   cp_wait<0>();
 }
 
-template <int TO, int TB, int WO, int WB, int S, int EPI = 0>
+template <int TO, int TB, int WO, int WB, int S, int EPI = 0, int SPLIT = 0>
 cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cudaStream_t st) {
   constexpr int OB = TO * WO, CB = TB * WB;
   const size_t smem = (size_t)S * (OB + CB) * 32 * 8 + (EPI ? 2 * OB * 32 * 4 : 0)
       + sizeof(void*) * (size_t)g.nterms * (1 + OB);
   if (smem > 220 * 1024) return cudaErrorNotSupported;   // caller falls back
   static int smem_cur = 0, smem_cur1 = 0;
-  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 1>, (int)((int)smem), &smem_cur);
+  cudaError_t e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 1, SPLIT>, (int)((int)smem), &smem_cur);
   if (e == cudaSuccess)
-    e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 0>, (int)((int)smem), &smem_cur1);
+    e = smem_attr_once((const void*)k_mac_pipe<TO, TB, WO, WB, S, EPI, 0, SPLIT>, (int)((int)smem), &smem_cur1);
   if (e != cudaSuccess) return e;
-  dim3 block(32, 8);
+  dim3 block(32, WO * WB);
   const int tiles = ((BC + CB - 1) / CB) * ((g.nout + OB - 1) / OB) * R;
   // coefficient chunks per CTA: as many as still leave >= 8 CTAs per SM
   int jc = mac_jc();
@@ -309,9 +380,9 @@ cudaError_t mac_pipe_t(const HbMacGroupP& g, const HbRing& RG, int R, int BC, cu
   while (jc > 1 && (RG.n / 32) % jc) jc >>= 1;
   dim3 grid((BC + CB - 1) / CB, (g.nout + OB - 1) / OB, R * (RG.n / 32 / jc));
   if (jc > 1)
-    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 1>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, jc);
+    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 1, SPLIT>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, jc);
   else
-    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 0>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, 1);
+    (void)hb_launch(k_mac_pipe<TO, TB, WO, WB, S, EPI, 0, SPLIT>, dim3(grid), dim3(block), smem, st, g, RG, R, BC, 1);
   return cudaGetLastError();
 }
 
@@ -337,12 +408,15 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   // output tile sized to the layer so no warp idles on absent outputs
   if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, S>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, S>(g, RG, rows, BC, st);
+  // long term lists (conv layers) on small primes: split partial sums, 4
+  // outputs x 4 clips per thread (32 accumulator doubles), tile HB_MAC_BIG
+  if (g.nterms > 32 && RG.split_ok && g.nout > 4) {
+    if (g.nout <= 8) return mac_pipe_t<4, 4, 2, 4, HB_MAC_STAGES_LONG, 0, 1>(g, RG, rows, BC, st);
+    return mac_pipe_t<HB_MAC_BIG, HB_MAC_STAGES_LONG, 0, 1>(g, RG, rows, BC, st);
+  }
   if (g.nout <= 8) return mac_pipe_t<8, 4, 1, 8, S>(g, RG, rows, BC, st);
   // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
-  // operand feeds twice the products of the 4x4 tile; measured +1.6 % on
-  // the bench step (hoisted key-switch GEMM and conv MAC) over 4x4 and 4x8
-  // (round-1 tile sweep).  Long term lists (conv layers) may take a deeper
-  // pipeline (HB_MAC_STAGES_LONG)
+  // operand feeds twice the products of the 4x4 tile (round-1 tile sweep)
   if (g.nterms > 32) return mac_pipe_t<8, 4, 2, 4, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
   return mac_pipe_t<8, 4, 2, 4, S>(g, RG, rows, BC, st);
 }

@@ -52,6 +52,7 @@ struct HbRing {
   int n;
   int nprimes;
   int use_f64;            // every prime < 2^42: transforms run on the fp64 pipe
+  int split_ok;           // every prime < 2^34: mac.cu may sum split products exactly
   const HbPrime* primes;  // [nprimes]
   const HbTw* tw_fwd;     // [nprimes][n]  psi^brv(j)            (ring.py:281)
   const HbTw* tw_inv;     // [nprimes][n]  psi^-brv(j)  (true inverse)
