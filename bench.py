@@ -244,10 +244,100 @@ def reference_arm(args):
 FP64_MEASURED_TFLOPS = 17.93   # DFMA/s measured on this pool (profiles/r01_microbench.txt)
 
 
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2b_roofline_traffic.json")
 
 
 def dominant_kernel_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
+    """The kernel with the largest share of the step (step_roofline families,
+    profiles/r2b_launches_summary.txt): k_ks3, the fused ModUp + key-switch
+    inner product of every non-hoisted key switch.  Engines without it
+    (integer-policy rings) report the rotation ModDown as before."""
+    if getattr(be, "fuse_ks", False):
+        return fused_ks_roofline(be, lvl, bsz, peaks)
+    return moddown_roofline(be, lvl, bsz, peaks)
+
+
+def fused_ks_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
+    """Time one k_ks3 launch -- the relinearisation key switch of bsz clips at
+    level lvl: bsz x (lvl+2) clusters, each the (lvl) forward NTTs of the
+    lifted digits under one target prime plus the products with the two key
+    rows, sums in tensor memory -- with CUDA events on the launching stream.
+
+    Algorithmic work per launch: bytes = digit coefficient
+    rows + their NTT-form identity rows (8N each, once per ciphertext) + the
+    key rows (2 x digits x rows, once) + the 2 x rows outputs per ciphertext;
+    fp64-pipe instructions = 8 per butterfly of every lift + 6 per modular
+    product.  The kernel is bound by the fp64 pipe (its HBM bytes are the
+    inputs and outputs only), so `achieved`/`peak` are fp64 instruction rates
+    and the HBM side is reported beside them.  `traffic` = DRAM read+write of
+    the same launch from an ncu --set full capture (tools/roofline_probe.py)."""
+    import torch
+    from paper_2104_09164_b200 import _native as nat
+    from paper_2104_09164_b200.ckks.engine import _Digits
+    from paper_2104_09164_b200.ckks.ring import _upload
+    n, logn = be.n, be.n.bit_length() - 1
+    ndig, rows = lvl + 1, lvl + 2
+    g = torch.Generator(device=be.dev).manual_seed(1)
+    src = be.ring.empty(bsz, ndig).random_(0, 1 << 30, generator=g)
+    coef = (be.ring.empty(bsz, ndig).random_(0, 1 << 30, generator=g) - (1 << 29)) \
+        .to(torch.float64).view(torch.int64)
+    ip = be.ring.empty(bsz * 2, rows)
+    rp = be.ring.row_ptrs
+    key = be.keys.relin
+    if key is None:   # a receiver without keys: any resident rows serve as key rows
+        raise RuntimeError("roofline probe needs the relinearisation key")
+    krow = np.array(list(range(lvl + 1)) + [key.lmax + 1])
+    kbr = rp(key.b).reshape(key.b.shape[0], key.lmax + 2)[0, krow]
+    kar = rp(key.a).reshape(key.a.shape[0], key.lmax + 2)[0, krow]
+    de = _Digits(coef, rp(src).reshape(bsz, ndig), lvl)
+    t = be._ksf_tasks(de, lvl, [(kbr, kar, (key.lmax + 2) * n, 0)],
+                      rp(ip).reshape(1, bsz, 2, rows), bsz)
+    d = _upload(t, be.dev)
+    L = nat.lib()
+    st = torch.cuda.current_stream()
+
+    def launch():
+        nat.check(L.hb_ks_fused(be.ring.handle, d.data_ptr(), len(t), st.cuda_stream), "ks_fused")
+    for _ in range(3):
+        launch()
+    reps = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        launch()
+    e1.record(st)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / reps
+    algo = (2 * bsz * ndig + 2 * ndig * rows + 2 * bsz * rows) * 8 * n
+    lifts = bsz * (rows * ndig - ndig)
+    bfly = lifts * (n // 2) * logn
+    fp64_ops = bfly * 8 + 2 * bsz * rows * ndig * n * 6
+    gbs = algo / sec / 1e9
+    peak_hbm = peaks.get("hbm_gbs", 6650.0)
+    fp64_frac = fp64_ops / sec / (FP64_MEASURED_TFLOPS * 1e12)
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            tr = json.load(f)
+        if tr.get("kernel") == "k_ks3" and tr.get("tasks") == len(t) and tr.get("n") == n:
+            traffic = tr["dram_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"kernel": "k_ks3 (fused ModUp + key-switch inner product, sums in tensor memory)",
+            "bound": "fp64", "achieved": round(fp64_ops / sec / 1e12, 3),
+            "peak": FP64_MEASURED_TFLOPS, "unit": "T fp64-pipe instr/s",
+            "frac": round(fp64_frac, 4), "traffic": traffic, "launch_us": round(sec * 1e6, 2),
+            "tasks_per_launch": len(t), "digits": ndig,
+            "algorithmic_bytes_per_launch": algo, "fp64_ops_per_launch": fp64_ops,
+            "hbm_achieved_gbs": round(gbs, 1), "hbm_peak_gbs": peak_hbm,
+            "hbm_frac": round(gbs / peak_hbm, 4),
+            "butterflies_per_s": round(bfly / sec / 1e12, 3),
+            "peak_source": "fp64: measured DFMA rate on this pool (profiles/r01_microbench.txt); "
+                           "hbm: " + ("MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback")}
+
+
+def moddown_roofline(be, lvl: int, bsz: int, peaks: dict) -> dict:
     """Time one rotation ModDown launch -- k_ntt3_fwd<FWD_MODDOWN_SCATTER>, the
     largest kernel share of the evaluation (profiles/r01_launches_*): the
     ModDown of bsz clips x 2 components x (l+1) rows of a rotation computed on
@@ -370,7 +460,8 @@ def step_roofline(enc, ct, be, run_pipeline, ms_graph: float, peaks: dict) -> di
             "hbm_frac": round(tot_b / sec / 1e9 / peak, 4),
             "fp64_frac": round(tot_f / sec / fp64_peak, 4),
             "eager_step_device_ms": round(tot_ms, 3), "graph_ms_per_step": round(ms_graph, 3),
-            "fp64_ops_note": "8 per NTT butterfly, 6 per modular product (fmod_mul + accumulate)",
+            "fp64_ops_note": "8 per NTT butterfly, 6 per modular product (fmod_mul + accumulate), "
+                             "3 per product of the split-sum layer MAC",
             "families": fams}
 
 

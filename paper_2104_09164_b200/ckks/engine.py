@@ -215,6 +215,8 @@ class CkksBackend(BackendBase):
         # one per rotation).  HEAR_B200_LAZY_MODDOWN=0 restores the eager path.
         self.lazy = (os.environ.get("HEAR_B200_LAZY_MODDOWN", "1") == "1" and self.ring.use_f64
                      and self.preperm and self.lift_once)
+        # smallest batch that takes the lazy form (its inner product is the GEMM)
+        self.lazy_min = int(os.environ.get("HEAR_B200_LAZY_MIN", str(self.ks_gemm_min)))
         self._pmod_dev = self._dev(self._pmod)
         # non-hoisted key switches (relinearisation, rot_each, rotate-and-add)
         # run ModUp and the inner product in ONE kernel (k_ks3: transforms in
@@ -721,21 +723,7 @@ class CkksBackend(BackendBase):
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
         if fused:
-            # ModUp + inner product in one kernel: one task per (job, clip, row)
-            t = np.zeros((nj, bsz, rows), dtype=nat.KSF_TASK)
-            cr = rp(de.coef).reshape(de.coef.shape[0], ndig)
-            ident = np.zeros((de.src.shape[0], rows), dtype=np.uint64)
-            ident[:, :ndig] = de.src
-            for j, (kbr, kar, kds, off) in enumerate(parts):
-                t["coef"][j] = cr[off:off + bsz, 0][:, None]
-                t["ident"][j] = ident[off:off + bsz]
-                t["kb"][j], t["ka"][j] = kbr[None, :], kar[None, :]
-                t["key_dstride"][j] = kds
-            t["out_b"], t["out_a"] = ipr[:, :, 0], ipr[:, :, 1]
-            t["ndig"] = ndig
-            t["dst_prime"] = gidx[None, None, :]
-            t["ident_digit"] = np.array(list(range(ndig)) + [-1])[None, None, :]
-            self.ring.ks_fused(t.ravel())
+            self.ring.ks_fused(self._ksf_tasks(de, lvl, parts, ipr, bsz))
         elif natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
             # every natural-order inner product in ONE GEMM launch: a hoisted
             # group shares its digit set, rot_each / relinearisation jobs bring
@@ -857,6 +845,29 @@ class CkksBackend(BackendBase):
                         self._ew(nat.EW_ADD, dst.ravel(), dst.ravel(), post[j].ravel(),
                                  primes=np.tile(np.arange(r), bsz * 2))
         return res
+
+    def _ksf_tasks(self, de: "_Digits", lvl: int, parts, ipr, bsz: int) -> np.ndarray:
+        """Task table of the fused ModUp + inner product (k_ks3): one task per
+        (job, clip, target row).  parts[j] = (key b row pointers [lvl+2], key a
+        row pointers, key digit stride in elements, clip offset into de);
+        ipr [nj, bsz, 2, lvl+2] output row pointers."""
+        ndig, rows = lvl + 1, lvl + 2
+        nj = len(parts)
+        gidx = np.array(list(range(lvl + 1)) + [self.S])
+        t = np.zeros((nj, bsz, rows), dtype=nat.KSF_TASK)
+        cr = self.ring.row_ptrs(de.coef).reshape(de.coef.shape[0], ndig)
+        ident = np.zeros((de.src.shape[0], rows), dtype=np.uint64)
+        ident[:, :ndig] = de.src
+        for j, (kbr, kar, kds, off) in enumerate(parts):
+            t["coef"][j] = cr[off:off + bsz, 0][:, None]
+            t["ident"][j] = ident[off:off + bsz]
+            t["kb"][j], t["ka"][j] = kbr[None, :], kar[None, :]
+            t["key_dstride"][j] = kds
+        t["out_b"], t["out_a"] = ipr[:, :, 0], ipr[:, :, 1]
+        t["ndig"] = ndig
+        t["dst_prime"] = gidx[None, None, :]
+        t["ident_digit"] = np.array(list(range(ndig)) + [-1])[None, None, :]
+        return t.ravel()
 
     def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs, rot=None):
         """Natural-order key-switch inner products of several jobs as one
@@ -1315,7 +1326,7 @@ class CkksBackend(BackendBase):
 
     def _lazy_ok(self, cts) -> bool:
         lvl, bsz = cts[0].level, cts[0].payload.batch
-        return (self.lazy and bsz >= self.ks_gemm_min
+        return (self.lazy and bsz >= self.lazy_min
                 and all(c.level == lvl and c.payload.batch == bsz for c in cts))
 
     def _raw_rot_many_each_lazy(self, cts, ks, want0: bool) -> list:

@@ -104,6 +104,7 @@ class StepStats:
 
     FP64_PER_BUTTERFLY = 8   # fmod_mul (5) + add + sub + conditional correction
     FP64_PER_MODMUL = 6      # fmod_mul (5) + accumulate
+    FP64_PER_SPLITMUL = 3    # mac.cu split sums: 2 DFMA + operand conversions / reductions
 
     def __init__(self, timed: bool = False):
         self.timed = timed
@@ -387,8 +388,17 @@ class RingContext:
             if _STATS:   # ct terms [bc, rows, N] once, pt rows once, outputs
                 _STATS.end("layer_mac_gemm", e0)
                 nbytes = (_uniq(cts) * bc + _uniq(pts) + nout * bc) * rows * 8 * self.n
-                _STATS.add("layer_mac_gemm", nbytes, nout * nterms * bc * rows * self.n
-                           * StepStats.FP64_PER_MODMUL)
+                # long term lists on small primes take the split partial sums:
+                # 2 DFMA per product + conversions and periodic reductions
+                per = StepStats.FP64_PER_SPLITMUL if (nterms > 32 and nout > 4 and self.split_ok) \
+                    else StepStats.FP64_PER_MODMUL
+                _STATS.add("layer_mac_gemm", nbytes, nout * nterms * bc * rows * self.n * per)
+
+    @property
+    def split_ok(self) -> bool:
+        """mac.cu sums split products exactly (every prime below 2^34)."""
+        return (self.use_f64 and max(self.primes) < (1 << 34)
+                and os.environ.get("HEAR_B200_MAC_SPLIT", "1") != "0")
 
     @property
     def use_f64(self) -> bool:

@@ -28,8 +28,7 @@ if a.write:
     def get(k):
         return float(v[h.index(k)].replace(",", "")) * scale.get(u[h.index(k)], 1)
     rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
-    rows = 2 * a.batch * (ps.max_level + 1)
-    out = {"kernel": "k_ntt3_fwd<FWD_MODDOWN_SCATTER>", "rows": rows, "n": ps.n,
+    out = {"kernel": "k_ks3", "tasks": a.batch * (ps.max_level + 2), "n": ps.n,
            "dram_bytes": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
            "duration_under_ncu": v[h.index("gpu__time_duration.sum")] + " " + u[h.index("gpu__time_duration.sum")],
            "source": os.path.basename(a.write)}
@@ -40,5 +39,5 @@ else:
     from paper_2104_09164_b200.ckks.engine import CkksBackend
     from paper_2104_09164_b200.ckks.params import gen_params
     ps = gen_params("fast-hear")
-    be = CkksBackend(ps, seed=0, keygen=False)
+    be = CkksBackend(ps, seed=0)
     print(bench.dominant_kernel_roofline(be, lvl=ps.max_level, bsz=a.batch, peaks={}))
