@@ -162,6 +162,16 @@ int hb_ks_gemm_rot(hb_ring* ring, const void* de, const void* keys, const void* 
 int hb_mac_shared_ext(hb_ring* ring, const void* cts, const void* pts, const void* pts_last,
                       const void* dsts, int nterms, int nout, int rows, int bc, int prime_last,
                       void* stream);
+/* Rotate-and-sum ct + sum_j rot_j(ct) of one hoisted group, in the extended
+ * basis and without materialising the rotations (hear/fastpath.py:141-154
+ * rotate_sum_each's odd part; each rotation engine.py:328-351): HbRotSumTask
+ * per (handle, output row), HbRotSumRot per amount (Galois gather map,
+ * reference-layout key components); nb clips per task, ndig digits:
+ *   out_b[m] = P (c0[m] + sum_j c0[pi_j m]) + sum_j sum_i de_i[pi_j m] kb_ij[m]
+ *   out_a[m] = P  c1[m]                     + sum_j sum_i de_i[pi_j m] ka_ij[m]
+ * (no P terms on the special row).  The caller divides P out once.           */
+int hb_rot_sum(hb_ring* ring, const void* tasks, int ntasks, const void* rots, int nrot,
+               int ndig, int nb, void* stream);
 /* Fused ModUp + key-switch inner product for non-hoisted key switches
  * (relinearisation, rot_each, rotate-and-add; engine.py:290-326 digit
  * expansion + ring.py:136-156 inner product in ONE kernel): one HbKsfTask per

@@ -51,6 +51,7 @@ def lib():
         L.hb_ks_gemm_rot.argtypes = [vp] * 9 + [i32] * 4 + [ctypes.c_longlong] * 3 + [i32, vp]
         L.hb_mac_shared_ext.argtypes = [vp] * 5 + [i32] * 5 + [vp]
         L.hb_ks_fused.argtypes = [vp, vp, i32, vp]
+        L.hb_rot_sum.argtypes = [vp, vp, i32, vp, i32, i32, i32, vp]
         L.hb_ew.argtypes = [vp, i32, vp, i32, vp]
         L.hb_tensor.argtypes = [vp, vp, i32, vp]
         L.hb_mac_strided.argtypes = [vp, vp, i32, vp, i32, i32, vp]
@@ -124,6 +125,13 @@ KSF_TASK = np.dtype([("coef", "<u8"), ("ident", "<u8"), ("kb", "<u8"), ("ka", "<
                      ("ndig", "<i4"), ("dst_prime", "<i4"), ("ident_digit", "<i4"),
                      ("_pad", "<i4")])
 
+ROTSUM_TASK = np.dtype([("de", "<u8"), ("c0", "<u8"), ("c1", "<u8"), ("out_b", "<u8"),
+                        ("out_a", "<u8"), ("de_bstride", "<i8"), ("de_dstride", "<i8"),
+                        ("c_bstride", "<i8"), ("out_bstride", "<i8"), ("pmod", "<u8"),
+                        ("prime", "<i4"), ("row", "<i4")])
+ROTSUM_ROT = np.dtype([("perm", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("key_dstride", "<i8"),
+                       ("special_row", "<i4"), ("_pad", "<i4")])
+
 # NTT fused modes (csrc/ntt.cu FwdMode)
 FWD_PLAIN, FWD_LIFT, FWD_MODDOWN, FWD_I64, FWD_MODDOWN_SCATTER, FWD_MODDOWN2 = 0, 1, 2, 3, 4, 5
 # element-wise ops (csrc/ops.cu EwOp)
@@ -134,7 +142,7 @@ EW_ADD, EW_SUB, EW_MUL, EW_MUL_SCALAR, EW_MULADD, EW_ADD_SCALED, EW_COPY, EW_PER
 def _check_layouts():
     L = _lib
     for kind, dt in enumerate((NTT_TASK, EW_TASK, MAC_TASK, MAC_TERM, None, KS_TASK2,
-                               BCONV_TASK, KSF_TASK)):
+                               BCONV_TASK, KSF_TASK, ROTSUM_TASK, ROTSUM_ROT)):
         if dt is not None and L.hb_sizeof_task(kind) != dt.itemsize:
             raise NativeError(f"task layout {kind} mismatch: C {L.hb_sizeof_task(kind)} "
                               f"vs numpy {dt.itemsize}")

@@ -1379,6 +1379,51 @@ class CkksBackend(BackendBase):
                 out[h][k] = Ct(CtExt(xr[h, q]), lvl, c.scale, self.n2)
         return out
 
+    def _rot_sum_ok(self, cts, ks) -> bool:
+        """ct + sum of distinct non-zero rotations, one ModDown (k_rot_sum_f64)."""
+        nz = [k for k in ks if k]
+        return (self._lazy_ok(cts) and ks.count(0) == 1 and len(set(nz)) == len(nz)
+                and os.environ.get("HEAR_B200_ROT_SUM", "1") == "1")
+
+    def _raw_rot_sum_each(self, cts, ks) -> list:
+        """[ct + sum_k rot(ct, k)]: the digit expansion of every handle, then
+        ONE kernel per level group that gathers the digits through each
+        amount's Galois map, multiplies by the (reference-layout) key rows and
+        sums in the extended basis -- no rotation is materialised -- and one
+        ModDown per handle."""
+        ks = [k for k in ks if k]
+        lvl, bsz = cts[0].level, cts[0].payload.batch
+        r, rows, ndig = lvl + 1, lvl + 2, lvl + 1
+        nh = len(cts)
+        rp = self.ring.row_ptrs
+        ctr = np.stack([rp(c.payload.data).reshape(bsz, 2, r) for c in cts])   # [nh, bsz, 2, r]
+        de = self._decompose(ctr[:, :, 1].reshape(nh * bsz, r), lvl)
+        der = rp(de).reshape(nh, bsz, ndig, rows)
+        acc = self.ring.empty(nh, bsz, 2, rows)
+        accr = rp(acc).reshape(nh, bsz, 2, rows)
+        rots = np.zeros(len(ks), dtype=nat.ROTSUM_ROT)
+        for q, k in enumerate(ks):
+            key = self._rot_key(k)
+            if key.lmax < lvl:
+                raise LevelScaleError(f"key switching key trimmed to level {key.lmax}, need {lvl}")
+            rots[q] = (self.ring.perm_dev(self.ring.galois_element(k)).data_ptr(),
+                       key.b.data_ptr(), key.a.data_ptr(), (key.lmax + 2) * self.n,
+                       key.lmax + 1, 0)
+        t = np.zeros((nh, rows), dtype=nat.ROTSUM_TASK)
+        t["de"] = der[:, 0, 0, :]
+        t["c0"][:, :r], t["c1"][:, :r] = ctr[:, 0, 0, :], ctr[:, 0, 1, :]
+        t["out_b"], t["out_a"] = accr[:, 0, 0, :], accr[:, 0, 1, :]
+        t["de_bstride"], t["de_dstride"] = ndig * rows * self.n, rows * self.n
+        t["c_bstride"], t["out_bstride"] = 2 * r * self.n, 2 * rows * self.n
+        t["pmod"][:, :r] = self._pmod[:r][None, :]
+        t["prime"] = np.array(list(range(r)) + [self.S])[None, :]
+        t["row"] = np.array(list(range(r)) + [-1])[None, :]
+        self.ring.rot_sum(t.ravel(), rots, ndig, bsz)
+        del de
+        res = self._mod_down_ext(acc.reshape(nh * bsz, 2, rows, self.n), lvl)
+        res = res.reshape(nh, bsz, 2, r, self.n)
+        return [Ct(CtData(res[h]), lvl, c.scale, self.n2) for h, c in enumerate(cts)]
+
     def _raw_rot_many(self, a: Ct, ks) -> dict:
         if not ks:
             return {}

@@ -467,6 +467,21 @@ class RingContext:
                     + 2 * int(ndig.sum()) * self.n * StepStats.FP64_PER_MODMUL
                 _STATS.add("keyswitch_fused", nbytes, fp64)
 
+    def rot_sum(self, tasks: np.ndarray, rots: np.ndarray, ndig: int, nb: int):
+        """ct + sum_j rot_j(ct) in the extended basis (csrc/ops.cu k_rot_sum_f64)."""
+        if len(tasks):
+            d, r = _upload(tasks, self.device), _upload(rots, self.device)
+            e0 = _STATS.begin() if _STATS else None
+            nat.check(self._lib.hb_rot_sum(self.handle, _ptr(d), len(tasks), _ptr(r), len(rots),
+                                           ndig, nb, self.stream), "rot_sum")
+            if _STATS:   # digit rows and c rows once, key rows once, two outputs per task
+                _STATS.end("rot_sum", e0)
+                m = len(tasks)
+                nrows = len(set(tasks["prime"].tolist()))
+                nbytes = (m * nb * (ndig + 4) + 2 * len(rots) * ndig * nrows) * 8 * self.n
+                _STATS.add("rot_sum", nbytes, 2 * m * nb * len(rots) * ndig * self.n
+                           * StepStats.FP64_PER_MODMUL)
+
     def ks_inner2(self, tasks: np.ndarray, nb: int):
         if len(tasks):
             d = _upload(tasks, self.device)

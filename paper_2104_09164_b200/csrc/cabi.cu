@@ -46,6 +46,8 @@ cudaError_t launch_ks_gemm(const void*, const void*, const void*, const void*, i
                            const void* pmod = nullptr);
 cudaError_t launch_ks_inner2(const void*, int, int, const HbPrime*, int, cudaStream_t);
 cudaError_t launch_ks3(const HbKsfTask*, int, const HbRing&, cudaStream_t);
+cudaError_t launch_rot_sum(const void*, int, const void*, int, int, int, const HbPrime*, int,
+                           cudaStream_t);
 cudaError_t launch_bconv(const void*, int, int, const HbPrime*, int, cudaStream_t);
 int bconv_task_size();
 cudaError_t launch_lift_center(const u64*, u64, long long*, int, cudaStream_t);
@@ -257,6 +259,8 @@ int hb_sizeof_task(int kind) {
     case 5: return (int)sizeof(HbKsTask2);
     case 6: return bconv_task_size();
     case 7: return (int)sizeof(HbKsfTask);
+    case 8: return (int)sizeof(HbRotSumTask);
+    case 9: return (int)sizeof(HbRotSumRot);
     default: return -1;
   }
 }
@@ -356,6 +360,15 @@ int hb_ks_gemm_rot(hb_ring* r, const void* de, const void* keys, const void* key
                                  de_bstride, dst_bstride, prime_last, 0, (cudaStream_t)stream,
                                  scat, c0s, c0, c0_bstride, pmod);
   return e ? fail(e, "hb_ks_gemm_rot") : 0;
+}
+
+// Rotate-and-sum of hoisted rotations in the extended basis (ops.cu).
+int hb_rot_sum(hb_ring* r, const void* tasks, int ntasks, const void* rots, int nrot, int ndig,
+               int nb, void* stream) {
+  if (!r->dev.use_f64) return fail(cudaErrorNotSupported, "hb_rot_sum: fp64 rings only");
+  cudaError_t e = launch_rot_sum(tasks, ntasks, rots, nrot, ndig, nb, r->dev.primes, r->dev.n,
+                                 (cudaStream_t)stream);
+  return e ? fail(e, "hb_rot_sum") : 0;
 }
 
 // Fused ModUp + key-switch inner product (ntt3.cu k_ks3, TMEM accumulators).

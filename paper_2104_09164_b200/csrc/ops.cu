@@ -824,6 +824,92 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
   return cudaGetLastError();
 }
 
+// Rotate-and-sum of hoisted rotations in the extended basis Q*P
+// (hear/fastpath.py:141-154 rotate_sum_each's odd part: ct + sum_j rot_j(ct),
+// each rotation engine.py:328-351) WITHOUT materialising the rotations:
+//   out_b[m] = P*(c0[m] + sum_j c0[pi_j(m)]) + sum_j sum_i d_i[pi_j(m)] * Kb_ij[m]
+//   out_a[m] = P* c1[m]                      + sum_j sum_i d_i[pi_j(m)] * Ka_ij[m]
+// on every chain row and (without the P terms) the special row; the caller
+// divides P out once.  The digits are gathered through the Galois map (it
+// permutes aligned 32-element blocks onto aligned blocks, so the gathers are
+// sector-exact), the keys are read in place (shared by the 8 clips of a CTA
+// through L1).  The unfused form wrote one extended rotation per amount and
+// re-read them all for the sum.
+__global__ void __launch_bounds__(256)
+k_rot_sum_f64(const HbRotSumTask* __restrict__ tasks, const HbRotSumRot* __restrict__ rots,
+              int nrot, int ndig, const HbPrime* __restrict__ primes, int n, int nb) {
+  HB_PDL_ENTRY();
+  const HbRotSumTask tk = tasks[blockIdx.y];
+  const int b = blockIdx.x * blockDim.y + threadIdx.y;
+  const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
+  if (j >= n || b >= nb) return;
+  const HbPrime P = primes[tk.prime];
+  const double p = P.pd, pinv = P.pinv;
+  const u64* de = tk.de + b * tk.de_bstride;
+  const bool chain = tk.row >= 0;
+  double b0 = 0, b1 = 0, a0 = 0, a1 = 0;
+  u64 s0 = 0, s1 = 0, t0 = 0, t1 = 0;   // sums of c0 terms / the identity's c1
+  if (chain) {
+    const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(tk.c0 + b * tk.c_bstride + j));
+    const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(tk.c1 + b * tk.c_bstride + j));
+    s0 = v0.x; s1 = v0.y; t0 = v1.x; t1 = v1.y;
+  }
+  for (int q = 0; q < nrot; ++q) {
+    const HbRotSumRot rt = rots[q];
+    const int2 pp = __ldg(reinterpret_cast<const int2*>(rt.perm + j));
+    if (chain) {
+      s0 += __ldg(tk.c0 + b * tk.c_bstride + pp.x);
+      s1 += __ldg(tk.c0 + b * tk.c_bstride + pp.y);
+    }
+    const size_t krow = (size_t)(chain ? tk.row : rt.special_row) * n + j;
+    const u64* kbp = rt.kb + krow;
+    const u64* kap = rt.ka + krow;
+#pragma unroll 2
+    for (int i = 0; i < ndig; ++i) {
+      const u64* d = de + i * tk.de_dstride;
+      const double x0 = u64_to_f(__ldg(d + pp.x)), x1 = u64_to_f(__ldg(d + pp.y));
+      const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(kbp + i * rt.key_dstride));
+      const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(kap + i * rt.key_dstride));
+      const double q0 = x0 * pinv, q1 = x1 * pinv;
+      b0 += fmod_mul(u64_to_f(kb.x), x0, q0, p);
+      b1 += fmod_mul(u64_to_f(kb.y), x1, q1, p);
+      a0 += fmod_mul(u64_to_f(ka.x), x0, q0, p);
+      a1 += fmod_mul(u64_to_f(ka.y), x1, q1, p);
+    }
+    if ((q & 63) == 63) {   // balanced sums stay far below 2^53
+      b0 = fmod_reduce(b0, p, pinv); b1 = fmod_reduce(b1, p, pinv);
+      a0 = fmod_reduce(a0, p, pinv); a1 = fmod_reduce(a1, p, pinv);
+    }
+  }
+  if (chain) {   // + P * (sums of c0 / the identity's c1); sums < 2^45
+    const double pm = u64_to_f(tk.pmod), pmq = pm * pinv;
+    b0 += fmod_mul(u64_to_f(s0), pm, pmq, p);
+    b1 += fmod_mul(u64_to_f(s1), pm, pmq, p);
+    a0 += fmod_mul(u64_to_f(t0), pm, pmq, p);
+    a1 += fmod_mul(u64_to_f(t1), pm, pmq, p);
+  }
+  ulonglong2 rb, ra;
+  rb.x = fmod_canon(b0, p, pinv);
+  rb.y = fmod_canon(b1, p, pinv);
+  ra.x = fmod_canon(a0, p, pinv);
+  ra.y = fmod_canon(a1, p, pinv);
+  *reinterpret_cast<ulonglong2*>(tk.out_b + b * tk.out_bstride + j) = rb;
+  *reinterpret_cast<ulonglong2*>(tk.out_a + b * tk.out_bstride + j) = ra;
+}
+
+cudaError_t launch_rot_sum(const void* tasks, int ntasks, const void* rots, int nrot, int ndig,
+                           int nb, const HbPrime* primes, int n, cudaStream_t st) {
+  if (ntasks <= 0 || nb <= 0) return cudaSuccess;
+  if (nrot > 1024) return cudaErrorInvalidValue;   // c0 sums must stay below 2^45
+  const int by = nb < 8 ? nb : 8;
+  dim3 block(32, by);
+  dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
+  (void)hb_launch(k_rot_sum_f64, dim3(grid), dim3(block), 0, st,
+                  reinterpret_cast<const HbRotSumTask*>(tasks),
+                  reinterpret_cast<const HbRotSumRot*>(rots), nrot, ndig, primes, n, nb);
+  return cudaGetLastError();
+}
+
 // Many-term modular sums: dst = sum_k srcs[term_off + k] (mod p) per row task
 // (HbMacTask layout, pt unused) -- the left-to-right add chains of sum_each
 // (hear/fastpath.py rotate-and-sum / FC partial sums, ring.py:159 pw_add) in

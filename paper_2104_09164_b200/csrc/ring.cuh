@@ -169,6 +169,28 @@ struct HbFftTables {
   const int* slot_of;   // [n2]:   DFT bin m -> slot j with m_j = m (inverse of m_j)
 };
 
+// Rotate-and-sum in the extended basis (ops.cu k_rot_sum_f64): one output row
+// of one handle, and one entry per rotation amount of the group.
+struct HbRotSumTask {
+  const u64* de;     // clip 0, digit 0, this row of the digit expansion
+  const u64* c0;     // clip 0, this row of c0 / c1 (null on the special row)
+  const u64* c1;
+  u64* out_b;        // clip 0, this row of the two output components
+  u64* out_a;
+  long long de_bstride, de_dstride, c_bstride, out_bstride;
+  u64 pmod;          // P mod p_row
+  int prime;
+  int row;           // chain row index, or -1 for the special row
+};
+struct HbRotSumRot {
+  const int* perm;   // rotated[m] = in[perm[m]]
+  const u64* kb;     // digit 0, row 0 of the (reference-layout) key components
+  const u64* ka;
+  long long key_dstride;
+  int special_row;   // row index of the key's special row
+  int _pad;
+};
+
 // Clip-blocked key-switch inner product task (ops.cu k_ks_inner2).
 struct HbKsTask2 {
   const u64* de;      // clip 0, digit 0, row r

@@ -202,3 +202,24 @@ def test_merged_moddown_rescale_bit_identical(setup):
     assert (want.level, want.scale) == (got.level, got.scale)
     assert torch.equal(want.payload.data, got.payload.data)
     assert be.counters.total()["rescale"] == 1
+
+
+def test_rot_sum_kernel_bit_identical_to_materialised_sum(setup, monkeypatch):
+    """k_rot_sum_f64 (digits gathered through each Galois map, keys in the
+    reference layout, sums in the extended basis, nothing materialised)
+    equals the sum of the extended-basis rotations bit for bit, with the same
+    counters as rot_many_each + sum_each."""
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    ks = [0] + amounts
+    monkeypatch.setenv("HEAR_B200_ROT_SUM", "0")
+    be.reset_counters()
+    want = be.rot_sum_each(cts, ks)
+    c_want = be.counters.as_dict()
+    monkeypatch.setenv("HEAR_B200_ROT_SUM", "1")
+    be.reset_counters()
+    assert be._rot_sum_ok(cts, ks)
+    got = be.rot_sum_each(cts, ks)
+    assert be.counters.as_dict() == c_want
+    for w, g in zip(want, got):
+        assert (w.level, w.scale) == (g.level, g.scale)
+        assert torch.equal(w.payload.data, g.payload.data)
