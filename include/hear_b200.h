@@ -176,14 +176,18 @@ int hb_rot_sum(hb_ring* ring, const void* tasks, int ntasks, const void* rots, i
  * (relinearisation, rot_each, rotate-and-add; engine.py:290-326 digit
  * expansion + ring.py:136-156 inner product in ONE kernel): one HbKsfTask per
  * (ciphertext, target row) = {coef, ident, kb, ka, out_b, out_a, key_dstride,
- * ndig, dst_prime, ident_digit}:
+ * ndig, dst_prime, ident_digit, scat, c0, pmod}:
  *   out_{b,a}[j] = sum_i NTT_dst(lift(coef_i))[j] * k{b,a}[i*key_dstride + j]
  * where coef_i = coef + i*N holds digit i's centred lift as doubles
  * (coefficient domain, written by hb_ntt_inv with scal = 1) and digit
  * ident_digit is taken from the NTT-form row `ident` instead of transformed.
  * The digit expansion is never written: the transforms run in shared memory
  * of a thread-block cluster and the running sums live in tensor memory
- * (csrc/ntt3.cu k_ks3).  fp64 rings with hb_ntt_fused_ks() == 1 only.          */
+ * (csrc/ntt3.cu k_ks3).  With scat != 0 the outputs are stored through that
+ * scatter map (the inverse Galois map of a pre-permuted rotation key) and
+ * out_b gains pmod * c0[j]: out_b / out_a are rows of the ROTATED ciphertext
+ * in the extended basis (lazy ModDown).  fp64 rings with hb_ntt_fused_ks()
+ * == 1 only.                                                                 */
 int hb_ks_fused(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
  * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */

@@ -123,7 +123,7 @@ BCONV_TASK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("dst_off", "<u8"), ("tab
 KSF_TASK = np.dtype([("coef", "<u8"), ("ident", "<u8"), ("kb", "<u8"), ("ka", "<u8"),
                      ("out_b", "<u8"), ("out_a", "<u8"), ("key_dstride", "<i8"),
                      ("ndig", "<i4"), ("dst_prime", "<i4"), ("ident_digit", "<i4"),
-                     ("_pad", "<i4")])
+                     ("_pad", "<i4"), ("scat", "<u8"), ("c0", "<u8"), ("pmod", "<u8")])
 
 ROTSUM_TASK = np.dtype([("de", "<u8"), ("c0", "<u8"), ("c1", "<u8"), ("out_b", "<u8"),
                         ("out_a", "<u8"), ("de_bstride", "<i8"), ("de_dstride", "<i8"),

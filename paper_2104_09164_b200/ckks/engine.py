@@ -669,7 +669,7 @@ class CkksBackend(BackendBase):
         return de
 
     def _ks_apply_many(self, de: torch.Tensor, lvl: int, jobs, bsz: int | None = None,
-                       rescale: bool = False) -> list:
+                       rescale: bool = False, ext: bool = False) -> list:
         """Key-switch decomposed digits once per job and ModDown.
 
         job = (key, perm_dev | None, addend_ptrs [bsz, 2, lvl+1] uint64 (0 = none),
@@ -722,6 +722,17 @@ class CkksBackend(BackendBase):
                 add[j] = addend
                 if gather_c0 and perm is not None:
                     perms[j, :, 0] = perm.data_ptr()
+        if ext:
+            # rotations left in the extended basis: the fused kernel scatters
+            # its sums through the Galois map and adds P * c0 -- `ip` IS the
+            # rotated ciphertext [nj, bsz, 2, lvl+2, N], no ModDown
+            if not fused or len(late) != nj:
+                raise LevelScaleError("extended-basis rotations need the fused key switch "
+                                      "and pre-permuted keys")
+            rot = [(self.ring.perm_inv_for(perm).data_ptr(), c0) for _, perm, c0 in late]
+            self.ring.ks_fused(self._ksf_tasks(de, lvl, parts, ipr, bsz, rot=rot))
+            ipx = ip.reshape(nj, bsz, 2, rows, self.n)
+            return [ipx[j] for j in range(nj)]
         if fused:
             self.ring.ks_fused(self._ksf_tasks(de, lvl, parts, ipr, bsz))
         elif natural and bsz >= self.ks_gemm_min and self.ring.use_f64:
@@ -846,7 +857,7 @@ class CkksBackend(BackendBase):
                                  primes=np.tile(np.arange(r), bsz * 2))
         return res
 
-    def _ksf_tasks(self, de: "_Digits", lvl: int, parts, ipr, bsz: int) -> np.ndarray:
+    def _ksf_tasks(self, de: "_Digits", lvl: int, parts, ipr, bsz: int, rot=None) -> np.ndarray:
         """Task table of the fused ModUp + inner product (k_ks3): one task per
         (job, clip, target row).  parts[j] = (key b row pointers [lvl+2], key a
         row pointers, key digit stride in elements, clip offset into de);
@@ -867,6 +878,11 @@ class CkksBackend(BackendBase):
         t["ndig"] = ndig
         t["dst_prime"] = gidx[None, None, :]
         t["ident_digit"] = np.array(list(range(ndig)) + [-1])[None, None, :]
+        if rot is not None:   # per job: (scatter map pointer, c0 row pointers [bsz, lvl+1])
+            for j, (scat, c0) in enumerate(rot):
+                t["scat"][j] = scat
+                t["c0"][j, :, :ndig] = c0
+            t["pmod"][:, :, :ndig] = self._pmod[:ndig][None, None, :]
         return t.ravel()
 
     def _ks_gemm(self, der, lvl: int, keys, ipr, bsz: int, offs, rot=None):
@@ -988,32 +1004,61 @@ class CkksBackend(BackendBase):
 
     def _mac_ext(self, jobs) -> list:
         """[(level, job indices, acc [len, B, 2, level+2, N])]: the products
-        summed modulo every chain prime and the special prime, per group of
-        jobs sharing one term list."""
-        groups: dict = {}
-        for i, terms in enumerate(jobs):
+        summed modulo every chain prime and the special prime.  Jobs of one
+        level run as ONE shared-term GEMM over the union of their term lists
+        (a job's absent terms take an all-zero plaintext) when the union is
+        at most 1.5x the longest list -- the baby-step sums of a BSGS
+        convolution differ by a few edge terms -- else per group of jobs
+        sharing a term list."""
+        for terms in jobs:
             for ct, pt in terms:
                 if not isinstance(ct.payload, CtExt):
                     raise LevelScaleError("extended-basis and plain handles mixed in one sum")
                 if pt.payload.shape[0] != pt.level + 2:
                     raise LevelScaleError("plaintext lacks its special-prime row")
-            key = (terms[0][0].level, tuple(ct.payload.xdata.data_ptr() for ct, _ in terms))
-            groups.setdefault(key, []).append(i)
         row8 = 8 * self.n
         res = []
-        for (lvl, ctkey), idx in groups.items():
+        for lvl, idx in self._by_level(jobs, lambda t: t[0][0].level).items():
             bsz = jobs[idx[0]][0][0].payload.batch
             rows = lvl + 2
-            acc = self.ring.empty(len(idx), bsz, 2, rows)
-            dsts = self.ring.row_ptrs(acc).reshape(len(idx), -1)[:, 0]
-            pts = np.array([[pt.payload.data_ptr() for _, pt in jobs[i]] for i in idx],
-                           dtype=np.uint64)
-            last = np.array([[pt.payload.data_ptr() + (pt.level + 1) * row8 for _, pt in jobs[i]]
-                             for i in idx], dtype=np.uint64)
-            self.ring.mac_shared(np.array(ctkey, dtype=np.uint64), pts, dsts, rows, 2 * bsz,
-                                 pts_last=last, prime_last=self.S)
-            res.append((lvl, idx, acc))
+            union: dict = {}
+            for i in idx:
+                for ct, _ in jobs[i]:
+                    union.setdefault(ct.payload.xdata.data_ptr(), len(union))
+            longest = max(len(jobs[i]) for i in idx)
+            if len(union) <= 1.5 * longest:
+                groups = [(list(union), idx)]
+            else:
+                by_list: dict = {}
+                for i in idx:
+                    key = tuple(ct.payload.xdata.data_ptr() for ct, _ in jobs[i])
+                    by_list.setdefault(key, []).append(i)
+                groups = [(list(k), g) for k, g in by_list.items()]
+            zero = np.uint64(self._zero_rows(rows).data_ptr())
+            for ctkey, g in groups:
+                pos = {c: q for q, c in enumerate(ctkey)}
+                acc = self.ring.empty(len(g), bsz, 2, rows)
+                dsts = self.ring.row_ptrs(acc).reshape(len(g), -1)[:, 0]
+                pts = np.full((len(g), len(ctkey)), zero, dtype=np.uint64)
+                last = np.full((len(g), len(ctkey)), zero, dtype=np.uint64)
+                for q, i in enumerate(g):
+                    for ct, pt in jobs[i]:
+                        t = pos[ct.payload.xdata.data_ptr()]
+                        if pts[q, t] != zero:
+                            raise LevelScaleError("a handle appears twice in one accumulation")
+                        pts[q, t] = pt.payload.data_ptr()
+                        last[q, t] = pt.payload.data_ptr() + (pt.level + 1) * row8
+                self.ring.mac_shared(np.array(ctkey, dtype=np.uint64), pts, dsts, rows, 2 * bsz,
+                                     pts_last=last, prime_last=self.S)
+                res.append((lvl, g, acc))
         return res
+
+    def _zero_rows(self, rows: int) -> torch.Tensor:
+        """An all-zero plaintext block of at least `rows` rows."""
+        z = getattr(self, "_zrows", None)
+        if z is None or z.shape[0] < rows:
+            self._zrows = z = self.ring.zeros(max(rows, self.L + 2))
+        return z
 
     def _md_rescale(self, rows: np.ndarray, lvl: int, addend) -> torch.Tensor:
         """rescale(ModDown(x) + addend) in one step (cluster NTT): rows
@@ -1135,9 +1180,11 @@ class CkksBackend(BackendBase):
         one pass over level+2 rows per group, then ONE ModDown per group
         instead of one per rotation."""
         out = [None] * len(groups)
-        for g in groups:
-            if not all(isinstance(c.payload, CtExt) for c in g):
-                raise LevelScaleError("extended-basis and plain handles mixed in one sum")
+        # plain handles of a mixed group (the unrotated term) join as P * ct
+        plain = {id(c): c for g in groups for c in g if not isinstance(c.payload, CtExt)}
+        if plain:
+            lifted = dict(zip(plain, self._lift_ext(list(plain.values()))))
+            groups = [[lifted.get(id(c), c) for c in g] for g in groups]
         for lvl, js in self._by_level(groups, lambda g: g[0].level).items():
             bsz = groups[js[0]][0].payload.batch
             rows = lvl + 2
@@ -1161,6 +1208,29 @@ class CkksBackend(BackendBase):
             res = res.reshape(len(js), bsz, 2, lvl + 1, self.n)
             for q, j in enumerate(js):
                 out[j] = Ct(CtData(res[q]), lvl, groups[j][0].scale, self.n2)
+        return out
+
+    def _lift_ext(self, cts) -> list:
+        """P * ct on the chain rows, a zero special row: plain handles in the
+        extended basis (the identity term of a lazy sum)."""
+        out = [None] * len(cts)
+        rp = self.ring.row_ptrs
+        for lvl, idx in self._by_level(cts, lambda c: c.level).items():
+            bsz = cts[idx[0]].payload.batch
+            r, rows = lvl + 1, lvl + 2
+            nh = len(idx)
+            x0 = self.ring.empty(nh, bsz, 2, rows)
+            z = np.uint64(self._zero_row().data_ptr())
+            b = np.full((nh, bsz, 2, rows), z, dtype=np.uint64)
+            b[..., :r] = np.stack([rp(cts[i].payload.data).reshape(bsz, 2, r) for i in idx])
+            m = nh * bsz * 2
+            zero1 = np.zeros(1, dtype=np.uint64)
+            self._ew(nat.EW_ADD_SCALED, rp(x0), np.full(m * rows, z, dtype=np.uint64), b.ravel(),
+                     primes=np.tile(np.array(list(range(r)) + [self.S]), m),
+                     scal=np.tile(np.concatenate([self._pmod[:r], zero1]), m),
+                     scal_sh=np.tile(np.concatenate([self._pmod_sh[:r], zero1]), m))
+            for q, i in enumerate(idx):
+                out[i] = Ct(CtExt(x0[q]), lvl, cts[i].scale, self.n2)
         return out
 
     def _raw_add_each(self, pairs) -> list:
@@ -1207,7 +1277,9 @@ class CkksBackend(BackendBase):
         per = bsz * (lvl + 1) * (lvl + 2) * self.n * 8
         return max(1, int(self.ks_budget_bytes // max(per, 1)))
 
-    def _raw_rot_each(self, items) -> list:
+    def _raw_rot_each(self, items, lazy: bool = False) -> list:
+        """lazy: the rotations only feed a sum -- where the fused key switch
+        runs they stay in the extended basis (CtExt, no ModDown)."""
         out = [None] * len(items)
         for lvl, idx in self._by_level(items, lambda it: it[0].level).items():
             bsz = items[idx[0]][0].payload.batch
@@ -1222,11 +1294,12 @@ class CkksBackend(BackendBase):
                 for q, i in enumerate(chunk):
                     key, perm, add, g = self._rot_job(*items[i])
                     jobs.append((key, perm, add, g, q * bsz))
-                res = self._ks_apply_many(de, lvl, jobs, bsz)
+                ext = lazy and self.lazy and isinstance(de, _Digits)
+                res = self._ks_apply_many(de, lvl, jobs, bsz, ext=ext)
                 del de
                 for q, i in enumerate(chunk):
                     ct = items[i][0]
-                    out[i] = Ct(CtData(res[q]), lvl, ct.scale, self.n2)
+                    out[i] = Ct(CtExt(res[q]) if ext else CtData(res[q]), lvl, ct.scale, self.n2)
         return out
 
     def _raw_rot_add_each(self, items) -> list:
@@ -1342,18 +1415,8 @@ class CkksBackend(BackendBase):
         ctr = np.stack([rp(c.payload.data).reshape(bsz, 2, r) for c in cts])   # [nh, bsz, 2, r]
         out = [{} for _ in cts]
         if want0:
-            x0 = self.ring.empty(nh, bsz, 2, rows)
-            z = np.uint64(self._zero_row().data_ptr())
-            b = np.full((nh, bsz, 2, rows), z, dtype=np.uint64)
-            b[..., :r] = ctr
-            m = nh * bsz * 2
-            zero1 = np.zeros(1, dtype=np.uint64)
-            self._ew(nat.EW_ADD_SCALED, rp(x0), np.full(m * rows, z, dtype=np.uint64), b.ravel(),
-                     primes=np.tile(np.array(list(range(r)) + [self.S]), m),
-                     scal=np.tile(np.concatenate([self._pmod[:r], zero1]), m),
-                     scal_sh=np.tile(np.concatenate([self._pmod_sh[:r], zero1]), m))
-            for h, c in enumerate(cts):
-                out[h][0] = Ct(CtExt(x0[h]), lvl, c.scale, self.n2)
+            for h, x in enumerate(self._lift_ext(cts)):
+                out[h][0] = x
         de = self._decompose(ctr[:, :, 1].reshape(nh * bsz, r), lvl)
         der = rp(de).reshape(nh * bsz, ndig, rows)
         xr = self.ring.empty(nh, nk, bsz, 2, rows)

@@ -258,7 +258,7 @@ def hconv(cts: list, weights: ConvWeights, plan: ConvPlan, backend: BackendBase,
                     rot_amt.append(taps[k] if plan.strategy == "giant" else 0)
                     owner.append(j)
         partials = backend.mac_many(jobs)
-        moved = backend.rot_each(list(zip(partials, rot_amt)))
+        moved = backend.rot_each(list(zip(partials, rot_amt)), lazy=True)   # only summed below
         groups = [[c for c, o in zip(moved, owner) if o == j] for j in js]
         outs += backend.rescale_each(backend.sum_each(groups))
     return outs

@@ -57,9 +57,9 @@ constexpr int THREADS3 = 256;
 // (cp.async.bulk.prefetch) while the block pass runs.
 template <int LOGN>
 __host__ __device__ constexpr int smem3() { return TILE3 * 8 + ((1 << (LOGN - 7)) - 1 + 480) * 16 + 16; }
-// k_ks3: + its task (64 B) behind the two barrier words
+// k_ks3: + its task (88 B) behind the two barrier words
 template <int LOGN>
-__host__ __device__ constexpr int smem3k() { return smem3<LOGN>() + 64; }
+__host__ __device__ constexpr int smem3k() { return smem3<LOGN>() + 96; }
 constexpr int MINB3 = 4;
 // N = 2^16 runs 16-CTA clusters (non-portable size): per launch within
 // -6..+1 % of the two-pass kernels, but the pipeline then takes the
@@ -850,13 +850,28 @@ k_ks3(const HbKsfTask* __restrict__ tasks, HbRing R) {
       aa0 += fmod_mul(x0, ka0, ka0 * pinv, pd);
       aa1 += fmod_mul(x1, ka1, ka1 * pinv, pd);
       if (lastd) {
+        const int* scat = tk.scat;
+        if (scat && tk.c0) {   // + P * c0 (the rotated c0, still at the source index)
+          const ulonglong2 c2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.c0 + base + j));
+          const double pm = u64_to_f(tk.pmod), pmq = pm * pinv;
+          ab0 += fmod_mul(u64_to_f(c2.x), pm, pmq, pd);
+          ab1 += fmod_mul(u64_to_f(c2.y), pm, pmq, pd);
+        }
         ulonglong2 ob, oa;
         ob.x = fmod_canon(ab0, pd, pinv);
         ob.y = fmod_canon(ab1, pd, pinv);
         oa.x = fmod_canon(aa0, pd, pinv);
         oa.y = fmod_canon(aa1, pd, pinv);
-        *reinterpret_cast<ulonglong2*>(tk.out_b + base + j) = ob;
-        *reinterpret_cast<ulonglong2*>(tk.out_a + base + j) = oa;
+        if (scat) {
+          const int2 sc = __ldg(reinterpret_cast<const int2*>(scat + base + j));
+          tk.out_b[sc.x] = ob.x;
+          tk.out_b[sc.y] = ob.y;
+          tk.out_a[sc.x] = oa.x;
+          tk.out_a[sc.y] = oa.y;
+        } else {
+          *reinterpret_cast<ulonglong2*>(tk.out_b + base + j) = ob;
+          *reinterpret_cast<ulonglong2*>(tk.out_a + base + j) = oa;
+        }
       } else {
         tmem_st4(tacc + 8 * i, ab0, ab1, aa0, aa1);
       }

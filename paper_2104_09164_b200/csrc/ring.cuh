@@ -112,6 +112,13 @@ struct HbKsfTask {
   int dst_prime;
   int ident_digit;     // the digit served by `ident` (-1: none, the special row)
   int _pad;
+  // rotation left in the extended basis (lazy ModDown): outputs stored through
+  // the scatter map (the inverse Galois map of the pre-permuted key), out_b
+  // plus pmod * c0 on chain rows -- out_b / out_a are then rows of the rotated
+  // ciphertext in basis Q*P.  scat = null: plain inner-product rows.
+  const int* scat;
+  const u64* c0;       // this target row of the rotated handle's c0 (null: special row)
+  u64 pmod;            // P mod p_dst
 };
 
 // One output row of a plaintext multiply-accumulate:

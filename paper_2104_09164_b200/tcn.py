@@ -436,8 +436,10 @@ def run_tcn(encoder: TcnEncoder, ct: Ct, backend: BackendBase) -> Ct:
             ts = pl.ts[i]
             pts = encoder.conv_pts(i)
             g, giants, terms = pl.bsgs[i]
-            baby = backend.rot_many(ct, [e * B + k * ts for e in range(g)
-                                         for k in range(cv.kernel)])
+            # the baby steps only feed the inner sums: their ModDown may be
+            # deferred to one per inner sum
+            baby = backend.rot_many_each([ct], [e * B + k * ts for e in range(g)
+                                                for k in range(cv.kernel)], lazy=True)[0]
             acc = None
             # giant steps in groups of GIANT_GROUP: the inner sums of one
             # group are live at a time (B clips x rows per handle); same op
@@ -446,7 +448,7 @@ def run_tcn(encoder: TcnEncoder, ct: Ct, backend: BackendBase) -> Ct:
                 grp = giants[g0:g0 + GIANT_GROUP]
                 inner = backend.mac_many([[(baby[(e * B + k * ts) % backend.n2], pts[(D, e, k)])
                                            for e, k in terms[D]] for D in grp])
-                giant = backend.rot_each([(x, g * D * B) for x, D in zip(inner, grp)])
+                giant = backend.rot_each([(x, g * D * B) for x, D in zip(inner, grp)], lazy=True)
                 part = backend.sum_each([giant])[0]
                 acc = part if acc is None else backend.add(acc, part)
             ct = backend.rescale(acc)

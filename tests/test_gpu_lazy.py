@@ -223,3 +223,29 @@ def test_rot_sum_kernel_bit_identical_to_materialised_sum(setup, monkeypatch):
     for w, g in zip(want, got):
         assert (w.level, w.scale) == (g.level, g.scale)
         assert torch.equal(w.payload.data, g.payload.data)
+
+
+def test_lazy_rot_each_extended_rotations(setup):
+    """rot_each(lazy=True): the fused key switch scatters through the Galois
+    map and adds P*c0, leaving each rotation in the extended basis; its
+    ModDown equals the eager rotation bit for bit, and a mixed sum (the
+    unrotated handle joins as P*ct) decrypts like the eager sum."""
+    be, lvl, bsz, amounts, cts, rng, torch = setup
+    items = [(cts[0], amounts[0]), (cts[1], amounts[1]), (cts[0], amounts[2])]
+    old = be.fuse_ks_min
+    try:
+        be.fuse_ks_min = 0
+        eager = be.rot_each(items)
+        lazy = be.rot_each(items, lazy=True)
+        for e, l in zip(eager, lazy):
+            assert not hasattr(l.payload, "data")
+            assert torch.equal(be._mod_down_ext(l.payload.xdata, lvl), e.payload.data)
+        be.reset_counters()
+        s_lazy = be.sum_each([[cts[0], lazy[0], lazy[2]]])[0]
+        c_lazy = be.counters.as_dict()
+        be.reset_counters()
+        s_eager = be.sum_each([[cts[0], eager[0], eager[2]]])[0]
+        assert be.counters.as_dict() == c_lazy
+        assert np.abs(be.dec(s_lazy) - be.dec(s_eager)).max() <= 1e-4
+    finally:
+        be.fuse_ks_min = old
