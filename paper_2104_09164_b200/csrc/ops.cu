@@ -835,7 +835,10 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
 // sector-exact), the keys are read in place (shared by the 8 clips of a CTA
 // through L1).  The unfused form wrote one extended rotation per amount and
 // re-read them all for the sum.
-__global__ void __launch_bounds__(256)
+#ifndef HB_RS_MINB
+#define HB_RS_MINB 4   // <= 64 registers: the gather chain is latency-bound, 4 CTAs per SM (8.8 -> 6.2 ms per step)
+#endif
+__global__ void __launch_bounds__(256, HB_RS_MINB)
 k_rot_sum_f64(const HbRotSumTask* __restrict__ tasks, const HbRotSumRot* __restrict__ rots,
               int nrot, int ndig, const HbPrime* __restrict__ primes, int n, int nb) {
   HB_PDL_ENTRY();
