@@ -115,3 +115,50 @@ def test_batched_contract_forms_on_simulator():
     sums = be.sum_each([cts, cts[:2], cts[2:]])
     assert sum(v.get("add", 0) for v in be.counters.as_dict().values()) == 3
     assert np.allclose(be.dec(sums[0]), sum(be.dec(c) for c in cts))
+
+
+def test_lazy_contract_forms_are_the_plain_sequences_on_simulator():
+    """The forms that let the GPU engine defer / merge ModDowns --
+    rot_many_each(lazy), rot_each(lazy), rot_sum_each, mac_rescale_many,
+    square_rescale_each -- are, on an engine without those fast paths, exactly
+    the reference's op sequences: same slot values, same counters
+    (hear/convolution.py:276-312, hear/fastpath.py:123-154)."""
+    rng = np.random.default_rng(5)
+    be = SimBackend(gen_params("fast-hear"))
+    lvl = 6
+    cts = [be.enc(rng.uniform(-1, 1, be.n2), level=lvl) for _ in range(2)]
+    pts = [be.encode(rng.uniform(-1, 1, be.n2), lvl, be.params.msg_scale) for _ in range(6)]
+    ks = [0, 3, 9]
+
+    def counted(fn):
+        be.reset_counters()
+        out = fn()
+        return out, be.counters.as_dict()
+
+    lazy, c1 = counted(lambda: be.rot_many_each(cts, ks, lazy=True))
+    plain, c2 = counted(lambda: be.rot_many_each(cts, ks))
+    assert c1 == c2
+    for a, b in zip(lazy, plain):
+        for k in ks:
+            assert np.array_equal(be.dec(a[k]), be.dec(b[k]))
+    items = [(cts[0], 3), (cts[1], 0), (cts[1], 9)]
+    a, c1 = counted(lambda: be.rot_each(items, lazy=True))
+    b, c2 = counted(lambda: be.rot_each(items))
+    assert c1 == c2 and all(np.array_equal(be.dec(x), be.dec(y)) for x, y in zip(a, b))
+    a, c1 = counted(lambda: be.rot_sum_each(cts, ks))
+    b, c2 = counted(lambda: be.sum_each([[r[k] for k in ks]
+                                         for r in be.rot_many_each(cts, ks)]))
+    assert c1 == c2 and all(np.array_equal(be.dec(x), be.dec(y)) for x, y in zip(a, b))
+    jobs = [[(plain[h][k], pts[3 * h + q]) for q, k in enumerate(ks)] for h in range(2)]
+    a, c1 = counted(lambda: be.mac_rescale_many(jobs))
+    b, c2 = counted(lambda: be.rescale_each(be.mac_many(jobs)))
+    assert c1 == c2
+    for x, y in zip(a, b):
+        assert (x.level, x.scale) == (y.level, y.scale) == (lvl - 1, y.scale)
+        assert np.array_equal(be.dec(x), be.dec(y))
+    a, c1 = counted(lambda: be.square_rescale_each(cts))
+    b, c2 = counted(lambda: be.rescale_each(be.square_each(cts)))
+    assert c1 == c2
+    for x, y in zip(a, b):
+        assert (x.level, x.scale) == (y.level, y.scale)
+        assert np.array_equal(be.dec(x), be.dec(y))
