@@ -111,7 +111,8 @@ MAC_OUT = np.dtype([("dst", "<u8"), ("nterms", "<i4"), ("term_off", "<i4")])
 KS_TASK2 = np.dtype([("de", "<u8"), ("kb", "<u8"), ("ka", "<u8"), ("out_b", "<u8"),
                      ("out_a", "<u8"), ("perm", "<u8"), ("de_bstride", "<i8"),
                      ("de_dstride", "<i8"), ("key_stride", "<i8"), ("out_bstride", "<i8"),
-                     ("ndig", "<i4"), ("prime", "<i4")])
+                     ("ndig", "<i4"), ("prime", "<i4"), ("scat", "<u8"), ("c0", "<u8"),
+                     ("c0_bstride", "<i8"), ("pmod", "<u8")])
 TENSOR_TASK = np.dtype([("a0", "<u8"), ("a1", "<u8"), ("b0", "<u8"), ("b1", "<u8"),
                         ("d0", "<u8"), ("d1", "<u8"), ("d2", "<u8"),
                         ("prime", "<i4"), ("_pad", "<i4")])

@@ -215,8 +215,10 @@ class CkksBackend(BackendBase):
         # one per rotation).  HEAR_B200_LAZY_MODDOWN=0 restores the eager path.
         self.lazy = (os.environ.get("HEAR_B200_LAZY_MODDOWN", "1") == "1" and self.ring.use_f64
                      and self.preperm and self.lift_once)
-        # smallest batch that takes the lazy form (its inner product is the GEMM)
-        self.lazy_min = int(os.environ.get("HEAR_B200_LAZY_MIN", str(self.ks_gemm_min)))
+        # smallest batch that takes the lazy forms (below ks_gemm_min the
+        # extended-basis rotations come from the per-job inner-product kernel:
+        # B=1 latency 4.06 -> 3.49 ms)
+        self.lazy_min = int(os.environ.get("HEAR_B200_LAZY_MIN", "1"))
         self._pmod_dev = self._dev(self._pmod)
         # non-hoisted key switches (relinearisation, rot_each, rotate-and-add)
         # run ModUp and the inner product in ONE kernel (k_ks3: transforms in
@@ -1431,11 +1433,32 @@ class CkksBackend(BackendBase):
             keys.append((key.bp, key.ap, key.lmax))
             inv = self.ring.perm_inv_dev(self.ring.galois_element(k)).data_ptr()
             scat += [inv, inv]
-        for h in range(nh):
-            c0s = np.zeros(2 * nk, dtype=np.uint64)
-            c0s[0::2] = ctr[h, 0, 0, 0]
-            self._ks_gemm(der, lvl, keys, xrr[h], bsz, [h * bsz] * nk,
-                          rot=(scat, c0s, 2 * r * self.n, self._pmod_dev.data_ptr()))
+        if bsz < self.ks_gemm_min:
+            # a few clips: the per-job inner product (lower latency than the
+            # GEMM there) with the same rotation epilogue
+            gidx = np.array(list(range(lvl + 1)) + [self.S])
+            parts = []
+            for h in range(nh):
+                for q, (kb_t, ka_t, lmax) in enumerate(keys):
+                    krow = np.array(list(range(lvl + 1)) + [lmax + 1])
+                    c0 = np.zeros(rows, dtype=np.uint64)
+                    c0[:r] = ctr[h, 0, 0, :]
+                    parts.append(_tasks(
+                        nat.KS_TASK2, rows, de=der[h * bsz, 0, :],
+                        kb=rp(kb_t).reshape(kb_t.shape[0], lmax + 2)[0, krow],
+                        ka=rp(ka_t).reshape(ka_t.shape[0], lmax + 2)[0, krow],
+                        out_b=xrr[h, q, 0, 0], out_a=xrr[h, q, 0, 1], perm=0,
+                        de_bstride=ndig * rows * self.n, de_dstride=rows * self.n,
+                        key_stride=(lmax + 2) * self.n, out_bstride=2 * rows * self.n, ndig=ndig,
+                        prime=gidx, scat=scat[2 * q], c0=c0, c0_bstride=2 * r * self.n,
+                        pmod=np.concatenate([self._pmod[:r], np.zeros(1, dtype=np.uint64)])))
+            self.ring.ks_inner2(np.concatenate(parts), bsz)
+        else:
+            for h in range(nh):
+                c0s = np.zeros(2 * nk, dtype=np.uint64)
+                c0s[0::2] = ctr[h, 0, 0, 0]
+                self._ks_gemm(der, lvl, keys, xrr[h], bsz, [h * bsz] * nk,
+                              rot=(scat, c0s, 2 * r * self.n, self._pmod_dev.data_ptr()))
         del de
         for h, c in enumerate(cts):
             for q, k in enumerate(ks):

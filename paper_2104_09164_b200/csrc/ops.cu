@@ -805,11 +805,27 @@ k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__
     a0 += fmod_mul(ka0, x0, q0, p);
     a1 += fmod_mul(ka1, x1, q1, p);
   }
+  if (tk.scat && tk.c0) {   // + P * c0 (the rotated c0, still at the source index)
+    const ulonglong2 c2 = __ldg(reinterpret_cast<const ulonglong2*>(tk.c0 + b * tk.c0_bstride + j));
+    const double pm = u64_to_f(tk.pmod), pmq = pm * pinv;
+    b0 += fmod_mul(u64_to_f(c2.x), pm, pmq, p);
+    b1 += fmod_mul(u64_to_f(c2.y), pm, pmq, p);
+  }
   ulonglong2 rb, ra;
   rb.x = fmod_canon(b0, p, pinv);
   rb.y = fmod_canon(b1, p, pinv);
   ra.x = fmod_canon(a0, p, pinv);
   ra.y = fmod_canon(a1, p, pinv);
+  if (tk.scat) {   // rotated ciphertext rows in the extended basis
+    const int2 sc = __ldg(reinterpret_cast<const int2*>(tk.scat + j));
+    u64* ob = tk.out_b + b * tk.out_bstride;
+    u64* oa = tk.out_a + b * tk.out_bstride;
+    ob[sc.x] = rb.x;
+    ob[sc.y] = rb.y;
+    oa[sc.x] = ra.x;
+    oa[sc.y] = ra.y;
+    return;
+  }
   *reinterpret_cast<ulonglong2*>(tk.out_b + b * tk.out_bstride + j) = rb;
   *reinterpret_cast<ulonglong2*>(tk.out_a + b * tk.out_bstride + j) = ra;
 }

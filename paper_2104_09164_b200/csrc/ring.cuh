@@ -209,4 +209,11 @@ struct HbKsTask2 {
   long long de_bstride, de_dstride, key_stride, out_bstride;
   int ndig;
   int prime;
+  // rotation left in the extended basis (fp64 kernel only; lazy ModDown at
+  // small batches): outputs stored through the scatter map, out_b plus
+  // pmod * c0[b*c0_bstride + j] when c0 is set.  scat = null: as before.
+  const int* scat;
+  const u64* c0;
+  long long c0_bstride;
+  u64 pmod;
 };

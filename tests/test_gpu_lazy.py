@@ -249,3 +249,26 @@ def test_lazy_rot_each_extended_rotations(setup):
         assert np.abs(be.dec(s_lazy) - be.dec(s_eager)).max() <= 1e-4
     finally:
         be.fuse_ks_min = old
+
+
+def test_lazy_rotations_at_small_batch():
+    """Below the GEMM's batch threshold the extended-basis rotations come from
+    the per-job inner product kernel with the same rotation epilogue: their
+    ModDown equals the eager rotations bit for bit (1 and 3 clips)."""
+    import torch
+    from paper_2104_09164_b200.ckks.engine import CkksBackend
+    from paper_2104_09164_b200.ckks.params import gen_params
+    be = CkksBackend(gen_params("fast-hear"), seed=2)
+    be.lazy_min = 1
+    lvl, amounts = 5, [2, 11, 8191]
+    be.ensure_rotation_keys({a: lvl for a in amounts})
+    rng = np.random.default_rng(8)
+    for bsz in (1, 3):
+        assert bsz < be.ks_gemm_min
+        cts = [be.enc(rng.uniform(-1, 1, (bsz, be.n2)), level=lvl) for _ in range(2)]
+        eager = be._raw_rot_many_each(cts, amounts)
+        pre = be.rot_many_each(cts, [0] + amounts, lazy=True)
+        for h in range(2):
+            for k in amounts:
+                x = pre[h][k].payload.xdata
+                assert torch.equal(be._mod_down_ext(x, lvl), eager[h][k].payload.data), (bsz, h, k)
