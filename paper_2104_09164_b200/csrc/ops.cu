@@ -764,13 +764,16 @@ cudaError_t launch_mac_gemm_f64(const void* cts, const void* pts, const void* ds
 // fp64 variant of the clip-blocked key-switch inner product.
 __global__ void __launch_bounds__(256)
 k_ks_inner2_f64(const HbKsTask2* __restrict__ tasks, const HbPrime* __restrict__ primes, int n,
-                int nb) {
+                int nb, int by) {
   HB_PDL_ENTRY();
   const HbKsTask2 tk = tasks[blockIdx.y];
   // grid: x = clip group (fastest), y = task, z = coefficient chunk (slowest):
-  // the clips of one key row run back to back, so the key is read from HBM once
-  const int b = blockIdx.x * blockDim.y + threadIdx.y;
-  const int j = 2 * (blockIdx.z * 32 + threadIdx.x);
+  // the clips of one key row run back to back, so the key is read from HBM once.
+  // blockDim.y = by clips x (blockDim.y / by) coefficient chunks: at one or two
+  // clips a CTA still has 8 warps (one-warp CTAs streamed the keys at half
+  // the HBM rate)
+  const int b = blockIdx.x * by + threadIdx.y % by;
+  const int j = 2 * ((blockIdx.z * (blockDim.y / by) + threadIdx.y / by) * 32 + threadIdx.x);
   if (j >= n || b >= nb) return;
   const HbPrime P = primes[tk.prime];
   const double p = P.pd, pinv = P.pinv;
@@ -834,9 +837,10 @@ cudaError_t launch_ks_inner2_f64(const void* tasks, int ntasks, int nb, const Hb
                                  int n, cudaStream_t st) {
   if (ntasks <= 0 || nb <= 0) return cudaSuccess;
   const int by = nb < 8 ? nb : 8;
-  dim3 block(32, by);
-  dim3 grid((nb + by - 1) / by, ntasks, (n / 2 + 31) / 32);
-  (void)hb_launch(k_ks_inner2_f64, dim3(grid), dim3(block), 0, st, reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb);
+  const int cy = 8 / by;   // coefficient chunks per CTA
+  dim3 block(32, by * cy);
+  dim3 grid((nb + by - 1) / by, ntasks, (n / 2 / 32 + cy - 1) / cy);
+  (void)hb_launch(k_ks_inner2_f64, dim3(grid), dim3(block), 0, st, reinterpret_cast<const HbKsTask2*>(tasks), primes, n, nb, by);
   return cudaGetLastError();
 }
 
