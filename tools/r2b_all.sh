@@ -11,7 +11,7 @@ run config3 1500 bench.py --workload config3 --steps 5 --warmup 3
 run config2 1500 bench.py --workload config2 --steps 3 --warmup 3
 run 2dw128 1200 bench.py --net 2d-w128 --batch 32 --steps 5 --warmup 3 --no-cpu-baseline
 run hear 1200 bench.py --mode hear --batch 64 --steps 5 --warmup 3 --no-cpu-baseline
-HEAR_B200_LAZY_MIN=1 run b1lazy 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
+HEAR_B200_LAZY_MIN=8 run b1eager 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
 HEAR_B200_LAZY_MIN=1 HEAR_B200_KS_FUSED_MIN=40 run b1lazyfused 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
 HEAR_B200_KS_FUSED_MIN=40 run b1fused 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
 timeout 900 python tools/stream_bench.py > gpurun_out/r2b_stream_config4.json 2> gpurun_out/r2b_stream.err; echo "stream rc=$?"
