@@ -63,3 +63,33 @@ def test_fused_launch_is_taken():
         set_step_stats(None)
     assert st.fam["keyswitch_fused"]["launches"] == 1
     assert "ntt_fwd_modup_lift" not in st.fam and "keyswitch_gemm" not in st.fam
+
+
+@pytest.mark.parametrize("lvl,handles", [(12, 1), (3, 4)])
+def test_fused_key_switch_deterministic_under_load(lvl, handles):
+    """k_ks3 with every SM busy (128 clips per handle: thousands of clusters
+    looping over the digits, four CTAs per SM sharing the tensor memory) is
+    deterministic and equals the unfused path bit for bit.  Guards the
+    per-digit barrier / mbarrier-phase protocol and the TMEM column
+    ownership: an error there corrupts a few rows only under load."""
+    import torch
+    be = _pair("fast-hear")
+    rng = np.random.default_rng(4)
+    cts = [be.enc(rng.uniform(-1, 1, (128, be.n2)), level=lvl) for _ in range(handles)]
+    be.ensure_rotation_keys({5: lvl})
+    be.fuse_ks_min = 1 << 60
+    want_sq = [c.payload.data.clone() for c in be.square_each(cts)]
+    want_ra = [c.payload.data.clone() for c in be.rot_add_each([(c, 5) for c in cts])]
+    be.fuse_ks_min = 0
+    for _ in range(4):
+        got_sq = be.square_each(cts)
+        got_ra = be.rot_add_each([(c, 5) for c in cts])
+        lazy = be.rot_each([(c, 5) for c in cts], lazy=True)
+        for w, g in zip(want_sq, got_sq):
+            assert torch.equal(w, g.payload.data)
+        for w, g in zip(want_ra, got_ra):
+            assert torch.equal(w, g.payload.data)
+        for c, l, w in zip(cts, lazy, want_ra):   # ModDown(ext rotation) + ct == rot_add
+            md = be._mod_down_ext(l.payload.xdata, lvl)
+            rot = be._raw_add_each([(c, type(c)(type(c.payload)(md), lvl, c.scale, be.n2))])[0]
+            assert torch.equal(rot.payload.data, w)

@@ -15,4 +15,4 @@ HEAR_B200_LAZY_MIN=8 run b1eager 900 bench.py --steps 3 --warmup 3 --no-cpu-base
 HEAR_B200_LAZY_MIN=1 HEAR_B200_KS_FUSED_MIN=40 run b1lazyfused 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
 HEAR_B200_KS_FUSED_MIN=40 run b1fused 900 bench.py --steps 3 --warmup 3 --no-cpu-baseline
 timeout 900 python tools/stream_bench.py > gpurun_out/r2b_stream_config4.json 2> gpurun_out/r2b_stream.err; echo "stream rc=$?"
-python tools/bench_summary.py gpurun_out/r2b_config0.json gpurun_out/r2b_config3.json gpurun_out/r2b_config2.json gpurun_out/r2b_2dw128.json gpurun_out/r2b_hear.json gpurun_out/r2b_b1lazy.json gpurun_out/r2b_b1lazyfused.json gpurun_out/r2b_b1fused.json
+python tools/bench_summary.py gpurun_out/r2b_config0.json gpurun_out/r2b_config3.json gpurun_out/r2b_config2.json gpurun_out/r2b_2dw128.json gpurun_out/r2b_hear.json gpurun_out/r2b_b1eager.json gpurun_out/r2b_b1lazyfused.json gpurun_out/r2b_b1fused.json
