@@ -576,6 +576,41 @@ class CkksBackend(BackendBase):
         self._ew(nat.EW_ADD, rp(out), rp(x), b.ravel(), primes=self._row_primes(2 * bsz, r))
         return Ct(CtData(out), a.level, a.scale, self.n2)
 
+    def _raw_add_plain_each(self, pairs) -> list:
+        """One launch per level group: c0 rows + plaintext, c1 rows copied."""
+        out = [None] * len(pairs)
+        rp = self.ring.row_ptrs
+        z = np.uint64(self._zero_row().data_ptr())
+        for lvl, idx in self._by_level(pairs, lambda pr: pr[0].level).items():
+            bsz = pairs[idx[0]][0].payload.batch
+            r = lvl + 1
+            res = self.ring.empty(len(idx), bsz, 2, r)
+            b = np.full((len(idx), bsz, 2, r), z, dtype=np.uint64)
+            for q, i in enumerate(idx):
+                b[q, :, 0] = rp(pairs[i][1].payload)[:r]
+            a = np.concatenate([rp(pairs[i][0].payload.data) for i in idx])
+            self._ew(nat.EW_ADD, rp(res), a, b.ravel(),
+                     primes=self._row_primes(len(idx) * bsz * 2, r))
+            for q, i in enumerate(idx):
+                c = pairs[i][0]
+                out[i] = Ct(CtData(res[q]), lvl, c.scale, self.n2)
+        return out
+
+    def _raw_mod_down_each(self, cts, to_level: int) -> list:
+        """The kept rows of every handle in one copy launch per source level."""
+        out = [None] * len(cts)
+        rp = self.ring.row_ptrs
+        r = to_level + 1
+        for lvl, idx in self._by_level(cts, lambda c: c.level).items():
+            bsz = cts[idx[0]].payload.batch
+            res = self.ring.empty(len(idx), bsz, 2, r)
+            src = np.concatenate([rp(cts[i].payload.data).reshape(bsz * 2, lvl + 1)[:, :r].ravel()
+                                  for i in idx])
+            self._ew(nat.EW_COPY, rp(res), src, primes=self._row_primes(len(idx) * bsz * 2, r))
+            for q, i in enumerate(idx):
+                out[i] = Ct(CtData(res[q]), to_level, cts[i].scale, self.n2)
+        return out
+
     def _zero_row(self) -> torch.Tensor:
         if getattr(self, "_zrow", None) is None:
             self._zrow = self.ring.zeros(1)
