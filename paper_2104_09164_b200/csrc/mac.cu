@@ -406,7 +406,11 @@ static cudaError_t mac_pipe_dispatch_rot(const HbMacGroupP& g, const HbRing& RG,
 static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
                                      cudaStream_t st) {
   constexpr int S = HB_MAC_STAGES;
-  if (BC <= 2 && !g.cts_per_tile) return mac_pipe_t<2, 2, 8, 1, S>(g, RG, rows, BC, st);
+  if (BC <= 2 && !g.cts_per_tile) {
+    // one clip: 8 warps x 1 output when the layer has at most 8 (no idle warps)
+    if (g.nout <= 8) return mac_pipe_t<1, 2, 8, 1, S>(g, RG, rows, BC, st);
+    return mac_pipe_t<2, 2, 8, 1, S>(g, RG, rows, BC, st);
+  }
   // one (b, a) output pair per tile when every job brings its own digits
   if (g.cts_per_tile) return mac_pipe_t<2, 4, 1, 8, S>(g, RG, rows, BC, st);
   // output tile sized to the layer so no warp idles on absent outputs
