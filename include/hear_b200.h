@@ -90,8 +90,15 @@ int hear_sub_scaled_inv(hb_ring* ring, unsigned long long* rows, const unsigned 
  * pre-permuted keys, the result scattered through the inverse Galois map
  * (perm) and the addend read in natural order.  Modes 2/4 add the optional
  * post-addend `add2` at the destination index (the add of rotate-and-sum,
- * fastpath.py rot-add, fused).  Clusters of N/4096 CTAs on fp64 rings at
- * N = 2^13 / 2^14 (csrc/ntt3.cu), else two-pass (csrc/ntt2.cu). */
+ * fastpath.py rot-add, fused).  5 (cluster NTT only): the ModDown of mode 2
+ * merged with the rescale that follows it (engine.py:213-227 then 263-281):
+ * src = centred special-prime row, `perm` REINTERPRETED as a second source
+ * row y (centred doubles: the ModDown'ed top row in the coefficient domain,
+ * hb_ew op 10), scal_sh = P mod p_dst, scal = (P q_l)^-1, add2 = q_l^-1 by
+ * value:  dst = (aux - NTT(src + P*y)) * scal + add * add2 -- one transform
+ * per target row instead of two, same residues as the two steps.  Clusters
+ * of N/4096 CTAs on fp64 rings at N = 2^13 .. 2^16 (csrc/ntt3.cu), else
+ * two-pass (csrc/ntt2.cu). */
 int hb_ntt_fwd(hb_ring* ring, const void* tasks, int count, int mode, void* stream);
 /* Inverse NTT over row tasks (ring.py:120, true inverse twiddles).            */
 int hb_ntt_inv(hb_ring* ring, const void* tasks, int count, void* stream);
@@ -101,10 +108,10 @@ int hb_ntt_kernels(hb_ring* ring, int count);
 /* 1 when the ring's modular arithmetic runs on the fp64 pipe (every prime
  * < 2^42 and HEAR_B200_INT_NTT unset), else 0.                              */
 int hb_ring_uses_f64(const hb_ring* ring);
-/* 1 when hb_ntt_fwd accepts mode 5 on this ring (the cluster-fused NTT):
- * FWD_LIFT fused with the key-switch inner product, dst += NTT(lift(src)) *
- * aux and add2 += NTT(lift(src)) * add with 64-bit atomic adds of canonical
- * products (the caller reduces the sums afterwards).                         */
+/* 1 when the ring runs the cluster-fused NTT (fp64 rings, N = 2^13 .. 2^16):
+ * hb_ntt_inv then stores centred lifts as doubles for tasks with scal = 1
+ * (read back by forward tasks with src_prime = -1), hb_ntt_fwd accepts
+ * mode 5 and hb_ks_fused is available.                                       */
 int hb_ntt_fused_ks(const hb_ring* ring);
 /* Launch every library kernel with programmatic dependent launch (PDL:
  * the next kernel's CTAs are scheduled while the previous grid drains; each
@@ -115,7 +122,8 @@ int hb_set_pdl(int on);
 /* Element-wise op `op` over HbEwTask rows: 0 add (ring.py:159), 1 sub
  * (ring.py:167), 2 mul (ring.py:127), 3 scalar mul (ring.py:175), 4 a*b+c
  * (engine.py:202-203), 5 a+b*c (engine.py:204-208), 6 copy, 7 gather,
- * 8 (a-b)*c (ring.py:210).                                                   */
+ * 8 (a-b)*c (ring.py:210), 9 gathered a+b, 10 centre(((a-b)*scal + c) mod p)
+ * on centred-double rows (the top row of a merged ModDown + rescale).        */
 int hb_ew(hb_ring* ring, int op, const void* tasks, int count, void* stream);
 /* Many-term sums dst = sum_k srcs[term_off + k] (mod p) over HbMacTask rows
  * (the add chains of sum_each: hear/fastpath.py rotate-and-sum and FC
