@@ -198,7 +198,10 @@ int hb_rot_sum(hb_ring* ring, const void* tasks, int ntasks, const void* rots, i
  * == 1 only.                                                                 */
 int hb_ks_fused(hb_ring* ring, const void* tasks, int count, void* stream);
 /* Key-switch inner product, one task per (job, output row), nb clips per task
- * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).         */
+ * (ring.py:136-156 pw_mul_accum_perm, key rows shared across clips).  fp64
+ * rings: a task with scat != 0 stores its sums through that scatter map and
+ * adds pmod * c0 to the b component -- the rotation left in the extended
+ * basis (lazy ModDown at batches below the GEMM's).                          */
 int hb_ks_inner2(hb_ring* ring, const void* tasks, int count, int nb, void* stream);
 /* Fast RNS base conversion, one task per (polynomial, source basis):
  * dst_t = sum_i [src_i * qhat_i^-1]_{q_i} * (qhat_i mod p_t) mod p_t
