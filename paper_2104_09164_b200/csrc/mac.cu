@@ -147,28 +147,52 @@ k_mac_pipe(HbMacGroupP g, HbRing RG, int R, int BC, int JCrt) {
   const bool c0term = EPI && !last && g.c0 != nullptr;
   const int TT = T + (c0term ? 1 : 0);
   const int Q = TT * JC;
-  // copy plan: chunk c -> stage row c/16 (ct rows first), 16-byte part c%16
+  // copy plan: chunk c -> stage row c/16 (ct rows first), 16-byte part c%16.
+  // Everything but the term's base pointer is fixed per thread: the stage
+  // offset, the pointer-table slot and the element offset of each of the
+  // thread's copies are computed once (recomputing them cost ~20 of the
+  // ~140 instructions a thread issues per term of the split-sum MAC)
+  constexpr int NCP = (CHUNKS + NT - 1) / NT;
+  uint32_t cp_soff[NCP];
+  int cp_slot[NCP], cp_b[NCP];
+  size_t cp_goff[NCP];
+#pragma unroll
+  for (int k = 0; k < NCP; ++k) {
+    const int c = tid + k * NT;
+    const int row = c >> 4, part = c & 15;
+    cp_soff[k] = (uint32_t)(row * 32 + part * 2) * 8u;
+    if (c >= CHUNKS) {
+      cp_slot[k] = -1;
+      cp_b[k] = 0;
+      cp_goff[k] = 0;
+    } else if (row < CB) {
+      const int b = bc + row < BC ? bc + row : BC - 1;
+      cp_slot[k] = 0;
+      cp_b[k] = b;
+      cp_goff[k] = (size_t)b * g.ct_bstride + rn + jbase + part * 2;
+    } else {
+      cp_slot[k] = T + (row - CB) * T;
+      cp_b[k] = -1;
+      cp_goff[k] = prn + jbase + part * 2;
+    }
+  }
   auto issue = [&](int q, int ch, int t) {
     const uint32_t sb = s_addr(stages + (q % S) * STAGE);
-    const size_t j0 = jbase + ch * 32;
+    const size_t jo = (size_t)ch * 32;
 #pragma unroll
-    for (int k = 0; k < (CHUNKS + NT - 1) / NT; ++k) {
-      const int c = tid + k * NT;
-      if (c < CHUNKS) {
-        const int row = c >> 4, part = c & 15;
-        const u64* src;
-        if (row < CB) {
-          const int b = bc + row < BC ? bc + row : BC - 1;
-          src = (EPI && t == T) ? g.c0 + (size_t)b * g.c0_bstride + rn + j0 + part * 2
-                                : ptab[t] + (size_t)b * g.ct_bstride + rn + j0 + part * 2;
-        } else {
-          if (EPI && t == T) continue;
-          src = ptab[T + (row - CB) * T + t] + prn + j0 + part * 2;
-        }
-        cp16(sb + (uint32_t)(row * 32 + part * 2) * 8u, src);
+    for (int k = 0; k < NCP; ++k) {
+      if (cp_slot[k] < 0) continue;
+      const u64* src;
+      if (EPI && t == T) {             // the c0 term: ct rows only
+        if (cp_b[k] < 0) continue;
+        src = g.c0 + (size_t)cp_b[k] * g.c0_bstride + rn + jbase + jo + (cp_soff[k] >> 3 & 31);
+      } else {
+        src = ptab[cp_slot[k] + t] + cp_goff[k] + jo;
       }
+      cp16(sb + cp_soff[k], src);
     }
     if (EPI && t == 0) {   // this chunk's scatter indices (4-byte copies)
+      const size_t j0 = jbase + jo;
       const uint32_t sc0 = s_addr(scbuf + (ch & 1) * OB * 32);
       for (int c = tid; c < OB * 32; c += NT) {
         const int o = c >> 5, oo = oc + o < O ? oc + o : O - 1;
