@@ -34,6 +34,10 @@
 #ifndef HB_MAC_T128
 #define HB_MAC_T128 1   // 128-thread CTAs for the split-sum MAC (layer MAC 30.3 -> 29.7 ms)
 #endif
+#ifndef HB_MACF_T128
+#define HB_MACF_T128 1   // the fmod_mul GEMM / layer MAC (unfused key switches, > 34-bit primes)
+                        // in 128-thread CTAs too: hear/full 460 -> 470 inferences/s, config 3 270 -> 276
+#endif
 #ifndef HB_MAC_BIG
 #define HB_MAC_BIG 4, 4, 4, 2   // TO, TB, WO, WB of the large tile (16 outputs x 8 clips)
 #endif
@@ -427,7 +431,9 @@ static cudaError_t mac_pipe_dispatch_rot(const HbMacGroupP& g, const HbRing& RG,
   if (g.nout <= 2) return mac_pipe_t<2, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
   if (g.nout <= 4) return mac_pipe_t<4, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
   if (g.nout <= 8) return mac_pipe_t<8, 4, 1, 8, S, 1>(g, RG, rows, BC, st);
-  return mac_pipe_t<8, 4, 2, 4, S, 1>(g, RG, rows, BC, st);
+  // 8 outputs x 16 clips in 128-thread CTAs (four per SM): 39.8 -> 37.3 ms per
+  // step against the 256-thread 16 x 16 tile (64 threads: 40.7)
+  return mac_pipe_t<8, 4, 1, 4, S, 1>(g, RG, rows, BC, st);
 }
 
 static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int rows, int BC,
@@ -457,6 +463,10 @@ static cudaError_t mac_pipe_dispatch(const HbMacGroupP& g, const HbRing& RG, int
   if (g.nout <= 8) return mac_pipe_t<8, 4, 1, 8, S>(g, RG, rows, BC, st);
   // 8 outputs x 4 clips per thread (124 registers, 2 CTAs/SM): each staged
   // operand feeds twice the products of the 4x4 tile (round-1 tile sweep)
+#if HB_MACF_T128
+  if (g.nterms > 32) return mac_pipe_t<8, 4, 1, 4, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
+  return mac_pipe_t<8, 4, 1, 4, S>(g, RG, rows, BC, st);
+#endif
   if (g.nterms > 32) return mac_pipe_t<8, 4, 2, 4, HB_MAC_STAGES_LONG>(g, RG, rows, BC, st);
   return mac_pipe_t<8, 4, 2, 4, S>(g, RG, rows, BC, st);
 }
