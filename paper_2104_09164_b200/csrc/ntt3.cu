@@ -342,7 +342,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) rb[bsw(blk * 128 + u * 8 + cc)] = x[u];
   }
-  __syncthreads();
+  __syncwarp();   // the fine stages below read this warp's four blocks only
   const size_t base = (size_t)rank * TILE3;
   constexpr int N8 = N / 8;
   const HbTwD* t3 = R.tw3_fwd + (size_t)tk.dst_prime * N;
@@ -354,8 +354,10 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   };
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int g2 = t + q * THREADS3;          // 512 groups of 8
-    const int b2 = g2 >> 4, G8 = g2 & 15;
+    // 512 groups of 8; a warp takes the groups of the four blocks its
+    // stride-8 pass owns (blk = t >> 3), so the two passes hand over inside
+    // the warp (__syncwarp, no CTA barrier)
+    const int b2 = 4 * (t >> 5) + 2 * q + ((t & 31) >> 4), G8 = t & 15;
     const int e0 = b2 * 128 + G8 * 8;
     V x[8];
 #pragma unroll
@@ -519,8 +521,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
   };
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int g2 = t + q * THREADS3;
-    const int b2 = g2 >> 4, G8 = g2 & 15;
+    const int b2 = 4 * (t >> 5) + 2 * q + ((t & 31) >> 4), G8 = t & 15;   // warp-local, see k_ntt3_fwd
     const int e0 = b2 * 128 + G8 * 8;
     V x[8];
 #pragma unroll
@@ -541,7 +542,7 @@ k_ntt3_inv(const HbNttTask* __restrict__ tasks, HbRing R) {
       sm[2 * pc + 1] = pol.inv_round_end(x[2 * v + 1]);
     }
   }
-  __syncthreads();
+  __syncwarp();   // the stride-8 stages below read this warp's four blocks only
   {
     const int blk = t >> 3, cc = t & 7;
     V x[16];
@@ -800,11 +801,10 @@ k_ks3(const HbKsfTask* __restrict__ tasks, HbRing R) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) rb[bsw(blk * 128 + u * 8 + cc)] = x[u];
       }
-      __syncthreads();
+      __syncwarp();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int g2 = t + q * THREADS3;
-        const int b2 = g2 >> 4, G8 = g2 & 15;
+        const int b2 = 4 * (t >> 5) + 2 * q + ((t & 31) >> 4), G8 = t & 15;   // warp-local
         const int e0 = b2 * 128 + G8 * 8;
         V x[8];
 #pragma unroll
