@@ -379,7 +379,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
       }
     }
   }
-  __syncthreads();
+  __syncwarp();   // the epilogue below stays on this warp's four blocks (512 elements)
   // ---- epilogue on 16-byte chunks, lanes contiguous (coalesced HBM traffic).
   // ModDown on the fp64 pipe: (x_r - y) * P^-1 (+ addend) from the balanced
   // transform output y, one canonicalisation (the integer sub/Shoup/add
@@ -388,7 +388,7 @@ k_ntt3_fwd(const HbNttTask* __restrict__ tasks, HbRing R) {
   const double sd = u64_to_f(tk.scal), sq = sd * pinv;
 #pragma unroll 4
   for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-    const int k = t + i * THREADS3;
+    const int k = (t >> 5) * (TILE3 / 2 / 8) + i * 32 + (t & 31);   // warp w: chunks [256w, 256w + 256)
     const size_t j = base + 2 * k;
     const int pc = swz3_chunk(k);
     ulonglong2 o;
@@ -821,13 +821,13 @@ k_ks3(const HbKsfTask* __restrict__ tasks, HbRing R) {
           rb[2 * pc + 1] = x[2 * v + 1];
         }
       }
-      __syncthreads();
+      __syncwarp();   // the accumulate loop stays on this warp's four blocks
     }
     // ---- accumulate x * key into the thread's TMEM columns; after the last
     // digit canonicalise and store instead
 #pragma unroll KS3_UNROLL
     for (int i = 0; i < TILE3 / 2 / THREADS3; ++i) {
-      const int k = t + i * THREADS3;
+      const int k = (t >> 5) * (TILE3 / 2 / 8) + i * 32 + (t & 31);   // warp-local chunks
       const size_t j = 2 * (size_t)k;
       double x0, x1;
       if (ident) {
